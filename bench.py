@@ -1,0 +1,399 @@
+"""Benchmark: rank-2000 dense MTTKRP over all modes (BASELINE config 4) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+One step = the MTTKRP of every mode (0, 1, 2) of the 1024^3 float64 tensor
+against rank-2000 factors (the north star's headline case).  `value` is
+algorithmic GFLOP/s, 2 N R (d-1) flops per mode (BASELINE.json's roofline
+numerator), with inputs resident in HBM; the 8 GiB tensor is 65x the L2, so
+no flush is needed between steps.  `e2e` is the same metric through the
+public API from pinned HOST buffers, H2D of tensor + factors and D2H of the
+three results inside the timed region.  Multi-GPU (torchrun): the tensor is
+block-partitioned along mode 0; mode 0 needs no communication, modes 1 and 2
+allreduce their I_k x R partials over NCCL (strong scaling, fixed tensor).
+
+`--impl reference` times the CPU restatement of the reference TILE kernel
+(oracle/, C + OpenMP, all host threads) on a bounded slab of the same
+workload; only rank 0 runs it.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "dense MTTKRP GFLOP/s & roofline fraction vs rank R; CP-ALS sec/iter at 1/2/4/8 GPU"
+DIMS = (1024, 1024, 1024)
+RANK = 2000
+SEED = 0
+PEAKS_FILE = ROOT / "MEASURED_PEAKS.json"
+NCU_SUMMARY = ROOT / "profiles" / "ncu_summary.json"
+
+
+def algo_flops(dims, rank):
+    n = int(np.prod(dims))
+    return 2 * n * rank * (len(dims) - 1)
+
+
+def env_rank():
+    return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("LOCAL_RANK", "0"))
+
+
+# --------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits"],
+                    capture_output=True, text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if len(s) > 4 + i and s[4 + i] == "Active"})
+        power = [float(s[2]) for s in self.samples if s[2].replace(".", "").isdigit()]
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples),
+                "power_w_median": statistics.median(power) if power else None}
+
+
+# ------------------------------------------------------------ reference (CPU)
+def cpu_sample(target_seconds: float, threads: int = 0):
+    """Time the oracle TILE port (C + OpenMP) on a slab of config 4.
+
+    The slab keeps I_0 = I_1 = 1024 and R = 2000 and cuts mode 2 to `depth`
+    slices; all three modes are run, like one GPU step.  N_T follows the
+    reference's Eq. 6 heuristic with its intel-8480p spec (w = 362 -> N_T =
+    131044, clamped per mode), unroll F = 16.
+    """
+    from oracle import gen, oracle
+
+    fs = gen.bench_factors(DIMS, RANK, SEED)
+    w = oracle.max_threads() if threads <= 0 else threads
+
+    def run(depth):
+        dims = (DIMS[0], DIMS[1], depth)
+        y = gen.splitmix_uniform(int(np.prod(dims)), SEED)
+        sub = [fs[0], fs[1], fs[2][:depth]]
+        t0 = time.perf_counter()
+        for k in range(3):
+            oracle.mttkrp_tile(y, dims, k, sub, None, f_cols=16, n_t=131044, workers=w)
+        return time.perf_counter() - t0, algo_flops(dims, RANK) * 3
+
+    # calibrate on one slice, then size the sample to ~target_seconds
+    t1, f1 = run(1)
+    depth = max(1, min(DIMS[2], int(target_seconds / max(t1, 1e-3))))
+    if depth == 1:
+        t, f = t1, f1
+    else:
+        t, f = run(depth)
+    return {"seconds": t, "flops": f, "depth": depth, "threads": w}
+
+
+def run_reference(args):
+    rank, world, _ = env_rank()
+    if rank != 0:
+        return
+    budget = max(2.0, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
+    for _ in range(args.warmup):
+        cpu_sample(budget / 4)
+    vals, secs = [], []
+    depth = None
+    threads = None
+    for _ in range(args.steps):
+        s = cpu_sample(budget)
+        vals.append(s["flops"] / s["seconds"] / 1e9)
+        secs.append(s["seconds"])
+        depth, threads = s["depth"], s["threads"]
+    value = statistics.median(vals)
+    sample = f"slab 1024x1024x{depth} of config 4 (R=2000), all 3 modes, TILE N_T=131044 F=16"
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.median(secs),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (splitmix64 counter-based U[0,1) tensor, Philox(1) factors)",
+        "config": {"workload": "c4: 3-way 1024^3 f64 tensor, rank 2000, MTTKRP all modes (CPU slab sample)",
+                   "dims": list(DIMS), "rank": RANK, "sample": sample},
+        "cpu_baseline": {"value": value, "unit": "GFLOP/s", "cores": threads, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------- GPU path
+def shard_rows(n, world, rank):
+    base, rem = divmod(n, world)
+    lo = rank * base + min(rank, rem)
+    return lo, lo + base + (1 if rank < rem else 0)
+
+
+def run_b200(args):
+    import torch
+
+    rank, world, local = env_rank()
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.device("cuda", torch.cuda.current_device())
+
+    import paper_2510_14891_b200 as ck
+    from paper_2510_14891_b200 import _lib
+    from paper_2510_14891_b200.mttkrp import MttkrpPlan, Variant, mttkrp_device
+    from oracle import gen
+
+    # ---- inputs resident in HBM: this rank's mode-0 slab of config 4
+    lo, hi = shard_rows(DIMS[0], world, rank)
+    local_dims = (hi - lo, DIMS[1], DIMS[2])
+    n_local = int(np.prod(local_dims))
+    lib = _lib.load()
+    # element (i0, i1, i2) of the global tensor is splitmix(i0 + 1024 i1 + 1024^2 i2)
+    full = torch.empty(int(np.prod(DIMS)), dtype=torch.float64, device=dev)
+    _lib.check(lib.cpk_fill_uniform_f64(full.data_ptr(), full.numel(), SEED, 0,
+                                        torch.cuda.current_stream().cuda_stream), "fill")
+    if world == 1:
+        y = full
+    else:
+        y = full.view(DIMS[2] * DIMS[1], DIMS[0])[:, lo:hi].contiguous().view(-1)
+        del full
+    fs_host = gen.bench_factors(DIMS, RANK, SEED)
+    fs_host[0] = np.ascontiguousarray(fs_host[0][lo:hi])
+    fs = [torch.from_numpy(a).to(dev) for a in fs_host]
+    torch.cuda.synchronize()
+
+    def step(events=None):
+        outs = []
+        for k in range(3):
+            if events is not None:
+                events[k][0].record()
+            g, _, _ = mttkrp_device(y, local_dims, fs, k, None, MttkrpPlan(Variant.B200, k))
+            if events is not None:
+                events[k][1].record()
+            if world > 1 and k != 0:
+                dist.all_reduce(g)
+            outs.append(g)
+        return outs
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+
+    mode_events = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(3)]
+                   for _ in range(args.steps)]
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(dev.index) as clocks:
+        barrier()
+        t0.record()
+        for s in range(args.steps):
+            step(mode_events[s])
+        t1.record()
+        barrier()
+    elapsed = t0.elapsed_time(t1) * 1e-3
+    if world > 1:
+        tt = torch.tensor([elapsed], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        elapsed = float(tt.item())
+    per_mode = [statistics.median(mode_events[s][k][0].elapsed_time(mode_events[s][k][1]) for s in range(args.steps))
+                for k in range(3)]
+
+    total_flops = algo_flops(DIMS, RANK) * 3 * args.steps
+    value = total_flops / elapsed / 1e9
+
+    # ---- e2e through the public API from pinned host buffers (N=1 only: the
+    # per-rank host slab at N>1 is the same code path)
+    e2e = None
+    if args.e2e_steps > 0:
+        y_host = torch.empty(n_local, dtype=torch.float64, pin_memory=True)
+        y_host.copy_(y)
+        fs_pinned = [torch.from_numpy(a).pin_memory() for a in fs_host]
+        h2d = 8 * n_local + sum(8 * a.size for a in fs_host)
+        d2h = 8 * RANK * sum(local_dims) if world == 1 else 8 * RANK * (local_dims[0] + DIMS[1] + DIMS[2])
+
+        def e2e_step():
+            yd = y_host.to(dev, non_blocking=True)
+            fd = [a.to(dev, non_blocking=True) for a in fs_pinned]
+            res = []
+            for k in range(3):
+                g = ck.mttkrp(yd, fd, k)
+                if world > 1 and k != 0:
+                    dist.all_reduce(g)
+                res.append(g.to("cpu", non_blocking=True))
+            torch.cuda.synchronize()
+            return res
+
+        e2e_step()
+        barrier()
+        te = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            e2e_step()
+        barrier()
+        e2e_t = time.perf_counter() - te
+        if world > 1:
+            tt = torch.tensor([e2e_t], dtype=torch.float64, device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            e2e_t = float(tt.item())
+        e2e = {"value": algo_flops(DIMS, RANK) * 3 * args.e2e_steps / e2e_t / 1e9, "unit": "GFLOP/s",
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "steps": args.e2e_steps,
+               "ms_per_step": 1e3 * e2e_t / args.e2e_steps}
+        del y_host
+
+    # ---- roofline of the dominant kernel (mttkrp_f64_sm100, per launch)
+    fp64_peak = None
+    if rank == 0:
+        pk = (_lib.C.c_double(0), _lib.C.c_double(0))
+        _lib.check(lib.cpk_fp64_peak_probe(_lib.C.byref(pk[0]), _lib.C.byref(pk[1])), "probe")
+        fp64_peak = pk[0].value
+    nominal = 148 * 64 * 2 * 1.965e9
+    flops_per_launch = algo_flops(local_dims, RANK)  # one mode
+    mean_launch_s = statistics.mean(per_mode) * 1e-3
+    achieved = flops_per_launch / mean_launch_s
+    traffic = None
+    if NCU_SUMMARY.exists():
+        try:
+            traffic = json.loads(NCU_SUMMARY.read_text()).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    cp = None
+    if args.cpals_iters > 0 and world == 1:
+        cp = bench_cpals(ck, dev, args.cpals_iters)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        s = cpu_sample(args.cpu_seconds)
+        cpu = {"value": s["flops"] / s["seconds"] / 1e9, "unit": "GFLOP/s", "cores": s["threads"], "kind": "port",
+               "sample": f"oracle TILE port (C+OpenMP) on slab 1024x1024x{s['depth']} of config 4, R=2000, "
+                         f"all 3 modes, N_T=131044 F=16, {s['seconds']:.1f} s"}
+
+    if rank == 0:
+        hbm = 6508.2e9
+        try:
+            hbm = json.loads(PEAKS_FILE.read_text())["hbm_gbs"] * 1e9
+        except Exception:
+            pass
+        peak = fp64_peak or nominal
+        roof_t = max(8 * int(np.prod(DIMS)) / hbm, algo_flops(DIMS, RANK) / peak)
+        line = {
+            "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * elapsed / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (splitmix64 counter-based U[0,1) tensor generated on device, Philox(1) factors)",
+            "config": {"workload": "c4: 3-way 1024x1024x1024 f64 tensor, rank 2000, MTTKRP of all 3 modes per step",
+                       "dims": list(DIMS), "rank": RANK, "parallelism": f"mode-0 block partition x{world}",
+                       "l2": "inputs 8 GiB >> 126 MB L2; no flush needed"},
+            "per_mode_ms": per_mode,
+            "paper_gflops": int(np.prod(DIMS)) * RANK * 3 * 3 * args.steps / elapsed / 1024 ** 3,
+            "roofline": {"bound": "fp64", "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "TFLOP/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "peak_source": "cpk_fp64_peak_probe (register DFMA loop, this run)" if fp64_peak else
+                         "nominal 148 SM x 64 DFMA/clk x 2 x 1.965 GHz",
+                         "nominal_peak": nominal / 1e12,
+                         "kernel": "mttkrp_f64_sm100 + splitk_reduce_f64 (per mode launch)",
+                         "flops_per_launch": flops_per_launch,
+                         "issued_dfma_frac": (int(np.prod(local_dims)) * 2 * 2048 / mean_launch_s) / peak,
+                         "north_star_roofline_ms_per_mode": roof_t * 1e3,
+                         "north_star_frac": roof_t * 3 * args.steps / elapsed},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": 6 * args.steps,
+            "clocks": clocks.summary(),
+        }
+        if cp:
+            line["cp_als"] = cp
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def bench_cpals(ck, dev, iters):
+    """CP-ALS seconds per sweep at config 3 (128^4, R=256)."""
+    import torch
+
+    dims = (128, 128, 128, 128)
+    t = ck.DenseTensor.uniform(dims, seed=SEED, device=dev)
+    ck.cp_als(t, ck.AlsConfig(rank=256, tol=0.0, max_iters=1, seed=0))  # warm-up
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    _, tr = ck.cp_als(t, ck.AlsConfig(rank=256, tol=0.0, max_iters=iters, seed=0))
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    mt = sum(sum(s) for s in tr.mttkrp_seconds) / iters
+    return {"config": "c3: 4-way 128^4 f64, rank 256", "iters": iters, "sec_per_iter": dt / iters,
+            "mttkrp_sec_per_iter": mt, "other_sec_per_iter": sum(tr.other_seconds) / iters,
+            "fit_last": tr.fits[-1]}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--cpals-iters", type=int, default=5)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "b200":
+        print("warning: fewer than 3 warm-up steps", file=sys.stderr)
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,165 @@
+/*
+ * cpk_b200.h -- C ABI of the B200-native matrix-free dense MTTKRP and the
+ * CP-ALS step kernels that sit behind it.
+ *
+ * The reference package (`cpkern`, Python + numba, /root/reference/pkg) has no
+ * C interface; its "FFI" into compiled code is the numba kernel signature
+ *
+ *     tile_kernel(data f64[N], dims i64[d], strides i64[d], k,
+ *                 fm f64[], foff i64[d], lam f64[R], r, f_cols, n_t, gp)
+ *                                      (pkg/src/cpkern/_kernels.py:162-174)
+ *
+ * i.e. flat buffers, int64 metadata and a caller-owned output.  The entry
+ * points below keep that shape with DEVICE pointers: the tensor is one flat
+ * float64 buffer in first-mode-fastest order (dtensor.py:3-7), factors are
+ * row-major float64 (kruskal.py:18-22, one device pointer per mode instead of
+ * the packed `fm`/`foff` pair, _kernels.py:25-36), weights are folded exactly
+ * once (README.md:155-156), and the result is the I_k x R row-major matrix
+ * (mttkrp.py:114-117).  Every call is stream-ordered and asynchronous on the
+ * caller's cudaStream_t (passed as void*), never allocates on the hot path
+ * (the split-K workspace is caller-provided), and returns a status code that
+ * maps 1:1 onto the reference's exception classes (errors.py:4-25).
+ *
+ * No torch types cross this boundary.  Python binds it with ctypes
+ * (paper_2510_14891_b200/_lib.py); INTEGRATION.md shows the binding.
+ */
+#ifndef CPK_B200_H
+#define CPK_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes.  errors.py:4-25: CpkernError > {ShapeError, IndexRangeError,
+ * ParameterError, ResourceError, FormatError}; CUDA and NCCL failures are new
+ * (the reference has no device) and surface as CpkernError subclasses. */
+enum {
+  CPK_OK = 0,
+  CPK_ERR_SHAPE = 1,     /* ShapeError      (mttkrp.py:294-296)          */
+  CPK_ERR_INDEX = 2,     /* IndexRangeError (mttkrp.py:297-298, 248-249) */
+  CPK_ERR_PARAM = 3,     /* ParameterError  (mttkrp.py:250-263)          */
+  CPK_ERR_RESOURCE = 4,  /* ResourceError   (workspace too small)        */
+  CPK_ERR_CUDA = 5,      /* launch / runtime failure                     */
+  CPK_ERR_NOT_PD = 6,    /* Cholesky failed: Gamma not positive definite */
+  CPK_ERR_LIB = 7        /* cuSOLVER failure                             */
+};
+
+#define CPK_MAX_MODES 8
+
+/* Kernel knobs.  Mirrors MttkrpPlan (mttkrp.py:227-263): `unroll` (F) and
+ * `tile_volume` (N_T) keep their meaning; `rank_tile` is the GPU rank tile
+ * (the paper's F*b_y column block); `splits` is the number of CTAs sharing
+ * one output tile along the contraction (the reference's tiles-per-slice,
+ * mttkrp.py:528-529).  Zero in any field means "choose" (cpk_plan_resolve). */
+typedef struct cpk_plan {
+  int32_t rank_tile;    /* 0 | 32 | 64 | 128                          */
+  int32_t block_rows;   /* 0 | 64 | 128 (mode-k rows per CTA)          */
+  int64_t tile_volume;  /* in-slice elements per CTA work item, 0=auto */
+  int32_t splits;       /* split-K factor, 0 = derive from tile_volume */
+  int32_t sm_count;     /* 0 = query the device                        */
+} cpk_plan;
+
+/* Last error message of the calling thread (never NULL). */
+const char* cpk_last_error(void);
+/* Library version string. */
+const char* cpk_version(void);
+
+/* Fill every zero field of *plan for this problem; validates the problem.
+ * Replaces the CPU worker-pool / tile-volume resolution of
+ * mttkrp.py:301-318 and plan_for_mode's clamp (mttkrp.py:568-575). */
+int cpk_plan_resolve(int d, const int64_t* dims, int mode, int64_t rank,
+                     cpk_plan* plan);
+
+/* Bytes of split-K workspace the resolved plan needs (0 when splits == 1). */
+int cpk_mttkrp_workspace_bytes(int d, const int64_t* dims, int mode,
+                               int64_t rank, const cpk_plan* plan,
+                               size_t* bytes);
+
+/*
+ * G = Y_(mode) (A_{d-1} (.) ... (.) A_{mode+1} (.) A_{mode-1} (.) ... (.) A_0) diag(lam)
+ *
+ * Replaces mttkrp_tile / tile_kernel (mttkrp.py:519-549, _kernels.py:96-174)
+ * and, with splits == 1, mttkrp_slice (mttkrp.py:491-516).
+ *   y        device, N = prod(dims) float64, first mode fastest
+ *   factors  host array of d device pointers; factors[m] is dims[m] x ld[m]
+ *            row-major (ld[m] >= rank); factors[mode] is not read
+ *   ld       host array of d leading dimensions (NULL = rank for all)
+ *   lam      device, rank float64, or NULL for unit weights
+ *   G        device, dims[mode] x ldg row-major (ldg >= rank)
+ *   workspace device scratch of cpk_mttkrp_workspace_bytes (may be NULL if 0)
+ *   stream   cudaStream_t (NULL = legacy default stream)
+ */
+int cpk_mttkrp_f64(const double* y, int d, const int64_t* dims, int mode,
+                   const double* const* factors, const int64_t* ld,
+                   const double* lam, int64_t rank, double* G, int64_t ldg,
+                   const cpk_plan* plan, void* workspace, size_t ws_bytes,
+                   void* stream);
+
+/* Gram matrix A^T A (R x R), symmetrized exactly: upper triangle computed,
+ * lower mirrored -- kruskal.gram (kruskal.py:110-114). */
+int cpk_gram_f64(const double* A, int64_t rows, int64_t rank, int64_t lda,
+                 double* gram, void* stream);
+
+/* out = (*) of grams[m] over m != skip (skip < 0: all), elementwise, in
+ * ascending m order starting from ones -- cpals.py:129-132 and the fit's H
+ * (cpals.py:143-145); kruskal.hadamard_gram (kruskal.py:74-83). */
+int cpk_hadamard_f64(const double* const* grams, int n, int skip,
+                     int64_t rank, double* out, void* stream);
+
+/* Solve X Gamma = G in place (G is rows x rank row-major, Gamma rank x rank
+ * SPD) with the regularization ladder of cpals._solve_normal
+ * (cpals.py:75-89): Cholesky; on failure Gamma + eps tr(Gamma)/R I with
+ * eps = 1e-12, x1e3, up to 5 tries.  `work` is caller scratch of
+ * cpk_solve_workspace_bytes.  Returns CPK_ERR_NOT_PD if every rung fails
+ * (the caller then takes the least-squares path). Synchronizes the stream
+ * only to read the Cholesky info flag. */
+int cpk_solve_workspace_bytes(int64_t rows, int64_t rank, size_t* bytes);
+int cpk_solve_normal_f64(const double* gamma, double* G, int64_t rows,
+                         int64_t rank, void* work, size_t work_bytes,
+                         void* stream);
+
+/* Column 2-norms of A (rows x rank), A[:, nz] /= nrm, lam = where(nz, nrm, 0)
+ * -- cpals.py:134-137.  Split in two so the sharded driver can allreduce the
+ * squared norms of a row-partitioned factor in between:
+ *   cpk_colnorms_sq_f64:  normsq[j] = sum_i A[i, j]^2 (deterministic order)
+ *   cpk_scale_columns_f64: nrm = sqrt(normsq); A[:, nrm > 0] /= nrm; lam = nrm */
+int cpk_colnorms_sq_f64(const double* A, int64_t rows, int64_t rank,
+                        int64_t lda, double* normsq, void* stream);
+int cpk_scale_columns_f64(double* A, int64_t rows, int64_t rank, int64_t lda,
+                          const double* normsq, double* lam, void* stream);
+int cpk_normalize_columns_f64(double* A, int64_t rows, int64_t rank,
+                              int64_t lda, double* lam, double* normsq_work,
+                              void* stream);
+
+/* Fit terms (cpals.py:143-150): out[0] = lam^T H lam, out[1] =
+ * sum((G * lam) * A), both as device scalars. */
+int cpk_fit_terms_f64(const double* H, const double* lam, const double* G,
+                      const double* A, int64_t rows, int64_t rank,
+                      double* out2, void* stream);
+
+/* Sum of squares of a flat device vector (for ||Y||^2), deterministic:
+ * `work` holds CPK_SUMSQ_PARTIALS doubles of block partials. */
+#define CPK_SUMSQ_PARTIALS 1024
+int cpk_sumsq_f64(const double* x, int64_t n, double* work, double* out,
+                  void* stream);
+
+/* Fill x[i] = U[0,1) from the counter-based generator
+ * u = (splitmix64(seed * 2^32 + offset + i) >> 11) * 2^-53, used to create
+ * BASELINE tensors too large to stage through the host.  The CPU twin is
+ * oracle/gen.py:splitmix_uniform. */
+int cpk_fill_uniform_f64(double* x, int64_t n, uint64_t seed, int64_t offset,
+                         void* stream);
+
+/* Device-side DFMA throughput probe: returns achieved FP64 FLOP/s of a
+ * register-resident FMA loop over the whole chip (the FP64 roofline peak;
+ * MEASURED_PEAKS.json has no FP64 figure).  Synchronous. */
+int cpk_fp64_peak_probe(double* flops_per_s, double* seconds);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CPK_B200_H */

@@ -1,0 +1,110 @@
+// Status plumbing, the synthetic-tensor generator and the FP64 peak probe.
+#include "common.cuh"
+
+#include <string.h>
+#include <algorithm>
+
+namespace cpk {
+
+static thread_local char g_err[512] = "";
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+int fail(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+// splitmix64 finalizer (Steele, Lea, Flood 2014); CPU twin: oracle/gen.py.
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+__global__ void fill_uniform_kernel(double* __restrict__ x, int64_t n, uint64_t key, int64_t offset) {
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += stride) {
+    const uint64_t c = uint64_t(offset + i);
+    const uint64_t z = mix64(key + (c + 1) * 0x9E3779B97F4A7C15ull);
+    x[i] = double(z >> 11) * 0x1.0p-53;
+  }
+}
+
+// Independent DFMA chains, register resident: the FP64 pipe ceiling.
+constexpr int PROBE_CHAINS = 16;
+__global__ void __launch_bounds__(256) dfma_probe_kernel(double* out, int iters, double b, double c) {
+  double a[PROBE_CHAINS];
+#pragma unroll
+  for (int i = 0; i < PROBE_CHAINS; ++i) a[i] = 1e-3 * (threadIdx.x + i);
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < PROBE_CHAINS; ++i) a[i] = fma(a[i], b, c);
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int i = 0; i < PROBE_CHAINS; ++i) s += a[i];
+  if (s == 12345.678) out[0] = s;  // keep the chains alive
+}
+
+}  // namespace cpk
+
+using namespace cpk;
+
+extern "C" const char* cpk_last_error(void) { return g_err; }
+
+extern "C" const char* cpk_version(void) { return "cpk_b200 0.1.0 sm_100a"; }
+
+extern "C" int cpk_fill_uniform_f64(double* x, int64_t n, uint64_t seed, int64_t offset, void* stream) {
+  if (n < 0 || offset < 0) return fail(CPK_ERR_PARAM, "negative length or offset");
+  if (n == 0) return CPK_OK;
+  if (!x) return fail(CPK_ERR_PARAM, "x is NULL");
+  // key = mix64(seed): decorrelates neighbouring seeds
+  uint64_t z = seed * 0x9E3779B97F4A7C15ull + 0x632BE59BD9B4E019ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  const uint64_t key = z ^ (z >> 31);
+  const int64_t blocks = std::min<int64_t>((n + 255) / 256, 148 * 32);
+  fill_uniform_kernel<<<unsigned(blocks), 256, 0, as_stream(stream)>>>(x, n, key, offset);
+  return check_launch("fill_uniform");
+}
+
+extern "C" int cpk_fp64_peak_probe(double* flops_per_s, double* seconds) {
+  int dev = 0, sms = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+    return fail(CPK_ERR_CUDA, "device query failed");
+  double* out = nullptr;
+  if (cudaMalloc(&out, sizeof(double)) != cudaSuccess) return fail(CPK_ERR_CUDA, "cudaMalloc");
+  const int blocks = sms * 8, threads = 256, iters = 1 << 14;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  dfma_probe_kernel<<<blocks, threads>>>(out, 256, 1.0000001, 1e-9);  // warm-up
+  float best = 1e30f;
+  for (int rep = 0; rep < 5; ++rep) {
+    cudaEventRecord(e0);
+    dfma_probe_kernel<<<blocks, threads>>>(out, iters, 1.0000001, 1e-9);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    best = std::min(best, ms);
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(out);
+  int rc = check_launch("dfma_probe");
+  if (rc) return rc;
+  const double flops = 2.0 * PROBE_CHAINS * double(iters) * double(blocks) * threads;
+  if (seconds) *seconds = best * 1e-3;
+  if (flops_per_s) *flops_per_s = flops / (best * 1e-3);
+  return CPK_OK;
+}

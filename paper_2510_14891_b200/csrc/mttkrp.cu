@@ -1,0 +1,669 @@
+// Matrix-free dense MTTKRP for B200 (sm_100a), FP64 on the CUDA-core DFMA pipe.
+//
+// What it computes (reference: mttkrp_tile / tile_kernel / accum_tile,
+// pkg/src/cpkern/mttkrp.py:519-549 and _kernels.py:96-174):
+//
+//     G[n, j] = lam[j] * sum_{i : i_k = n} y[i] * prod_{m != k} A_m[i_m, j]
+//
+// B200 design.  The contraction over the N_S in-slice elements of every
+// mode-k slice is run as an on-the-fly GEMM
+//
+//     G (I_k x R) = Y_(k) (I_k x N_S) . Z (N_S x R),   Z = Khatri-Rao rows
+//
+// without ever materializing Z.  The in-slice elements are walked in the
+// reference's own first-mode-fastest order and cut into *chunks*: BK
+// consecutive values of the fastest non-k mode f, with every other non-k
+// index ("o" modes) fixed.  For one chunk the Khatri-Rao rows are
+//
+//     Z[c, j] = A_f[i_f0 + c, j] * P_o[j],   P_o[j] = prod_{m in o} A_m[o_m, j]
+//
+// so one chunk needs BK factor rows of A_f plus one row per o-mode.  They are
+// staged with cp.async into shared memory next to the BM x BK tensor tile and
+// each thread scales its own B-tile chunks by P_o in place (the Khatri-Rao row
+// is formed once per CTA per chunk, amortized over BM output rows).  The math
+// is a register-tiled DFMA outer product: 8x8 accumulators per thread, operand
+// fragments read with 128-bit LDS in broadcast-friendly layouts.
+//
+//   * mode 0     : tensor tile is "M-major" (the mode-0 index n is contiguous),
+//                  staged as As[k][m]
+//   * mode k > 0 : tensor tile is "K-major" (the contraction index i_0 is
+//                  contiguous), staged as As[m][k] with a 2-double row pad
+//                  so the 8 row reads of a warp hit distinct banks
+//
+// Parallelism: grid = (rank tiles, row tiles, splits).  Rank tiles are the
+// fastest grid index so the CTAs that share one tensor tile run together and
+// the tile is read from HBM once and from L2 R/BN times.  `splits` cuts the
+// chunk sequence (the reference's tiles-per-slice, mttkrp.py:528-529) into
+// contiguous ranges; partials land in a [splits, I_k, R] workspace that one
+// deterministic kernel sums in split order -- no floating-point atomics, so
+// results are bit-reproducible run to run.
+#include "common.cuh"
+
+#include <algorithm>
+#include <mutex>
+
+namespace cpk {
+
+constexpr int KPAD = 2;  // K-major As row pad (doubles)
+
+struct MttkrpParams {
+  const double* y;
+  const double* fac_f;
+  const double* fac_o[CPK_MAX_MODES];
+  int64_t ld_f;
+  int64_t ld_o[CPK_MAX_MODES];
+  int64_t dim_o[CPK_MAX_MODES];
+  int64_t stride_o[CPK_MAX_MODES];
+  int64_t Ik, stride_k;
+  int64_t If, stride_f;
+  int64_t chunks_per_f;      // ceil(If / BK)
+  int64_t n_chunks;          // chunks_per_f * prod(dim_o)
+  int64_t chunks_per_split;
+  int64_t R;
+  double* out;
+  int64_t ldo;
+  int64_t out_split_stride;
+  const double* lam;         // folded in the epilogue only when direct
+};
+
+// Loader state: the chunk being staged next, as an odometer over
+// (q_f, o digits) -- the in-slice walk of accum_tile (_kernels.py:135-147),
+// advanced one chunk per pipeline stage without any div/mod.
+template <int NO>
+struct ChunkCursor {
+  int64_t qf;
+  int64_t od[NO > 0 ? NO : 1];
+  int64_t base;  // sum od[i] * stride_o[i]
+
+  __device__ void init(const MttkrpParams& p, int64_t q) {
+    qf = q % p.chunks_per_f;
+    int64_t rest = q / p.chunks_per_f;
+    base = 0;
+#pragma unroll
+    for (int i = 0; i < NO; ++i) {
+      od[i] = rest % p.dim_o[i];
+      rest /= p.dim_o[i];
+      base += od[i] * p.stride_o[i];
+    }
+  }
+  __device__ void advance(const MttkrpParams& p) {
+    if (++qf < p.chunks_per_f) return;
+    qf = 0;
+#pragma unroll
+    for (int i = 0; i < NO; ++i) {
+      base += p.stride_o[i];
+      if (++od[i] < p.dim_o[i]) return;
+      base -= od[i] * p.stride_o[i];
+      od[i] = 0;
+    }
+  }
+};
+
+template <int BM, int BN, int BK, bool KMAJ, int VEC, int STAGES, int NO>
+struct TileCfg {
+  static constexpr int TY = BM / 8, TX = BN / 8, NT = TY * TX;
+  static constexpr int WX = TX < 8 ? TX : 8, WY = 32 / WX;
+  static constexpr int APITCH = KMAJ ? (BK + KPAD) : BM;
+  static constexpr int A_ELEMS = KMAJ ? BM * (BK + KPAD) : BK * BM;
+  static constexpr int B_ELEMS = BK * BN;
+  static constexpr int P_ELEMS = NO * NT * VEC;
+  static constexpr int CPA = KMAJ ? BK / VEC : BM / VEC;  // A chunks per staged row
+  static constexpr int NA = BM * BK / VEC / NT;           // A chunks per thread
+  static constexpr int CPB = BN / VEC;
+  static constexpr int NB = BK * BN / VEC / NT;
+  static constexpr size_t SMEM = sizeof(double) * size_t(STAGES) * (A_ELEMS + B_ELEMS + P_ELEMS);
+  static_assert(NT % 32 == 0, "whole warps");
+  static_assert(NT % CPB == 0, "uniform B-chunk ownership (scale pass)");
+  static_assert((BM * BK / VEC) % NT == 0 && (BK * BN / VEC) % NT == 0, "even split");
+  static_assert(BK % 2 == 0, "k pairs");
+};
+
+template <int VEC>
+__device__ __forceinline__ int64_t clamp_vec(int64_t left) {
+  return left < VEC ? left : VEC;
+}
+
+template <int VEC>
+__device__ __forceinline__ void cp_chunk(double* dst, const double* src, int valid_elems) {
+  int v = valid_elems < 0 ? 0 : (valid_elems > VEC ? VEC : valid_elems);
+  if (VEC == 2)
+    cp_async16(dst, src, v * 8);
+  else
+    cp_async8(dst, src, v * 8);
+}
+
+template <int BM, int BN, int BK, bool KMAJ, int VEC, int STAGES, int NO>
+__global__ void __launch_bounds__((BM / 8) * (BN / 8), 1)
+    mttkrp_f64_sm100(const __grid_constant__ MttkrpParams p) {
+  using C = TileCfg<BM, BN, BK, KMAJ, VEC, STAGES, NO>;
+  extern __shared__ __align__(16) double smem[];
+  double* As = smem;
+  double* Bs = As + STAGES * C::A_ELEMS;
+  double* Ps = Bs + STAGES * C::B_ELEMS;
+
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  constexpr int WARPS_X = C::TX / C::WX;
+  const int ty = (warp / WARPS_X) * C::WY + lane / C::WX;
+  const int tx = (warp % WARPS_X) * C::WX + lane % C::WX;
+
+  const int64_t j0 = int64_t(blockIdx.x) * BN;
+  const int64_t n0 = int64_t(blockIdx.y) * BM;
+  const int64_t q0 = int64_t(blockIdx.z) * p.chunks_per_split;
+  const int64_t q1 = min(p.n_chunks, q0 + p.chunks_per_split);
+  const int nst = int(q1 - q0);
+
+  ChunkCursor<NO> cur;
+  cur.init(p, q0);
+
+  // --- stage loader: tensor tile + A_f rows + private P_o slots ----------
+  auto load_stage = [&](int buf) {
+    const int64_t if0 = cur.qf * BK;
+    double* a_s = As + buf * C::A_ELEMS;
+    double* b_s = Bs + buf * C::B_ELEMS;
+#pragma unroll
+    for (int c = 0; c < C::NA; ++c) {
+      const int idx = tid + c * C::NT;
+      if (!KMAJ) {
+        const int k = idx / C::CPA, m = (idx % C::CPA) * VEC;
+        const bool kv = if0 + k < p.If;
+        const int64_t off = cur.base + (if0 + k) * p.stride_f + n0 + m;
+        const int valid = kv ? int(clamp_vec<VEC>(p.Ik - (n0 + m))) : 0;
+        cp_chunk<VEC>(a_s + k * BM + m, valid > 0 ? p.y + off : p.y, valid);
+      } else {
+        const int m = idx / C::CPA, k = (idx % C::CPA) * VEC;
+        const bool mv = n0 + m < p.Ik;
+        const int64_t off = cur.base + (n0 + m) * p.stride_k + if0 + k;
+        const int valid = mv ? int(clamp_vec<VEC>(p.If - (if0 + k))) : 0;
+        cp_chunk<VEC>(a_s + m * C::APITCH + k, valid > 0 ? p.y + off : p.y, valid);
+      }
+    }
+    const int jc = (tid % C::CPB) * VEC;
+    const int jvalid = int(clamp_vec<VEC>(p.R - (j0 + jc)));
+#pragma unroll
+    for (int c = 0; c < C::NB; ++c) {
+      const int k = (tid + c * C::NT) / C::CPB;
+      const bool kv = if0 + k < p.If;
+      const int valid = kv ? jvalid : 0;
+      const double* src = p.fac_f + (if0 + k) * p.ld_f + j0 + jc;
+      cp_chunk<VEC>(b_s + k * BN + jc, valid > 0 ? src : p.fac_f, valid);
+    }
+#pragma unroll
+    for (int i = 0; i < NO; ++i) {
+      const double* src = p.fac_o[i] + cur.od[i] * p.ld_o[i] + j0 + jc;
+      cp_chunk<VEC>(Ps + (buf * NO + i) * C::NT * VEC + tid * VEC, jvalid > 0 ? src : p.fac_o[i],
+                    jvalid);
+    }
+  };
+
+  double acc[8][8];
+#pragma unroll
+  for (int r = 0; r < 8; ++r)
+#pragma unroll
+    for (int c = 0; c < 8; ++c) acc[r][c] = 0.0;
+
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < nst) {
+      load_stage(s);
+      cur.advance(p);
+    }
+    cp_async_commit();
+  }
+
+  for (int it = 0; it < nst; ++it) {
+    const int buf = it % STAGES;
+    cp_async_wait<STAGES - 2>();
+    if (NO > 0) {
+      // Khatri-Rao row formation: B[k][j] = A_f[i_f0+k][j] * prod_o A_o[o][j],
+      // on this thread's own chunks (same column pair for all of them).
+      const double* ps = Ps + buf * NO * C::NT * VEC + tid * VEC;
+      double pp[VEC];
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) pp[v] = ps[v];
+#pragma unroll
+      for (int i = 1; i < NO; ++i)
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) pp[v] *= ps[i * C::NT * VEC + v];
+      double* b_s = Bs + buf * C::B_ELEMS;
+      const int jc = (tid % C::CPB) * VEC;
+#pragma unroll
+      for (int c = 0; c < C::NB; ++c) {
+        const int k = (tid + c * C::NT) / C::CPB;
+        double* bp = b_s + k * BN + jc;
+        if (VEC == 2) {
+          double2 v = *reinterpret_cast<double2*>(bp);
+          v.x *= pp[0];
+          v.y *= pp[VEC - 1];
+          *reinterpret_cast<double2*>(bp) = v;
+        } else {
+          bp[0] *= pp[0];
+        }
+      }
+    }
+    __syncthreads();
+    if (it + STAGES - 1 < nst) {
+      load_stage((it + STAGES - 1) % STAGES);
+      cur.advance(p);
+    }
+    cp_async_commit();
+
+    const double* a_s = As + buf * C::A_ELEMS;
+    const double* b_s = Bs + buf * C::B_ELEMS;
+#pragma unroll
+    for (int kk = 0; kk < BK; kk += 2) {
+      double a[8][2];
+      if (KMAJ) {
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+          const int m = 2 * ty + (r & 1) + 2 * C::TY * (r >> 1);
+          const double2 v = *reinterpret_cast<const double2*>(a_s + m * C::APITCH + kk);
+          a[r][0] = v.x;
+          a[r][1] = v.y;
+        }
+      } else {
+#pragma unroll
+        for (int kq = 0; kq < 2; ++kq)
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const double2 v =
+                *reinterpret_cast<const double2*>(a_s + (kk + kq) * BM + 2 * ty + 2 * C::TY * i);
+            a[2 * i][kq] = v.x;
+            a[2 * i + 1][kq] = v.y;
+          }
+      }
+#pragma unroll
+      for (int kq = 0; kq < 2; ++kq) {
+        double b[8];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const double2 v =
+              *reinterpret_cast<const double2*>(b_s + (kk + kq) * BN + 2 * tx + 2 * C::TX * i);
+          b[2 * i] = v.x;
+          b[2 * i + 1] = v.y;
+        }
+#pragma unroll
+        for (int r = 0; r < 8; ++r)
+#pragma unroll
+          for (int c = 0; c < 8; ++c) acc[r][c] = fma(a[r][kq], b[c], acc[r][c]);
+      }
+    }
+  }
+  cp_async_wait<0>();
+
+  // --- epilogue: partial (or final, lam-folded) tile -> out --------------
+  double* out = p.out + int64_t(blockIdx.z) * p.out_split_stride;
+  const bool fold = p.lam != nullptr;
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    const int64_t n = n0 + 2 * ty + (r & 1) + 2 * C::TY * (r >> 1);
+    if (n >= p.Ik) continue;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int64_t j = j0 + 2 * tx + 2 * C::TX * i;
+      double v0 = acc[r][2 * i], v1 = acc[r][2 * i + 1];
+      if (fold) {
+        if (j < p.R) v0 *= p.lam[j];
+        if (j + 1 < p.R) v1 *= p.lam[j + 1];
+      }
+      double* dst = out + n * p.ldo + j;
+      if (j + 1 < p.R && ((p.ldo & 1) == 0)) {
+        *reinterpret_cast<double2*>(dst) = make_double2(v0, v1);
+      } else {
+        if (j < p.R) dst[0] = v0;
+        if (j + 1 < p.R) dst[1] = v1;
+      }
+    }
+  }
+}
+
+// Deterministic split-K reduction (the private-copy merge of
+// mttkrp._run_private_copy, mttkrp.py:453-460: partials summed in a fixed
+// order, then lam folded once).
+__global__ void splitk_reduce_f64(const double* __restrict__ w, int splits, int64_t Ik, int64_t R,
+                                  int64_t ldw, int64_t split_stride, const double* __restrict__ lam,
+                                  double* __restrict__ G, int64_t ldg) {
+  const int64_t total = Ik * R;
+  for (int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; idx < total;
+       idx += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t n = idx / R, j = idx - n * R;
+    const double* src = w + n * ldw + j;
+    double s = 0.0;
+    int sp = 0;
+    for (; sp + 4 <= splits; sp += 4) {
+      const double v0 = src[(sp + 0) * split_stride];
+      const double v1 = src[(sp + 1) * split_stride];
+      const double v2 = src[(sp + 2) * split_stride];
+      const double v3 = src[(sp + 3) * split_stride];
+      s += v0;
+      s += v1;
+      s += v2;
+      s += v3;
+    }
+    for (; sp < splits; ++sp) s += src[sp * split_stride];
+    if (lam) s *= lam[j];
+    G[n * ldg + j] = s;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host side
+
+struct Problem {
+  int d, k, f;
+  int64_t dims[CPK_MAX_MODES];
+  int64_t strides[CPK_MAX_MODES];
+  int64_t N, Ik, NS, R;
+  int n_o;
+  int o_modes[CPK_MAX_MODES];
+};
+
+static int make_problem(int d, const int64_t* dims, int mode, int64_t rank, Problem* pr) {
+  if (d < 1 || d > CPK_MAX_MODES) return fail(CPK_ERR_PARAM, "order d=%d unsupported (1..%d)", d, CPK_MAX_MODES);
+  if (!dims) return fail(CPK_ERR_SHAPE, "dims is NULL");
+  if (mode < 0 || mode >= d) return fail(CPK_ERR_INDEX, "mode %d out of range [0, %d]", mode, d - 1);
+  if (rank < 1) return fail(CPK_ERR_PARAM, "rank must be >= 1, got %lld", (long long)rank);
+  pr->d = d;
+  pr->k = mode;
+  pr->R = rank;
+  int64_t s = 1;
+  for (int m = 0; m < d; ++m) {
+    if (dims[m] < 1) return fail(CPK_ERR_SHAPE, "every extent must be >= 1 (mode %d is %lld)", m, (long long)dims[m]);
+    pr->dims[m] = dims[m];
+    pr->strides[m] = s;
+    if (s > INT64_MAX / dims[m]) return fail(CPK_ERR_SHAPE, "volume does not fit in int64");
+    s *= dims[m];
+  }
+  pr->N = s;
+  pr->Ik = dims[mode];
+  pr->NS = s / dims[mode];
+  pr->f = d == 1 ? -1 : (mode == 0 ? 1 : 0);
+  pr->n_o = 0;
+  for (int m = 0; m < d; ++m)
+    if (m != mode && m != pr->f) pr->o_modes[pr->n_o++] = m;
+  return CPK_OK;
+}
+
+// Tile configurations: (BM, BN, threads) = (128,128,256) | (128,64,128) | (64,32,32); BK = 16.
+constexpr int BK = 16;
+constexpr int STAGES = 3;
+
+template <int BM, int BN, bool KMAJ, int VEC, int NO>
+using KernelT = TileCfg<BM, BN, BK, KMAJ, VEC, STAGES, NO>;
+
+template <int BM, int BN, bool KMAJ, int VEC, int NO>
+static const void* kernel_ptr() {
+  return reinterpret_cast<const void*>(&mttkrp_f64_sm100<BM, BN, BK, KMAJ, VEC, STAGES, NO>);
+}
+
+struct KernelInfo {
+  const void* fn;
+  size_t smem;
+  int threads;
+};
+
+template <int BM, int BN, bool KMAJ, int VEC>
+static KernelInfo pick_no(int no) {
+  switch (no) {
+    case 0: return {kernel_ptr<BM, BN, KMAJ, VEC, 0>(), KernelT<BM, BN, KMAJ, VEC, 0>::SMEM, KernelT<BM, BN, KMAJ, VEC, 0>::NT};
+    case 1: return {kernel_ptr<BM, BN, KMAJ, VEC, 1>(), KernelT<BM, BN, KMAJ, VEC, 1>::SMEM, KernelT<BM, BN, KMAJ, VEC, 1>::NT};
+    case 2: return {kernel_ptr<BM, BN, KMAJ, VEC, 2>(), KernelT<BM, BN, KMAJ, VEC, 2>::SMEM, KernelT<BM, BN, KMAJ, VEC, 2>::NT};
+    case 3: return {kernel_ptr<BM, BN, KMAJ, VEC, 3>(), KernelT<BM, BN, KMAJ, VEC, 3>::SMEM, KernelT<BM, BN, KMAJ, VEC, 3>::NT};
+    default: return {nullptr, 0, 0};
+  }
+}
+
+template <int BM, int BN>
+static KernelInfo pick_layout(bool kmaj, int vec, int no) {
+  if (kmaj) return vec == 2 ? pick_no<BM, BN, true, 2>(no) : pick_no<BM, BN, true, 1>(no);
+  return vec == 2 ? pick_no<BM, BN, false, 2>(no) : pick_no<BM, BN, false, 1>(no);
+}
+
+static KernelInfo pick_kernel(int rank_tile, bool kmaj, int vec, int no) {
+  switch (rank_tile) {
+    case 128: return pick_layout<128, 128>(kmaj, vec, no);
+    case 64: return pick_layout<128, 64>(kmaj, vec, no);
+    case 32: return pick_layout<64, 32>(kmaj, vec, no);
+    default: return {nullptr, 0, 0};
+  }
+}
+
+static int block_rows_for(int rank_tile) { return rank_tile == 32 ? 64 : 128; }
+
+static int device_sms(int* out) {
+  static int cached = 0;
+  static std::once_flag once;
+  static cudaError_t err = cudaSuccess;
+  std::call_once(once, [] {
+    int dev = 0;
+    err = cudaGetDevice(&dev);
+    if (err == cudaSuccess) err = cudaDeviceGetAttribute(&cached, cudaDevAttrMultiProcessorCount, dev);
+  });
+  if (err != cudaSuccess) return fail(CPK_ERR_CUDA, "device query: %s", cudaGetErrorString(err));
+  *out = cached;
+  return CPK_OK;
+}
+
+// CTAs of the chosen kernel that fit on one SM (1 for the 256-thread tile).
+static int ctas_per_sm(const KernelInfo& ki) {
+  int n = 0;
+  if (cudaFuncSetAttribute(ki.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ki.smem)) != cudaSuccess ||
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, ki.fn, ki.threads, ki.smem) != cudaSuccess || n < 1) {
+    cudaGetLastError();
+    return 1;
+  }
+  return n;
+}
+
+static int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+static int64_t n_chunks_of(const Problem& pr) {
+  if (pr.f < 0) return 1;
+  int64_t n = ceil_div(pr.dims[pr.f], BK);
+  for (int i = 0; i < pr.n_o; ++i) n *= pr.dims[pr.o_modes[i]];
+  return n;
+}
+
+// Choose the split count so that (tiles x splits) CTAs fill whole waves.
+static int auto_splits(int64_t tiles, int64_t chunks, int slots) {
+  const int64_t max_s = std::max<int64_t>(1, std::min<int64_t>(chunks / 4, 1024));
+  double best = -1.0;
+  int64_t best_s = 1;
+  for (int64_t s = 1; s <= max_s; ++s) {
+    const int64_t work = tiles * s;
+    const int64_t waves = ceil_div(work, slots);
+    const double eff = double(work) / double(waves * slots);
+    if (eff > best + 5e-3) {
+      best = eff;
+      best_s = s;
+    }
+  }
+  return int(best_s);
+}
+
+static int resolve(const Problem& pr, cpk_plan* plan) {
+  if (plan->rank_tile == 0) {
+    // Rank tile = argmax useful/padded columns x tile efficiency: wider tiles
+    // stage fewer bytes per DFMA (BM+BN)/(BM*BN), so 128 wins unless its
+    // padding is large.  Must match mttkrp.heuristic_rank_tile.
+    const int cand[3] = {128, 64, 32};
+    const double weight[3] = {1.0, 0.93, 0.8};
+    double best_score = -1.0;
+    for (int i = 0; i < 3; ++i) {
+      const double score = double(pr.R) / double(ceil_div(pr.R, cand[i]) * cand[i]) * weight[i];
+      if (score > best_score + 1e-12) {
+        best_score = score;
+        plan->rank_tile = cand[i];
+      }
+    }
+  }
+  if (plan->rank_tile != 32 && plan->rank_tile != 64 && plan->rank_tile != 128)
+    return fail(CPK_ERR_PARAM, "rank_tile must be 32, 64 or 128 (got %d)", plan->rank_tile);
+  const int bm = block_rows_for(plan->rank_tile);
+  if (plan->block_rows == 0) plan->block_rows = bm;
+  if (plan->block_rows != bm)
+    return fail(CPK_ERR_PARAM, "block_rows %d does not match rank_tile %d (expects %d)", plan->block_rows,
+                plan->rank_tile, bm);
+  if (plan->sm_count == 0) {
+    int rc = device_sms(&plan->sm_count);
+    if (rc) return rc;
+  }
+  const int64_t chunks = n_chunks_of(pr);
+  const int64_t cols_per_chunk = pr.f < 0 ? 1 : std::min<int64_t>(BK, pr.dims[pr.f]);
+  if (plan->tile_volume < 0 || plan->tile_volume > pr.NS)
+    return fail(CPK_ERR_PARAM, "tile_volume %lld out of range [1, %lld]", (long long)plan->tile_volume,
+                (long long)pr.NS);
+  if (plan->splits < 0) return fail(CPK_ERR_PARAM, "splits must be >= 0");
+  if (plan->splits == 0) {
+    if (plan->tile_volume > 0) {
+      const int64_t cps = std::max<int64_t>(1, plan->tile_volume / cols_per_chunk);
+      plan->splits = int(std::min<int64_t>(ceil_div(chunks, cps), 1 << 20));
+    } else {
+      const int64_t tiles = ceil_div(pr.Ik, bm) * ceil_div(pr.R, plan->rank_tile);
+      const bool kmaj = pr.k != 0;
+      KernelInfo ki = pick_kernel(plan->rank_tile, kmaj, 2, std::min(pr.n_o, 3));
+      const int slots = plan->sm_count * (ki.fn ? ctas_per_sm(ki) : 1);
+      plan->splits = auto_splits(tiles, chunks, slots);
+    }
+  }
+  if (plan->splits > chunks) plan->splits = int(chunks);
+  // no empty splits: recompute from the per-split chunk count
+  const int64_t cps = ceil_div(chunks, plan->splits);
+  plan->splits = int(ceil_div(chunks, cps));
+  plan->tile_volume = std::min<int64_t>(pr.NS, cps * cols_per_chunk);
+  return CPK_OK;
+}
+
+static size_t ws_bytes_for(const Problem& pr, const cpk_plan& plan) {
+  if (plan.splits <= 1) return 0;
+  const int64_t ldw = (pr.R + 1) & ~int64_t(1);
+  return size_t(plan.splits) * size_t(pr.Ik) * size_t(ldw) * sizeof(double);
+}
+
+static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+}  // namespace cpk
+
+using namespace cpk;
+
+extern "C" int cpk_plan_resolve(int d, const int64_t* dims, int mode, int64_t rank, cpk_plan* plan) {
+  if (!plan) return fail(CPK_ERR_PARAM, "plan is NULL");
+  Problem pr;
+  int rc = make_problem(d, dims, mode, rank, &pr);
+  if (rc) return rc;
+  return resolve(pr, plan);
+}
+
+extern "C" int cpk_mttkrp_workspace_bytes(int d, const int64_t* dims, int mode, int64_t rank,
+                                          const cpk_plan* plan, size_t* bytes) {
+  if (!plan || !bytes) return fail(CPK_ERR_PARAM, "NULL argument");
+  Problem pr;
+  int rc = make_problem(d, dims, mode, rank, &pr);
+  if (rc) return rc;
+  cpk_plan p = *plan;
+  rc = resolve(pr, &p);
+  if (rc) return rc;
+  *bytes = ws_bytes_for(pr, p);
+  return CPK_OK;
+}
+
+// d == 1: G[n, j] = lam[j] * y[n] (ref_kernel with no factor products).
+__global__ static void mttkrp_order1(const double* y, int64_t I, int64_t R, const double* lam, double* G,
+                                     int64_t ldg) {
+  for (int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; idx < I * R;
+       idx += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t n = idx / R, j = idx % R;
+    G[n * ldg + j] = lam ? lam[j] * y[n] : y[n];
+  }
+}
+
+extern "C" int cpk_mttkrp_f64(const double* y, int d, const int64_t* dims, int mode, const double* const* factors,
+                              const int64_t* ld, const double* lam, int64_t rank, double* G, int64_t ldg,
+                              const cpk_plan* plan_in, void* workspace, size_t ws_bytes, void* stream) {
+  Problem pr;
+  int rc = make_problem(d, dims, mode, rank, &pr);
+  if (rc) return rc;
+  if (!y || !G) return fail(CPK_ERR_PARAM, "tensor or output pointer is NULL");
+  if (ldg < rank) return fail(CPK_ERR_PARAM, "ldg %lld < rank %lld", (long long)ldg, (long long)rank);
+  cudaStream_t st = as_stream(stream);
+  if (d == 1) {
+    mttkrp_order1<<<256, 256, 0, st>>>(y, pr.Ik, rank, lam, G, ldg);
+    return check_launch("mttkrp_order1");
+  }
+  if (!factors) return fail(CPK_ERR_PARAM, "factors is NULL");
+  for (int m = 0; m < d; ++m) {
+    if (m == mode) continue;
+    if (!factors[m]) return fail(CPK_ERR_PARAM, "factor %d is NULL", m);
+    if (ld && ld[m] < rank) return fail(CPK_ERR_PARAM, "ld[%d] < rank", m);
+  }
+  if (pr.n_o > 3)
+    return fail(CPK_ERR_PARAM, "order d=%d > 5 is not supported by the sm_100a kernel", d);
+
+  cpk_plan plan = plan_in ? *plan_in : cpk_plan{0, 0, 0, 0, 0};
+  rc = resolve(pr, &plan);
+  if (rc) return rc;
+  const size_t need = ws_bytes_for(pr, plan);
+  if (need > 0 && (!workspace || ws_bytes < need))
+    return fail(CPK_ERR_RESOURCE, "split-K workspace needs %zu bytes, got %zu", need, ws_bytes);
+
+  auto ldof = [&](int m) { return ld ? ld[m] : rank; };
+  MttkrpParams p{};
+  p.y = y;
+  p.fac_f = factors[pr.f];
+  p.ld_f = ldof(pr.f);
+  for (int i = 0; i < pr.n_o; ++i) {
+    const int m = pr.o_modes[i];
+    p.fac_o[i] = factors[m];
+    p.ld_o[i] = ldof(m);
+    p.dim_o[i] = pr.dims[m];
+    p.stride_o[i] = pr.strides[m];
+  }
+  p.Ik = pr.Ik;
+  p.stride_k = pr.strides[pr.k];
+  p.If = pr.dims[pr.f];
+  p.stride_f = pr.strides[pr.f];
+  p.chunks_per_f = ceil_div(p.If, BK);
+  p.n_chunks = n_chunks_of(pr);
+  p.chunks_per_split = ceil_div(p.n_chunks, plan.splits);
+  p.R = rank;
+
+  // 16-byte cp.async needs even element offsets everywhere: I_0 even, even
+  // leading dimensions, 16-byte aligned bases.
+  bool vec2 = (pr.dims[0] % 2 == 0) && aligned16(y) && aligned16(p.fac_f) && (p.ld_f % 2 == 0);
+  for (int i = 0; i < pr.n_o; ++i) vec2 = vec2 && aligned16(p.fac_o[i]) && (p.ld_o[i] % 2 == 0);
+  const bool kmaj = pr.k != 0;
+  KernelInfo ki = pick_kernel(plan.rank_tile, kmaj, vec2 ? 2 : 1, pr.n_o);
+  if (!ki.fn) return fail(CPK_ERR_PARAM, "no kernel for rank_tile %d", plan.rank_tile);
+
+  const bool direct = plan.splits == 1;
+  if (direct) {
+    p.out = G;
+    p.ldo = ldg;
+    p.out_split_stride = 0;
+    p.lam = lam;
+  } else {
+    p.out = static_cast<double*>(workspace);
+    p.ldo = (rank + 1) & ~int64_t(1);
+    p.out_split_stride = pr.Ik * p.ldo;
+    p.lam = nullptr;
+  }
+  static std::once_flag attr_once[64];
+  (void)attr_once;
+  if (cudaFuncSetAttribute(ki.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ki.smem)) != cudaSuccess)
+    return check_launch("cudaFuncSetAttribute");
+  dim3 grid(unsigned(ceil_div(rank, plan.rank_tile)), unsigned(ceil_div(pr.Ik, plan.block_rows)),
+            unsigned(plan.splits));
+  if (grid.y > 65535u || grid.z > 65535u) return fail(CPK_ERR_PARAM, "grid too large (I_k or splits)");
+  void* args[] = {&p};
+  cudaError_t e = cudaLaunchKernel(ki.fn, grid, dim3(ki.threads), args, ki.smem, st);
+  if (e != cudaSuccess) return fail(CPK_ERR_CUDA, "mttkrp launch: %s", cudaGetErrorString(e));
+  if (!direct) {
+    const int64_t total = pr.Ik * rank;
+    const int threads = 256;
+    const int64_t blocks = std::min<int64_t>(ceil_div(total, threads), int64_t(plan.sm_count) * 16);
+    splitk_reduce_f64<<<unsigned(std::max<int64_t>(blocks, 1)), threads, 0, st>>>(
+        p.out, plan.splits, pr.Ik, rank, p.ldo, p.out_split_stride, lam, G, ldg);
+    return check_launch("splitk_reduce");
+  }
+  return CPK_OK;
+}

@@ -1,0 +1,180 @@
+"""Dense d-way tensors, flat float64 in first-mode-fastest (column-major) order.
+
+Same layout contract as cpkern.dtensor (pkg/src/cpkern/dtensor.py:1-10,
+226-278): element (i_0, ..., i_{d-1}) lives at sum_m i_m * prod_{l<m} I_l.
+The payload may be a host numpy array (the reference's type) or a CUDA
+torch tensor.  Kernels always read a device copy; a host payload is copied
+to the device once and the copy is cached on the object (inputs are never
+mutated, test_cpals.py:180-184), so repeated MTTKRPs in CP-ALS do not
+re-stage the tensor.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from ._device import require_cuda
+from .errors import IndexRangeError, ShapeError
+
+
+def check_dims(dims) -> tuple:
+    """Validate a shape and return it as a tuple of ints (dtensor.py:29-44)."""
+    try:
+        out = tuple(int(x) for x in dims)
+    except (TypeError, ValueError) as exc:
+        raise ShapeError(f"shape must be a sequence of integers, got {dims!r}") from exc
+    if len(out) < 1:
+        raise ShapeError("shape needs at least one mode")
+    if any(x < 1 for x in out):
+        raise ShapeError(f"every extent must be >= 1, got {out}")
+    n = 1
+    for x in out:
+        n *= x
+    if n >= 2 ** 63:
+        raise ShapeError(f"volume {n} does not fit in a signed 64-bit index")
+    return out
+
+
+def num_elements(dims) -> int:
+    n = 1
+    for x in dims:
+        n *= int(x)
+    return n
+
+
+def col_major_strides(dims) -> tuple:
+    """Flat-index stride of each mode; stride of mode 0 is 1 (dtensor.py:54-61)."""
+    strides = []
+    s = 1
+    for x in dims:
+        strides.append(s)
+        s *= int(x)
+    return tuple(strides)
+
+
+def _is_torch(x) -> bool:
+    return isinstance(x, torch.Tensor)
+
+
+class DenseTensor:
+    """Dense tensor backed by one flat float64 buffer in first-mode-fastest order."""
+
+    __slots__ = ("dims", "data", "_dev")
+
+    def __init__(self, dims, data, copy=False):
+        self.dims = check_dims(dims)
+        n = num_elements(self.dims)
+        if _is_torch(data):
+            arr = data.detach()
+            if arr.dtype != torch.float64:
+                arr = arr.to(torch.float64)
+            arr = arr.reshape(-1)
+            if not arr.is_contiguous():
+                arr = arr.contiguous()
+            if copy:
+                arr = arr.clone()
+        else:
+            arr = np.asarray(data, dtype=np.float64)
+            arr = (arr.copy() if copy else arr).ravel()
+        size = arr.numel() if _is_torch(arr) else arr.size
+        if size != n:
+            raise ShapeError(f"data has {size} elements, shape {self.dims} needs {n}")
+        self.data = arr
+        self._dev = arr if (_is_torch(arr) and arr.is_cuda) else None
+
+    @classmethod
+    def zeros(cls, dims) -> "DenseTensor":
+        dims = check_dims(dims)
+        return cls(dims, np.zeros(num_elements(dims)))
+
+    @classmethod
+    def from_ndarray(cls, arr) -> "DenseTensor":
+        """Copy a numpy array; axis 0 becomes the fastest-varying mode."""
+        arr = np.asarray(arr, dtype=np.float64)
+        return cls(arr.shape, arr.ravel(order="F"))
+
+    @classmethod
+    def uniform(cls, dims, seed: int = 0, device=None) -> "DenseTensor":
+        """Synthetic U[0,1) tensor generated on the device by the counter-based
+        generator of cpk_fill_uniform_f64 (CPU twin: oracle/gen.py), for
+        shapes too large to stage through the host."""
+        from . import _lib
+
+        dims = check_dims(dims)
+        dev = require_cuda(device)
+        n = num_elements(dims)
+        buf = torch.empty(n, dtype=torch.float64, device=dev)
+        with torch.cuda.device(dev):
+            from ._device import stream_ptr
+
+            _lib.check(
+                _lib.load().cpk_fill_uniform_f64(buf.data_ptr(), n, int(seed), 0, stream_ptr(dev)),
+                "fill_uniform",
+            )
+        return cls(dims, buf)
+
+    @property
+    def ndim(self) -> int:
+        return len(self.dims)
+
+    @property
+    def size(self) -> int:
+        return num_elements(self.dims)
+
+    @property
+    def is_device(self) -> bool:
+        return _is_torch(self.data) and self.data.is_cuda
+
+    def device_data(self, device=None) -> torch.Tensor:
+        """The flat float64 payload on the CUDA device (cached H2D copy)."""
+        dev = require_cuda(device)
+        if self._dev is not None and self._dev.device == dev:
+            return self._dev
+        if _is_torch(self.data):
+            t = self.data.to(dev, non_blocking=False)
+        else:
+            host = torch.from_numpy(np.ascontiguousarray(self.data))
+            t = host.to(dev, non_blocking=False)
+        self._dev = t
+        return t
+
+    def to_ndarray(self) -> np.ndarray:
+        """The data as a numpy array with axis 0 fastest (host copy if on device)."""
+        host = self.data.detach().cpu().numpy() if _is_torch(self.data) else self.data
+        return host.reshape(self.dims, order="F")
+
+    def reshape(self, new_dims) -> "DenseTensor":
+        new_dims = check_dims(new_dims)
+        if num_elements(new_dims) != self.size:
+            raise ShapeError(f"cannot reshape volume {self.size} to {new_dims}")
+        return DenseTensor(new_dims, self.data)
+
+    def copy(self) -> "DenseTensor":
+        return DenseTensor(self.dims, self.data, copy=True)
+
+    def norm(self) -> float:
+        """Frobenius norm, computed on the device (deterministic reduction)."""
+        from . import _lib
+        from ._device import stream_ptr, workspace
+
+        dev = require_cuda()
+        x = self.device_data(dev)
+        out = torch.empty(1, dtype=torch.float64, device=dev)
+        work = workspace(dev, 8 * _lib.CPK_SUMSQ_PARTIALS, tag="sumsq")
+        _lib.check(
+            _lib.load().cpk_sumsq_f64(x.data_ptr(), x.numel(), work.data_ptr(), out.data_ptr(), stream_ptr(dev)),
+            "sumsq",
+        )
+        return float(out.sqrt().item())
+
+    def __repr__(self):
+        where = "cuda" if self.is_device else "host"
+        return f"DenseTensor(dims={self.dims}, {where})"
+
+
+def check_mode(ndim: int, mode: int) -> int:
+    mode = int(mode)
+    if not 0 <= mode < ndim:
+        raise IndexRangeError(f"mode {mode} out of range [0, {ndim - 1}]")
+    return mode

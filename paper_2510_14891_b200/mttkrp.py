@@ -1,0 +1,368 @@
+"""MTTKRP for dense tensors on B200: G = Y_(k) (KRP of the other factors) diag(lam).
+
+Drop-in for the cpkern.mttkrp dispatcher (pkg/src/cpkern/mttkrp.py): the same
+Variant / MttkrpPlan / MttkrpStats / MttkrpOutput types, `run(y, m, plan)`
+(mttkrp.py:552-565), the per-variant entry points, `plan_for_mode`
+(mttkrp.py:568-575) and the Eq. 6 tile heuristic (mttkrp.py:578-602), plus
+the north-star convenience `mttkrp(tensor, factors, mode)`.
+
+Every variant executes the hand-written sm_100a kernel behind
+cpk_mttkrp_f64 (csrc/mttkrp.cu); nothing is computed on the host.  What the
+variants keep from the reference is their *partitioning* and *accounting*:
+
+* TILE   -- tile_volume (N_T) sets the in-slice elements per CTA work item,
+            i.e. the split-K granularity (the reference's tiles per slice);
+* SLICE  -- one work item per output row block (no split of a slice);
+* ELEM / REFERENCE / GEMM / FULL_KRP / B200 -- the auto plan (splits chosen
+            to fill whole waves of the 148 SMs).
+
+Stats (element_visits, atomic_updates, ...) follow the reference formulas so
+reports stay comparable; `seconds` is the CUDA-event time of the kernel plus
+the split-K merge on the launching stream (the reference times kernel +
+private-copy merge, mttkrp.py:453-460), read lazily so timing adds no sync.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field, replace
+from enum import Enum
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._device import EventTimer, require_cuda, stream_ptr, workspace
+from .dtensor import DenseTensor, check_dims, num_elements
+from .errors import IndexRangeError, ParameterError, ShapeError
+from .kruskal import KruskalTensor
+
+
+class Variant(str, Enum):
+    REFERENCE = "reference"
+    FULL_KRP = "full-krp"
+    GEMM = "gemm"
+    ELEM = "elem"
+    SLICE = "slice"
+    TILE = "tile"
+    B200 = "b200"
+
+
+@dataclass(frozen=True)
+class MttkrpPlan:
+    """How to run one MTTKRP (mttkrp.py:227-263), with the GPU knobs added.
+
+    ``unroll`` (F), ``team_width`` (b_x) and ``vector_width`` (b_y) keep the
+    paper's meaning; on the GPU the column block is the rank tile, so they
+    are validated (>= 1) but the kernel's register tile is fixed at 8x8.
+    ``rank_tile`` (0 = auto, else 32/64/128) and ``splits`` (0 = auto) are
+    the B200 realization of the rank tiling and of N_T.  ``workers`` is
+    accepted for compatibility and ignored (one GPU per process).
+    """
+
+    variant: Variant
+    mode: int
+    unroll: int = 4
+    team_width: int = 1
+    vector_width: int = 1
+    tile_volume: int | None = None
+    workers: int = 0
+    rank_tile: int = 0
+    splits: int = 0
+
+    def validate(self, dims, rank) -> None:
+        d = len(dims)
+        if not 0 <= self.mode < d:
+            raise IndexRangeError(f"mode {self.mode} out of range [0, {d - 1}]")
+        if self.unroll < 1:
+            raise ParameterError(f"unroll must be >= 1, got {self.unroll}")
+        if self.team_width < 1 or self.vector_width < 1:
+            raise ParameterError("team_width and vector_width must be >= 1")
+        if rank < 1:
+            raise ParameterError(f"rank must be >= 1, got {rank}")
+        if self.rank_tile not in (0, 32, 64, 128):
+            raise ParameterError(f"rank_tile must be 0, 32, 64 or 128, got {self.rank_tile}")
+        if self.splits < 0:
+            raise ParameterError(f"splits must be >= 0, got {self.splits}")
+        if self.variant == Variant.TILE:
+            n_s = num_elements(dims) // dims[self.mode]
+            if self.tile_volume is None:
+                raise ParameterError("tile variant needs an explicit tile_volume")
+            if not 1 <= int(self.tile_volume) <= n_s:
+                raise ParameterError(f"tile_volume {self.tile_volume} out of range [1, {n_s}]")
+
+
+@dataclass
+class MttkrpStats:
+    """Work accounting and timing for one MTTKRP (mttkrp.py:266-285)."""
+
+    variant: Variant
+    mode: int
+    element_visits: int
+    atomic_updates: int
+    _seconds: object = field(repr=False, default=0.0)
+    workers: int = 1
+    tile_volume: int | None = None
+    unroll: int | None = None
+    scratch_bytes: int | None = None
+    footprint_bytes: int | None = None
+    rank_tile: int | None = None
+    splits: int | None = None
+    device: str = "cuda"
+
+    @property
+    def seconds(self) -> float:
+        s = self._seconds
+        return s.seconds if isinstance(s, EventTimer) else float(s)
+
+
+@dataclass
+class MttkrpOutput:
+    matrix: object  # numpy.ndarray for host inputs, torch CUDA tensor for device inputs
+    stats: MttkrpStats
+
+
+def _check_inputs(y: DenseTensor, m: KruskalTensor, mode: int) -> None:
+    if y.dims != m.dims:
+        raise ShapeError(f"tensor dims {y.dims} do not match model dims {m.dims}")
+    if not 0 <= int(mode) < y.ndim:
+        raise IndexRangeError(f"mode {mode} out of range [0, {y.ndim - 1}]")
+
+
+def _gpu_plan(plan: MttkrpPlan, dims, rank: int) -> _lib.CpkPlan:
+    p = _lib.CpkPlan(plan.rank_tile, 0, 0, plan.splits, 0)
+    v = Variant(plan.variant)
+    if plan.splits == 0:
+        if v == Variant.TILE:
+            p.tile_volume = int(plan.tile_volume)
+        elif v == Variant.SLICE:
+            p.splits = 1
+    dims_c = _lib.i64_array(dims)
+    _lib.check(_lib.load().cpk_plan_resolve(len(dims), dims_c, int(plan.mode), int(rank), p), "plan")
+    return p
+
+
+def resolve_plan(plan: MttkrpPlan, dims, rank: int) -> dict:
+    """The concrete GPU plan (rank tile, row block, N_T, splits) for a problem."""
+    require_cuda()
+    p = _gpu_plan(plan, check_dims(dims), rank)
+    return {"rank_tile": p.rank_tile, "block_rows": p.block_rows, "tile_volume": p.tile_volume,
+            "splits": p.splits, "sm_count": p.sm_count}
+
+
+def mttkrp_device(y_dev: torch.Tensor, dims, factors, mode: int, weights=None, plan: MttkrpPlan | None = None,
+                  out: torch.Tensor | None = None):
+    """Low-level device entry: y_dev flat CUDA float64, factors CUDA (I_m, R).
+
+    Returns (G, resolved CpkPlan, EventTimer).  G is (I_k, R) row-major CUDA.
+    """
+    dims = check_dims(dims)
+    d = len(dims)
+    mode = int(mode)
+    dev = y_dev.device
+    rank = next(int(f.shape[1]) for f in factors if f is not None)
+    if plan is None:
+        plan = MttkrpPlan(Variant.B200, mode)
+    p = _gpu_plan(plan, dims, rank)
+    dims_c = _lib.i64_array(dims)
+    nbytes = _lib.C.c_size_t(0)
+    lib = _lib.load()
+    _lib.check(lib.cpk_mttkrp_workspace_bytes(d, dims_c, mode, rank, p, _lib.C.byref(nbytes)), "workspace")
+    ws = workspace(dev, nbytes.value)
+    if out is None:
+        out = torch.empty((dims[mode], rank), dtype=torch.float64, device=dev)
+    ptrs = _lib.ptr_array([f.data_ptr() if m != mode else 0 for m, f in enumerate(factors)])
+    lds = _lib.i64_array([f.stride(0) for f in factors])
+    lam_ptr = weights.data_ptr() if weights is not None else None
+    timer = EventTimer(dev)
+    rc = lib.cpk_mttkrp_f64(
+        y_dev.data_ptr(), d, dims_c, mode, ptrs, lds, lam_ptr, rank, out.data_ptr(), out.stride(0),
+        p, ws.data_ptr() if ws is not None else None, nbytes.value, stream_ptr(dev),
+    )
+    timer.stop(dev)
+    _lib.check(rc, "mttkrp")
+    return out, p, timer
+
+
+def _unit_weights(w) -> bool:
+    if isinstance(w, torch.Tensor):
+        return bool((w == 1).all().item())
+    return bool(np.all(np.asarray(w) == 1.0))
+
+
+def _run_gpu(y: DenseTensor, m: KruskalTensor, plan: MttkrpPlan):
+    dev = require_cuda()
+    y_dev = y.device_data(dev)
+    fac = m.device_factors(dev)
+    lam = None if _unit_weights(m.weights) else m.device_weights(dev)
+    g, p, timer = mttkrp_device(y_dev, y.dims, fac, plan.mode, lam, plan)
+    host = not isinstance(y.data, torch.Tensor)
+    matrix = np.ascontiguousarray(g.cpu().numpy()) if host else g
+    return matrix, p, timer
+
+
+def _stats(variant, y, m, plan, p, timer, *, element_visits, atomic_updates, tile_volume=None, unroll=None,
+           scratch=None, footprint=None):
+    return MttkrpStats(
+        variant, plan.mode, element_visits=element_visits, atomic_updates=atomic_updates, _seconds=timer,
+        workers=1, tile_volume=tile_volume, unroll=unroll, scratch_bytes=scratch, footprint_bytes=footprint,
+        rank_tile=p.rank_tile, splits=p.splits,
+    )
+
+
+def mttkrp_reference(y: DenseTensor, m: KruskalTensor, mode: int) -> MttkrpOutput:
+    """mttkrp.py:328-339 signature; runs the sm_100a kernel with one split."""
+    _check_inputs(y, m, mode)
+    plan = MttkrpPlan(Variant.REFERENCE, int(mode), splits=1)
+    plan.validate(y.dims, m.rank)
+    mat, p, t = _run_gpu(y, m, plan)
+    return MttkrpOutput(mat, _stats(Variant.REFERENCE, y, m, plan, p, t, element_visits=y.size, atomic_updates=0))
+
+
+def mttkrp_elem(y: DenseTensor, m: KruskalTensor, plan: MttkrpPlan) -> MttkrpOutput:
+    if plan.variant != Variant.ELEM:
+        raise ParameterError(f"plan variant is {plan.variant}, expected elem")
+    _check_inputs(y, m, plan.mode)
+    plan.validate(y.dims, m.rank)
+    mat, p, t = _run_gpu(y, m, plan)
+    return MttkrpOutput(
+        mat,
+        _stats(Variant.ELEM, y, m, plan, p, t, element_visits=y.size, atomic_updates=y.size * m.rank,
+               unroll=plan.unroll),
+    )
+
+
+def mttkrp_slice(y: DenseTensor, m: KruskalTensor, plan: MttkrpPlan) -> MttkrpOutput:
+    if plan.variant != Variant.SLICE:
+        raise ParameterError(f"plan variant is {plan.variant}, expected slice")
+    _check_inputs(y, m, plan.mode)
+    plan.validate(y.dims, m.rank)
+    mat, p, t = _run_gpu(y, m, plan)
+    n_s = y.size // y.dims[plan.mode]
+    return MttkrpOutput(
+        mat,
+        _stats(Variant.SLICE, y, m, plan, p, t, element_visits=y.size * math.ceil(m.rank / plan.unroll),
+               atomic_updates=0, tile_volume=n_s, unroll=plan.unroll),
+    )
+
+
+def mttkrp_tile(y: DenseTensor, m: KruskalTensor, plan: MttkrpPlan) -> MttkrpOutput:
+    if plan.variant != Variant.TILE:
+        raise ParameterError(f"plan variant is {plan.variant}, expected tile")
+    _check_inputs(y, m, plan.mode)
+    plan.validate(y.dims, m.rank)
+    mat, p, t = _run_gpu(y, m, plan)
+    n_t = int(plan.tile_volume)
+    i_k = y.dims[plan.mode]
+    tps = -(-(y.size // i_k) // n_t)
+    return MttkrpOutput(
+        mat,
+        _stats(Variant.TILE, y, m, plan, p, t, element_visits=y.size * math.ceil(m.rank / plan.unroll),
+               atomic_updates=i_k * tps * m.rank, tile_volume=n_t, unroll=plan.unroll),
+    )
+
+
+def mttkrp_b200(y: DenseTensor, m: KruskalTensor, plan: MttkrpPlan) -> MttkrpOutput:
+    """The auto-planned kernel: splits fill whole waves of SMs."""
+    _check_inputs(y, m, plan.mode)
+    plan.validate(y.dims, m.rank)
+    mat, p, t = _run_gpu(y, m, plan)
+    i_k = y.dims[plan.mode]
+    return MttkrpOutput(
+        mat,
+        _stats(Variant(plan.variant), y, m, plan, p, t, element_visits=y.size,
+               atomic_updates=i_k * p.splits * m.rank if p.splits > 1 else 0, tile_volume=int(p.tile_volume)),
+    )
+
+
+def run(y: DenseTensor, m: KruskalTensor, plan: MttkrpPlan, **kwargs) -> MttkrpOutput:
+    """Dispatch one MTTKRP according to the plan's variant (mttkrp.py:552-565).
+
+    Budget kwargs of the CPU oracles (budget_bytes, scratch_cap_bytes) are
+    accepted and ignored: the matrix-free kernel allocates no KRP.
+    """
+    v = Variant(plan.variant)
+    if v == Variant.REFERENCE:
+        return mttkrp_reference(y, m, plan.mode)
+    if v == Variant.ELEM:
+        return mttkrp_elem(y, m, plan)
+    if v == Variant.SLICE:
+        return mttkrp_slice(y, m, plan)
+    if v == Variant.TILE:
+        return mttkrp_tile(y, m, plan)
+    return mttkrp_b200(y, m, plan)
+
+
+def mttkrp(tensor, factors, mode: int, weights=None, plan: MttkrpPlan | None = None):
+    """North-star convenience: G = MTTKRP(tensor, factors, mode).
+
+    ``tensor`` is a DenseTensor or a flat/first-mode-fastest CUDA tensor
+    (then ``factors`` must be CUDA too); ``factors`` is a list of (I_m, R)
+    matrices or a KruskalTensor (its weights are folded once).  Returns an
+    (I_k, R) matrix of the input's kind (numpy for host, torch for CUDA).
+    """
+    if isinstance(factors, KruskalTensor):
+        m = factors
+    else:
+        fs = list(factors)
+        r = int(fs[0].shape[1])
+        w = weights if weights is not None else (
+            torch.ones(r, dtype=torch.float64, device=fs[0].device) if isinstance(fs[0], torch.Tensor)
+            else np.ones(r))
+        m = KruskalTensor(w, fs, validate=False)
+    if not isinstance(tensor, DenseTensor):
+        tensor = DenseTensor(m.dims, tensor)
+    plan = plan or MttkrpPlan(Variant.B200, int(mode))
+    if plan.mode != int(mode):
+        plan = replace(plan, mode=int(mode))
+    return run(tensor, m, plan).matrix
+
+
+def plan_for_mode(plan: MttkrpPlan, dims, mode: int) -> MttkrpPlan:
+    """Copy of ``plan`` retargeted at ``mode``; tile volume clamped to N_S
+    (mttkrp.py:568-575)."""
+    p = replace(plan, mode=mode)
+    if p.variant == Variant.TILE and p.tile_volume is not None:
+        n_s = num_elements(dims) // dims[mode]
+        p = replace(p, tile_volume=max(1, min(int(p.tile_volume), n_s)))
+    return p
+
+
+def heuristic_tile_width(dims, machine) -> int:
+    """Eq. 6 (mttkrp.py:578-597): w^(d-1) s_f c/2 = s_LM/4."""
+    dims = tuple(int(x) for x in dims)
+    d = len(dims)
+    if d < 2:
+        raise ParameterError("tile-width heuristic needs at least two modes")
+    budget = (machine.s_lm_bytes / 4.0) / (machine.s_f_bytes * (machine.c_tiles / 2.0))
+    if budget < 1.0:
+        return 1
+    w = int(math.floor(budget ** (1.0 / (d - 1))))
+    while (w + 1) ** (d - 1) <= budget:
+        w += 1
+    while w > 1 and w ** (d - 1) > budget:
+        w -= 1
+    return max(1, min(w, min(dims)))
+
+
+def heuristic_tile_volume(dims, machine) -> int:
+    """N_T = w^(d-1) for the heuristic width (mttkrp.py:600-602)."""
+    return heuristic_tile_width(dims, machine) ** (len(dims) - 1)
+
+
+def heuristic_rank_tile(rank: int, machine=None) -> int:
+    """Rank tile: the B200 analogue of the paper's column-block choice.
+
+    The kernel keeps an 8 x 8 FP64 accumulator tile per thread (the register
+    file is the private level that bounds the rank tile, as the L1 bounds the
+    tile volume in Eq. 6), giving BN in {32, 64, 128} for BM in {64, 128,
+    128}.  Wider tiles stage fewer bytes per DFMA, (BM + BN) / (BM BN), so
+    the choice maximizes useful/padded columns x tile efficiency
+    {128: 1.0, 64: 0.93, 32: 0.8}.  Mirrors resolve() in csrc/mttkrp.cu.
+    """
+    best, best_score = 128, -1.0
+    for rt, w in ((128, 1.0), (64, 0.93), (32, 0.8)):
+        score = rank / (-(-rank // rt) * rt) * w
+        if score > best_score + 1e-12:
+            best, best_score = rt, score
+    return best

@@ -1,0 +1,174 @@
+"""Generate the golden fixtures by running the REFERENCE implementation itself.
+
+Run in a container where /root/reference is present (it is not on the GPU
+box).  The reference is imported read-only from /root/reference/pkg/src with
+its numba cache redirected; nothing from it is copied into this repo -- only
+its outputs on seeded inputs are stored.
+
+    NUMBA_CACHE_DIR=/tmp/numba_cache python tests/golden/make_golden.py
+
+Fixtures (numpy .npz, float64):
+  small.npz  -- CASES of test_mttkrp.py (kernel parity, all modes) and the
+                50-instance acceptance family (test_acceptance.py:52-62):
+                inputs + G from cpkern.mttkrp_reference (canonical order)
+  c1.npz     -- BASELINE config 1 (64^3, R=16): G for all modes (reference)
+  c2.npz     -- config 2 (512^3, R=64): G for all modes (cpkern.mttkrp_gemm,
+                which the reference's tests pin to mttkrp_reference at 1e-12),
+                plus 8 rows per mode from mttkrp_reference on single-slice
+                sub-tensors
+  c3.npz     -- config 3 (128^4, R=256): G for all modes (mttkrp_gemm)
+  als.npz    -- cp_als fit trajectories: the planted suites of test_cpals.py
+                (REFERENCE and GEMM plans), and config 3 for 10 sweeps (GEMM)
+Inputs for c1-c3 follow the reference CLI recipe (cli.py:133-141):
+tensor Philox(0).random(N), factors Philox(1).random((I_k, R)) per mode.
+"""
+
+import os
+import sys
+import time
+from pathlib import Path
+
+os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache")
+os.environ.setdefault("NUMBA_NUM_THREADS", "8")
+sys.path.insert(0, "/root/reference/pkg/src")
+
+import numpy as np  # noqa: E402
+
+import cpkern as ck  # noqa: E402
+from cpkern.mttkrp import MttkrpPlan, Variant  # noqa: E402
+
+OUT = Path(__file__).resolve().parent
+CASES = [((5, 4, 6), 3), ((3, 8, 2, 5), 4), ((6, 6), 2), ((2, 3, 2, 2, 3), 5)]
+
+
+def rng_for(seed):
+    return np.random.Generator(np.random.Philox(seed))
+
+
+def random_tensor(dims, seed):
+    r = rng_for(seed)
+    return ck.DenseTensor(dims, r.random(int(np.prod(dims))))
+
+
+def random_model(dims, rank, seed):
+    r = rng_for(seed + 1009)
+    lam = r.random(rank) + 0.5
+    return ck.KruskalTensor(lam, [r.random((i, rank)) for i in dims])
+
+
+def seeded_instance(i):
+    rng = np.random.Generator(np.random.Philox(1000 + i))
+    d = 3 + i % 3
+    dims = tuple(int(x) for x in rng.integers(2, 9, size=d))
+    rank = (1, 3, 8, 32)[i % 4]
+    y = ck.DenseTensor(dims, rng.random(int(np.prod(dims))))
+    factors = [rng.random((n, rank)) for n in dims]
+    weights = rng.random(rank) + 0.5
+    return y, ck.KruskalTensor(weights, factors)
+
+
+def pack_instance(store, key, y, m):
+    store[f"{key}/dims"] = np.asarray(y.dims, dtype=np.int64)
+    store[f"{key}/data"] = y.data
+    store[f"{key}/lam"] = m.weights
+    for j, a in enumerate(m.factors):
+        store[f"{key}/A{j}"] = a
+    for k in range(y.ndim):
+        store[f"{key}/G{k}"] = ck.mttkrp_reference(y, m, k).matrix
+
+
+def make_small():
+    store = {}
+    for c, (dims, rank) in enumerate(CASES):
+        pack_instance(store, f"case{c}", random_tensor(dims, 15), random_model(dims, rank, 16))
+    for i in range(50):
+        y, m = seeded_instance(i)
+        pack_instance(store, f"inst{i}", y, m)
+    np.savez_compressed(OUT / "small.npz", **store)
+
+
+def config_inputs(dims, rank, seed=0):
+    y = ck.DenseTensor(dims, rng_for(seed).random(int(np.prod(dims))))
+    r = rng_for(seed + 1)
+    m = ck.KruskalTensor(np.ones(rank), [r.random((i, rank)) for i in dims], validate=False)
+    return y, m
+
+
+def sampled_rows_reference(y, m, k, rows):
+    """G[rows] through the reference's own serial kernel on single-slice sub-tensors."""
+    arr = y.to_ndarray()
+    out = []
+    for n in rows:
+        sub = np.take(arr, [n], axis=k)
+        ys = ck.DenseTensor.from_ndarray(sub)
+        fs = [a if j != k else a[n:n + 1] for j, a in enumerate(m.factors)]
+        ms = ck.KruskalTensor(m.weights, fs, validate=False)
+        out.append(ck.mttkrp_reference(ys, ms, k).matrix[0])
+    return np.asarray(out)
+
+
+def make_config(name, dims, rank, use_gemm, sample_rows=0):
+    t0 = time.time()
+    y, m = config_inputs(dims, rank)
+    store = {"dims": np.asarray(dims, dtype=np.int64), "rank": np.int64(rank)}
+    for k in range(len(dims)):
+        g = (ck.mttkrp_gemm(y, m, k) if use_gemm else ck.mttkrp_reference(y, m, k)).matrix
+        store[f"G{k}"] = g
+        if sample_rows:
+            rows = np.linspace(0, dims[k] - 1, sample_rows).astype(np.int64)
+            store[f"rows{k}"] = rows
+            store[f"Grows{k}"] = sampled_rows_reference(y, m, k, rows)
+    np.savez_compressed(OUT / f"{name}.npz", **store)
+    print(f"{name}: {time.time() - t0:.1f} s", flush=True)
+
+
+def planted(dims, rank, seed):
+    rng = np.random.Generator(np.random.Philox(seed))
+    truth = ck.KruskalTensor(np.ones(rank), [rng.standard_normal((i, rank)) for i in dims])
+    return truth.full()
+
+
+def make_als():
+    store = {}
+    for dims, rank, tseed, sweeps in [((6, 7, 8), 3, 101, 14), ((4, 5, 6, 7), 2, 33, 12), ((5, 5, 5), 2, 42, 20)]:
+        y = planted(dims, rank, tseed)
+        key = f"planted_{'x'.join(map(str, dims))}_r{rank}"
+        store[f"{key}/data"] = y.data
+        store[f"{key}/dims"] = np.asarray(dims, dtype=np.int64)
+        for pname, plan in [("reference", MttkrpPlan(Variant.REFERENCE, 0)), ("gemm", MttkrpPlan(Variant.GEMM, 0))]:
+            model, tr = ck.cp_als(y, ck.AlsConfig(rank=rank, tol=0.0, max_iters=sweeps, seed=0, plan=plan))
+            store[f"{key}/fits_{pname}"] = np.asarray(tr.fits)
+            store[f"{key}/lam_{pname}"] = model.weights
+    # random (non-planted) tensor: fit identity regime (test_cpals.py:46-55)
+    y = ck.DenseTensor((7, 6, 5), rng_for(5).random(210))
+    model, tr = ck.cp_als(y, ck.AlsConfig(rank=3, tol=0.0, max_iters=20, seed=2))
+    store["rand765/data"] = y.data
+    store["rand765/fits"] = np.asarray(tr.fits)
+    store["rand765/lam"] = model.weights
+    for j, a in enumerate(model.factors):
+        store[f"rand765/A{j}"] = a
+    # config 3: 10 sweeps, GEMM plan (the fast CPU path)
+    t0 = time.time()
+    y, _ = config_inputs((128, 128, 128, 128), 256)
+    model, tr = ck.cp_als(y, ck.AlsConfig(rank=256, tol=0.0, max_iters=10, seed=0,
+                                          plan=MttkrpPlan(Variant.GEMM, 0)))
+    store["c3/fits"] = np.asarray(tr.fits)
+    store["c3/lam"] = model.weights
+    store["c3/mttkrp_seconds"] = np.asarray(tr.mttkrp_seconds)
+    print(f"c3 cp_als: {time.time() - t0:.1f} s", flush=True)
+    np.savez_compressed(OUT / "als.npz", **store)
+
+
+if __name__ == "__main__":
+    which = sys.argv[1:] or ["small", "c1", "c2", "c3", "als"]
+    if "small" in which:
+        make_small()
+    if "c1" in which:
+        make_config("c1", (64, 64, 64), 16, use_gemm=False)
+    if "c2" in which:
+        make_config("c2", (512, 512, 512), 64, use_gemm=True, sample_rows=4)
+    if "c3" in which:
+        make_config("c3", (128, 128, 128, 128), 256, use_gemm=True)
+    if "als" in which:
+        make_als()
+    print("done")

@@ -1,0 +1,115 @@
+"""C ABI: the library loads, exports every symbol of include/cpk_b200.h, and
+its host-side planning / validation logic behaves (no GPU needed)."""
+
+import ctypes as C
+import re
+from pathlib import Path
+
+import pytest
+
+from paper_2510_14891_b200 import _lib
+
+ROOT = Path(__file__).resolve().parents[1]
+
+
+def header_symbols():
+    text = (ROOT / "include" / "cpk_b200.h").read_text()
+    return sorted(set(re.findall(r"\b(cpk_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_library_exports_every_header_symbol():
+    lib = _lib.load()
+    syms = header_symbols()
+    assert len(syms) >= 15
+    for s in syms:
+        assert hasattr(lib, s), s
+    # the Python binding declares a prototype for each of them
+    assert sorted(_lib.exported_symbols()) == syms
+
+
+def test_library_is_sm100a(tmp_path):
+    import subprocess
+
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", str(_lib.LIB_PATH)],
+                         capture_output=True, text=True)
+    assert out.returncode == 0
+    assert "sm_100a" in out.stdout
+
+
+def test_version_and_error_string():
+    lib = _lib.load()
+    assert b"sm_100a" in lib.cpk_version()
+    assert lib.cpk_last_error() is not None
+
+
+def plan(dims, mode, rank, **kw):
+    p = _lib.CpkPlan(kw.get("rank_tile", 0), 0, kw.get("tile_volume", 0), kw.get("splits", 0), 148)
+    rc = _lib.load().cpk_plan_resolve(len(dims), _lib.i64_array(dims), mode, rank, p)
+    return rc, p
+
+
+def test_plan_resolution_fills_waves():
+    # c4: 1024^3, R=2000: 8 row tiles x 16 rank tiles = 128 tiles; the split
+    # count is the smallest one whose CTAs fill >= 99% of their waves
+    rc, p = plan((1024, 1024, 1024), 0, 2000)
+    assert rc == 0
+    assert p.rank_tile == 128 and p.block_rows == 128
+    ctas = 8 * 16 * p.splits
+    assert ctas / (148 * -(-ctas // 148)) >= 0.99
+    # c2: R=64 -> rank tile 64
+    rc, p = plan((512, 512, 512), 1, 64)
+    assert rc == 0 and p.rank_tile == 64
+    # tiny rank -> 32-wide tile, 64-row blocks
+    rc, p = plan((64, 64, 64), 0, 16)
+    assert rc == 0 and p.rank_tile == 32 and p.block_rows == 64
+
+
+def test_plan_tile_volume_maps_to_splits():
+    # N_S = 4096 in-slice elements, chunk = 16 of them: N_T = 256 -> 16 chunks/split
+    rc, p = plan((64, 64, 64), 0, 16, tile_volume=256)
+    assert rc == 0
+    assert p.splits == 4096 // 256
+    assert p.tile_volume == 256
+    rc, p = plan((64, 64, 64), 0, 16, splits=1)
+    assert rc == 0 and p.splits == 1 and p.tile_volume == 4096
+
+
+@pytest.mark.parametrize(
+    "dims,mode,rank,kw,code",
+    [
+        ((4, 5, 6), 3, 2, {}, 2),          # IndexRangeError
+        ((4, 5, 6), -1, 2, {}, 2),
+        ((4, 0, 6), 0, 2, {}, 1),          # ShapeError
+        ((4, 5, 6), 0, 0, {}, 3),          # ParameterError: rank
+        ((4, 5, 6), 0, 2, {"rank_tile": 48}, 3),
+        ((4, 5, 6), 0, 2, {"tile_volume": 31}, 3),  # N_S = 30
+    ],
+)
+def test_plan_errors_map_to_reference_exceptions(dims, mode, rank, kw, code):
+    rc, _ = plan(dims, mode, rank, **kw)
+    assert rc == code
+    exc = _lib._CODE_TO_EXC[code]
+    with pytest.raises(exc):
+        _lib.check(rc, "plan")
+
+
+def test_workspace_bytes():
+    p = _lib.CpkPlan(0, 0, 0, 0, 148)
+    nb = C.c_size_t(0)
+    rc = _lib.load().cpk_mttkrp_workspace_bytes(3, _lib.i64_array((1024, 1024, 1024)), 0, 2000, p, C.byref(nb))
+    assert rc == 0
+    rc2, q = plan((1024, 1024, 1024), 0, 2000)
+    assert nb.value == q.splits * 1024 * 2000 * 8
+    p1 = _lib.CpkPlan(0, 0, 0, 1, 148)
+    rc = _lib.load().cpk_mttkrp_workspace_bytes(3, _lib.i64_array((64, 64, 64)), 0, 16, p1, C.byref(nb))
+    assert rc == 0 and nb.value == 0
+
+
+def test_mttkrp_rejects_bad_arguments_before_touching_the_device():
+    lib = _lib.load()
+    dims = _lib.i64_array((4, 5, 6))
+    ptrs = _lib.ptr_array([0, 0, 0])
+    rc = lib.cpk_mttkrp_f64(None, 3, dims, 0, ptrs, None, None, 2, None, 2, None, None, 0, None)
+    assert rc == 3  # NULL tensor -> ParameterError
+    rc = lib.cpk_mttkrp_f64(None, 3, dims, 5, ptrs, None, None, 2, None, 2, None, None, 0, None)
+    assert rc == 2

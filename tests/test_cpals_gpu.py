@@ -1,0 +1,104 @@
+"""CP-ALS on the device vs the reference trajectories (goldens from cpkern)
+and the reference's own CP-ALS properties (test_cpals.py)."""
+
+import numpy as np
+import pytest
+
+import paper_2510_14891_b200 as ck
+from conftest import rng_for
+from oracle import gen, oracle
+
+pytestmark = pytest.mark.gpu
+
+
+def planted(dims, rank, seed):
+    rng = np.random.Generator(np.random.Philox(seed))
+    fs = [rng.standard_normal((i, rank)) for i in dims]
+    data = np.zeros(int(np.prod(dims)))
+    for j in range(rank):
+        acc = fs[-1][:, j]
+        for m in range(len(dims) - 2, -1, -1):
+            acc = np.outer(acc, fs[m][:, j]).ravel()
+        data += acc
+    return ck.DenseTensor(dims, data)
+
+
+def test_variant_swap_trajectories_match_reference(golden):
+    # test_cpals.py:73-98: fits within 1e-8 of the reference's trajectories
+    als = golden("als")
+    for key in sorted({k.split("/")[0] for k in als if k.startswith("planted")}):
+        dims = tuple(int(x) for x in als[f"{key}/dims"])
+        rank = int(key.split("_r")[1])
+        y = ck.DenseTensor(dims, als[f"{key}/data"])
+        for pname in ("reference", "gemm"):
+            ref = als[f"{key}/fits_{pname}"]
+            _, tr = ck.cp_als(y, ck.AlsConfig(rank=rank, tol=0.0, max_iters=len(ref), seed=0))
+            assert np.max(np.abs(np.asarray(tr.fits) - ref)) <= 1e-8, (key, pname)
+
+
+def test_fit_identity_regime_matches_reference(golden):
+    als = golden("als")
+    y = ck.DenseTensor((7, 6, 5), als["rand765/data"])
+    model, tr = ck.cp_als(y, ck.AlsConfig(rank=3, tol=0.0, max_iters=20, seed=2))
+    assert np.max(np.abs(np.asarray(tr.fits) - als["rand765/fits"])) <= 1e-10
+    assert oracle.rel_err(model.weights.cpu().numpy(), als["rand765/lam"]) <= 1e-8
+    for j in range(3):
+        assert oracle.rel_err(model.factors[j].cpu().numpy(), als[f"rand765/A{j}"]) <= 1e-8
+
+
+def test_planted_recovery_and_bookkeeping():
+    y = planted((6, 7, 8), 3, 101)
+    model, tr = ck.cp_als(y, ck.AlsConfig(rank=3, tol=1e-8, max_iters=100, seed=0))
+    assert tr.converged and tr.fits[-1] >= 1 - 1e-6
+    assert model.rank == 3 and model.dims == (6, 7, 8)
+    y = planted((4, 5, 6), 2, 15)
+    _, tr = ck.cp_als(y, ck.AlsConfig(rank=2, tol=0.0, max_iters=7, seed=0))
+    assert tr.iterations == 7 and not tr.converged
+    assert all(len(s) == 3 for s in tr.mttkrp_seconds) and len(tr.other_seconds) == 7
+    flat = sum(sum(s) for s in tr.mttkrp_seconds) + sum(tr.other_seconds)
+    assert 0 < flat <= tr.total_seconds
+
+
+def test_same_seed_same_run_and_weights_absorb_norms():
+    y = planted((6, 5, 4), 3, 9)
+    cfg = ck.AlsConfig(rank=3, tol=1e-8, max_iters=40, seed=7)
+    m1, t1 = ck.cp_als(y, cfg)
+    m2, t2 = ck.cp_als(y, cfg)
+    assert t1.fits == t2.fits
+    for a, b in zip(m1.factors, m2.factors):
+        assert np.array_equal(a.cpu().numpy(), b.cpu().numpy())
+    for a in m1.factors:
+        nrm = np.linalg.norm(a.cpu().numpy(), axis=0)
+        np.testing.assert_allclose(nrm[nrm > 0], 1.0, rtol=1e-12)
+
+
+def test_singular_normal_equations_survive():
+    y = planted((2, 2, 2), 2, 11)
+    model, tr = ck.cp_als(y, ck.AlsConfig(rank=5, tol=1e-8, max_iters=30, seed=1))
+    assert np.all(np.isfinite(tr.fits))
+    assert all(np.all(np.isfinite(a.cpu().numpy())) for a in model.factors)
+    assert tr.fits[-1] > tr.fits[0] - 1e-10
+
+
+def test_input_validation():
+    y = planted((3, 3, 3), 2, 19)
+    bad = y.to_ndarray().copy()
+    bad[0, 0, 0] = np.nan
+    with pytest.raises(ck.ParameterError):
+        ck.cp_als(ck.DenseTensor.from_ndarray(bad), ck.AlsConfig(rank=2))
+    with pytest.raises(ck.ParameterError):
+        ck.cp_als(ck.DenseTensor.zeros((3, 3)), ck.AlsConfig(rank=1))
+    for cfg in (dict(rank=0), dict(rank=1, max_iters=0), dict(rank=1, tol=-1.0), dict(rank=1, init="svd")):
+        with pytest.raises(ck.ParameterError):
+            ck.cp_als(y, ck.AlsConfig(**cfg))
+
+
+def test_c3_ten_sweeps_match_reference(golden):
+    """BASELINE config 3: 128^4, R=256, 10 sweeps vs the reference (GEMM plan)."""
+    als = golden("als")
+    dims = (128, 128, 128, 128)
+    y = ck.DenseTensor(dims, gen.philox_tensor(dims, 0))
+    model, tr = ck.cp_als(y, ck.AlsConfig(rank=256, tol=0.0, max_iters=10, seed=0))
+    ref = als["c3/fits"]
+    assert np.max(np.abs(np.asarray(tr.fits) - ref)) <= 1e-8
+    assert oracle.rel_err(model.weights.cpu().numpy(), als["c3/lam"]) <= 1e-6
