@@ -134,7 +134,8 @@ def cp_als(y: DenseTensor, config: AlsConfig) -> tuple:
             sweep_timers.append(timer)
             t_other = EventTimer(dev)
             hadamard(grams, skip=k, out=gamma)
-            a_hat = solver(gamma, g)
+            # the solve is in place; the fit needs the last mode's G itself
+            a_hat = solver(gamma, g.clone() if k == d - 1 else g)
             _lib.check(
                 lib.cpk_normalize_columns_f64(a_hat.data_ptr(), a_hat.shape[0], r, a_hat.stride(0),
                                               lam.data_ptr(), normsq.data_ptr(), sp),
