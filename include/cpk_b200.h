@@ -60,6 +60,8 @@ typedef struct cpk_plan {
   int64_t tile_volume;  /* in-slice elements per CTA work item, 0=auto */
   int32_t splits;       /* split-K factor, 0 = derive from tile_volume */
   int32_t sm_count;     /* 0 = query the device                        */
+  int32_t block_k;      /* 0 | 16 | 32: chunk depth (contraction tile) */
+  int32_t reserved;     /* must be 0                                   */
 } cpk_plan;
 
 /* Last error message of the calling thread (never NULL). */

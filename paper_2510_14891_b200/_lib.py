@@ -45,6 +45,8 @@ class CpkPlan(C.Structure):
         ("tile_volume", C.c_int64),
         ("splits", C.c_int32),
         ("sm_count", C.c_int32),
+        ("block_k", C.c_int32),
+        ("reserved", C.c_int32),
     ]
 
 

@@ -111,7 +111,9 @@ struct TileCfg {
   static constexpr int NA = BM * BK / VEC / NT;           // A chunks per thread
   static constexpr int CPB = BN / VEC;
   static constexpr int NB = BK * BN / VEC / NT;
-  static constexpr size_t SMEM = sizeof(double) * size_t(STAGES) * (A_ELEMS + B_ELEMS + P_ELEMS);
+  static constexpr size_t STAGE_BYTES = sizeof(double) * size_t(A_ELEMS + B_ELEMS + P_ELEMS);
+  static constexpr size_t SMEM = size_t(STAGES) * STAGE_BYTES;
+  static_assert(SMEM <= 227 * 1024, "shared memory budget");
   static_assert(NT % 32 == 0, "whole warps");
   static_assert(NT % CPB == 0, "uniform B-chunk ownership (scale pass)");
   static_assert((BM * BK / VEC) % NT == 0 && (BK * BN / VEC) % NT == 0, "even split");
@@ -384,47 +386,57 @@ static int make_problem(int d, const int64_t* dims, int mode, int64_t rank, Prob
   return CPK_OK;
 }
 
-// Tile configurations: (BM, BN, threads) = (128,128,256) | (128,64,128) | (64,32,32); BK = 16.
-constexpr int BK = 16;
-constexpr int STAGES = 3;
-
-template <int BM, int BN, bool KMAJ, int VEC, int NO>
-using KernelT = TileCfg<BM, BN, BK, KMAJ, VEC, STAGES, NO>;
-
-template <int BM, int BN, bool KMAJ, int VEC, int NO>
-static const void* kernel_ptr() {
-  return reinterpret_cast<const void*>(&mttkrp_f64_sm100<BM, BN, BK, KMAJ, VEC, STAGES, NO>);
-}
+// Tile configurations: (BM, BN, threads) = (128,128,256) | (128,64,128) | (64,32,32);
+// BK = 16 (any shape) or 32 (16-byte path only); as many stages (<= 3) as fit
+// in 227 KiB of shared memory.
+template <int BM, int BN, int BK, bool KMAJ, int VEC, int NO>
+struct Pick {
+  static constexpr size_t stage_bytes = TileCfg<BM, BN, BK, KMAJ, VEC, 1, NO>::STAGE_BYTES;
+  static constexpr int stages = (3 * stage_bytes <= 227 * 1024) ? 3 : 2;
+  using Cfg = TileCfg<BM, BN, BK, KMAJ, VEC, stages, NO>;
+};
 
 struct KernelInfo {
   const void* fn;
   size_t smem;
   int threads;
+  int stages;
 };
 
-template <int BM, int BN, bool KMAJ, int VEC>
+template <int BM, int BN, int BK, bool KMAJ, int VEC, int NO>
+static KernelInfo info() {
+  using P = Pick<BM, BN, BK, KMAJ, VEC, NO>;
+  return {reinterpret_cast<const void*>(&mttkrp_f64_sm100<BM, BN, BK, KMAJ, VEC, P::stages, NO>), P::Cfg::SMEM,
+          P::Cfg::NT, P::stages};
+}
+
+template <int BM, int BN, int BK, bool KMAJ, int VEC>
 static KernelInfo pick_no(int no) {
   switch (no) {
-    case 0: return {kernel_ptr<BM, BN, KMAJ, VEC, 0>(), KernelT<BM, BN, KMAJ, VEC, 0>::SMEM, KernelT<BM, BN, KMAJ, VEC, 0>::NT};
-    case 1: return {kernel_ptr<BM, BN, KMAJ, VEC, 1>(), KernelT<BM, BN, KMAJ, VEC, 1>::SMEM, KernelT<BM, BN, KMAJ, VEC, 1>::NT};
-    case 2: return {kernel_ptr<BM, BN, KMAJ, VEC, 2>(), KernelT<BM, BN, KMAJ, VEC, 2>::SMEM, KernelT<BM, BN, KMAJ, VEC, 2>::NT};
-    case 3: return {kernel_ptr<BM, BN, KMAJ, VEC, 3>(), KernelT<BM, BN, KMAJ, VEC, 3>::SMEM, KernelT<BM, BN, KMAJ, VEC, 3>::NT};
-    default: return {nullptr, 0, 0};
+    case 0: return info<BM, BN, BK, KMAJ, VEC, 0>();
+    case 1: return info<BM, BN, BK, KMAJ, VEC, 1>();
+    case 2: return info<BM, BN, BK, KMAJ, VEC, 2>();
+    case 3: return info<BM, BN, BK, KMAJ, VEC, 3>();
+    default: return {nullptr, 0, 0, 0};
   }
 }
 
 template <int BM, int BN>
-static KernelInfo pick_layout(bool kmaj, int vec, int no) {
-  if (kmaj) return vec == 2 ? pick_no<BM, BN, true, 2>(no) : pick_no<BM, BN, true, 1>(no);
-  return vec == 2 ? pick_no<BM, BN, false, 2>(no) : pick_no<BM, BN, false, 1>(no);
+static KernelInfo pick_layout(int bk, bool kmaj, int vec, int no) {
+  if (bk == 32) {
+    if (vec != 2) return {nullptr, 0, 0, 0};
+    return kmaj ? pick_no<BM, BN, 32, true, 2>(no) : pick_no<BM, BN, 32, false, 2>(no);
+  }
+  if (kmaj) return vec == 2 ? pick_no<BM, BN, 16, true, 2>(no) : pick_no<BM, BN, 16, true, 1>(no);
+  return vec == 2 ? pick_no<BM, BN, 16, false, 2>(no) : pick_no<BM, BN, 16, false, 1>(no);
 }
 
-static KernelInfo pick_kernel(int rank_tile, bool kmaj, int vec, int no) {
+static KernelInfo pick_kernel(int rank_tile, int bk, bool kmaj, int vec, int no) {
   switch (rank_tile) {
-    case 128: return pick_layout<128, 128>(kmaj, vec, no);
-    case 64: return pick_layout<128, 64>(kmaj, vec, no);
-    case 32: return pick_layout<64, 32>(kmaj, vec, no);
-    default: return {nullptr, 0, 0};
+    case 128: return pick_layout<128, 128>(bk, kmaj, vec, no);
+    case 64: return pick_layout<128, 64>(bk, kmaj, vec, no);
+    case 32: return pick_layout<64, 32>(bk, kmaj, vec, no);
+    default: return {nullptr, 0, 0, 0};
   }
 }
 
@@ -457,9 +469,9 @@ static int ctas_per_sm(const KernelInfo& ki) {
 
 static int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
-static int64_t n_chunks_of(const Problem& pr) {
+static int64_t n_chunks_of(const Problem& pr, int bk) {
   if (pr.f < 0) return 1;
-  int64_t n = ceil_div(pr.dims[pr.f], BK);
+  int64_t n = ceil_div(pr.dims[pr.f], bk);
   for (int i = 0; i < pr.n_o; ++i) n *= pr.dims[pr.o_modes[i]];
   return n;
 }
@@ -508,8 +520,15 @@ static int resolve(const Problem& pr, cpk_plan* plan) {
     int rc = device_sms(&plan->sm_count);
     if (rc) return rc;
   }
-  const int64_t chunks = n_chunks_of(pr);
-  const int64_t cols_per_chunk = pr.f < 0 ? 1 : std::min<int64_t>(BK, pr.dims[pr.f]);
+  if (plan->block_k == 0) {
+    // 32-deep chunks halve the per-stage overhead; they need the 16-byte
+    // path (even I_0) and a fastest non-k extent that fills them
+    plan->block_k = (pr.f >= 0 && pr.dims[0] % 2 == 0 && pr.dims[pr.f] >= 32) ? 32 : 16;
+  }
+  if (plan->block_k != 16 && plan->block_k != 32)
+    return fail(CPK_ERR_PARAM, "block_k must be 16 or 32 (got %d)", plan->block_k);
+  const int64_t chunks = n_chunks_of(pr, plan->block_k);
+  const int64_t cols_per_chunk = pr.f < 0 ? 1 : std::min<int64_t>(plan->block_k, pr.dims[pr.f]);
   if (plan->tile_volume < 0 || plan->tile_volume > pr.NS)
     return fail(CPK_ERR_PARAM, "tile_volume %lld out of range [1, %lld]", (long long)plan->tile_volume,
                 (long long)pr.NS);
@@ -521,7 +540,7 @@ static int resolve(const Problem& pr, cpk_plan* plan) {
     } else {
       const int64_t tiles = ceil_div(pr.Ik, bm) * ceil_div(pr.R, plan->rank_tile);
       const bool kmaj = pr.k != 0;
-      KernelInfo ki = pick_kernel(plan->rank_tile, kmaj, 2, std::min(pr.n_o, 3));
+      KernelInfo ki = pick_kernel(plan->rank_tile, plan->block_k, kmaj, 2, std::min(pr.n_o, 3));
       const int slots = plan->sm_count * (ki.fn ? ctas_per_sm(ki) : 1);
       plan->splits = auto_splits(tiles, chunks, slots);
     }
@@ -599,7 +618,7 @@ extern "C" int cpk_mttkrp_f64(const double* y, int d, const int64_t* dims, int m
   if (pr.n_o > 3)
     return fail(CPK_ERR_PARAM, "order d=%d > 5 is not supported by the sm_100a kernel", d);
 
-  cpk_plan plan = plan_in ? *plan_in : cpk_plan{0, 0, 0, 0, 0};
+  cpk_plan plan = plan_in ? *plan_in : cpk_plan{0, 0, 0, 0, 0, 0, 0};
   rc = resolve(pr, &plan);
   if (rc) return rc;
   const size_t need = ws_bytes_for(pr, plan);
@@ -622,17 +641,18 @@ extern "C" int cpk_mttkrp_f64(const double* y, int d, const int64_t* dims, int m
   p.stride_k = pr.strides[pr.k];
   p.If = pr.dims[pr.f];
   p.stride_f = pr.strides[pr.f];
-  p.chunks_per_f = ceil_div(p.If, BK);
-  p.n_chunks = n_chunks_of(pr);
-  p.chunks_per_split = ceil_div(p.n_chunks, plan.splits);
-  p.R = rank;
-
   // 16-byte cp.async needs even element offsets everywhere: I_0 even, even
   // leading dimensions, 16-byte aligned bases.
   bool vec2 = (pr.dims[0] % 2 == 0) && aligned16(y) && aligned16(p.fac_f) && (p.ld_f % 2 == 0);
   for (int i = 0; i < pr.n_o; ++i) vec2 = vec2 && aligned16(p.fac_o[i]) && (p.ld_o[i] % 2 == 0);
+  const int bk = (plan.block_k == 32 && vec2) ? 32 : 16;
+  p.chunks_per_f = ceil_div(p.If, bk);
+  p.n_chunks = n_chunks_of(pr, bk);
+  p.chunks_per_split = ceil_div(p.n_chunks, plan.splits);
+  p.R = rank;
+
   const bool kmaj = pr.k != 0;
-  KernelInfo ki = pick_kernel(plan.rank_tile, kmaj, vec2 ? 2 : 1, pr.n_o);
+  KernelInfo ki = pick_kernel(plan.rank_tile, bk, kmaj, vec2 ? 2 : 1, pr.n_o);
   if (!ki.fn) return fail(CPK_ERR_PARAM, "no kernel for rank_tile %d", plan.rank_tile);
 
   const bool direct = plan.splits == 1;

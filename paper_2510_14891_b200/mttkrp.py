@@ -55,8 +55,9 @@ class MttkrpPlan:
     ``unroll`` (F), ``team_width`` (b_x) and ``vector_width`` (b_y) keep the
     paper's meaning; on the GPU the column block is the rank tile, so they
     are validated (>= 1) but the kernel's register tile is fixed at 8x8.
-    ``rank_tile`` (0 = auto, else 32/64/128) and ``splits`` (0 = auto) are
-    the B200 realization of the rank tiling and of N_T.  ``workers`` is
+    ``rank_tile`` (0 = auto, else 32/64/128), ``splits`` (0 = auto) and
+    ``block_k`` (chunk depth, 0 = auto, else 16/32) are the B200
+    realization of the rank tiling and of N_T.  ``workers`` is
     accepted for compatibility and ignored (one GPU per process).
     """
 
@@ -69,6 +70,7 @@ class MttkrpPlan:
     workers: int = 0
     rank_tile: int = 0
     splits: int = 0
+    block_k: int = 0
 
     def validate(self, dims, rank) -> None:
         d = len(dims)
@@ -84,6 +86,8 @@ class MttkrpPlan:
             raise ParameterError(f"rank_tile must be 0, 32, 64 or 128, got {self.rank_tile}")
         if self.splits < 0:
             raise ParameterError(f"splits must be >= 0, got {self.splits}")
+        if self.block_k not in (0, 16, 32):
+            raise ParameterError(f"block_k must be 0, 16 or 32, got {self.block_k}")
         if self.variant == Variant.TILE:
             n_s = num_elements(dims) // dims[self.mode]
             if self.tile_volume is None:
@@ -130,7 +134,7 @@ def _check_inputs(y: DenseTensor, m: KruskalTensor, mode: int) -> None:
 
 
 def _gpu_plan(plan: MttkrpPlan, dims, rank: int) -> _lib.CpkPlan:
-    p = _lib.CpkPlan(plan.rank_tile, 0, 0, plan.splits, 0)
+    p = _lib.CpkPlan(plan.rank_tile, 0, 0, plan.splits, 0, plan.block_k, 0)
     v = Variant(plan.variant)
     if plan.splits == 0:
         if v == Variant.TILE:
@@ -147,7 +151,7 @@ def resolve_plan(plan: MttkrpPlan, dims, rank: int) -> dict:
     require_cuda()
     p = _gpu_plan(plan, check_dims(dims), rank)
     return {"rank_tile": p.rank_tile, "block_rows": p.block_rows, "tile_volume": p.tile_volume,
-            "splits": p.splits, "sm_count": p.sm_count}
+            "splits": p.splits, "sm_count": p.sm_count, "block_k": p.block_k}
 
 
 def mttkrp_device(y_dev: torch.Tensor, dims, factors, mode: int, weights=None, plan: MttkrpPlan | None = None,
