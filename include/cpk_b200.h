@@ -61,8 +61,15 @@ typedef struct cpk_plan {
   int32_t splits;       /* split-K factor, 0 = derive from tile_volume */
   int32_t sm_count;     /* 0 = query the device                        */
   int32_t block_k;      /* 0 | 16 | 32: chunk depth (contraction tile) */
-  int32_t reserved;     /* must be 0                                   */
+  int32_t engine;       /* CPK_ENGINE_*: data-movement engine          */
 } cpk_plan;
+
+/* engine: AUTO picks the warp-specialized TMA kernel when the problem is
+ * aligned (rank tile 128, chunk depth 32, even I_0 and leading dimensions,
+ * 16-byte aligned bases, d <= 5), else the cp.async kernel. */
+#define CPK_ENGINE_AUTO 0
+#define CPK_ENGINE_CPASYNC 1
+#define CPK_ENGINE_TMA 2
 
 /* Last error message of the calling thread (never NULL). */
 const char* cpk_last_error(void);

@@ -44,7 +44,9 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         return LIB
     LIBDIR.mkdir(exist_ok=True)
     nvcc = str(CUDA_HOME / "bin" / "nvcc")
-    objs = []
+    from concurrent.futures import ThreadPoolExecutor
+
+    jobs = []
     for src in sources():
         obj = LIBDIR / (src.stem + ".o")
         cmd = [
@@ -54,8 +56,10 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         ]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
-        _run(cmd, verbose)
-        objs.append(str(obj))
+        jobs.append((cmd, str(obj)))
+    with ThreadPoolExecutor(max_workers=max(1, min(len(jobs), os.cpu_count() or 1))) as ex:
+        list(ex.map(lambda j: _run(j[0], verbose), jobs))
+    objs = [o for _, o in jobs]
     link = [
         nvcc, *ARCH, "-shared", "-o", str(LIB), *objs,
         "-L", str(CUDA_HOME / "lib64"), "-lcusolver",

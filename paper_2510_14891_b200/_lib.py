@@ -46,7 +46,7 @@ class CpkPlan(C.Structure):
         ("splits", C.c_int32),
         ("sm_count", C.c_int32),
         ("block_k", C.c_int32),
-        ("reserved", C.c_int32),
+        ("engine", C.c_int32),
     ]
 
 

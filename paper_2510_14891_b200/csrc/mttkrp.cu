@@ -38,6 +38,7 @@
 // deterministic kernel sums in split order -- no floating-point atomics, so
 // results are bit-reproducible run to run.
 #include "common.cuh"
+#include "mttkrp_internal.cuh"
 
 #include <algorithm>
 #include <mutex>
@@ -525,6 +526,8 @@ static int resolve(const Problem& pr, cpk_plan* plan) {
     // path (even I_0) and a fastest non-k extent that fills them
     plan->block_k = (pr.f >= 0 && pr.dims[0] % 2 == 0 && pr.dims[pr.f] >= 32) ? 32 : 16;
   }
+  if (plan->engine < CPK_ENGINE_AUTO || plan->engine > CPK_ENGINE_TMA)
+    return fail(CPK_ERR_PARAM, "engine must be 0 (auto), 1 (cp.async) or 2 (TMA)");
   if (plan->block_k != 16 && plan->block_k != 32)
     return fail(CPK_ERR_PARAM, "block_k must be 16 or 32 (got %d)", plan->block_k);
   const int64_t chunks = n_chunks_of(pr, plan->block_k);
@@ -667,16 +670,40 @@ extern "C" int cpk_mttkrp_f64(const double* y, int d, const int64_t* dims, int m
     p.out_split_stride = pr.Ik * p.ldo;
     p.lam = nullptr;
   }
-  static std::once_flag attr_once[64];
-  (void)attr_once;
-  if (cudaFuncSetAttribute(ki.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ki.smem)) != cudaSuccess)
-    return check_launch("cudaFuncSetAttribute");
-  dim3 grid(unsigned(ceil_div(rank, plan.rank_tile)), unsigned(ceil_div(pr.Ik, plan.block_rows)),
-            unsigned(plan.splits));
-  if (grid.y > 65535u || grid.z > 65535u) return fail(CPK_ERR_PARAM, "grid too large (I_k or splits)");
-  void* args[] = {&p};
-  cudaError_t e = cudaLaunchKernel(ki.fn, grid, dim3(ki.threads), args, ki.smem, st);
-  if (e != cudaSuccess) return fail(CPK_ERR_CUDA, "mttkrp launch: %s", cudaGetErrorString(e));
+  WsRequest wr{};
+  wr.y = y;
+  wr.d = d;
+  wr.k = mode;
+  wr.n_o = pr.n_o;
+  for (int m = 0; m < d; ++m) {
+    wr.dims[m] = pr.dims[m];
+    wr.factors[m] = factors[m];
+    wr.ld[m] = ldof(m);
+  }
+  wr.rank = rank;
+  wr.rank_tile = plan.rank_tile;
+  wr.block_k = bk;
+  wr.splits = plan.splits;
+  wr.out = p.out;
+  wr.ldo = p.ldo;
+  wr.out_split_stride = p.out_split_stride;
+  wr.lam = p.lam;
+  const bool want_ws = plan.engine == CPK_ENGINE_TMA || (plan.engine == CPK_ENGINE_AUTO && ws_eligible(wr));
+  if (want_ws) {
+    if (!ws_eligible(wr))
+      return fail(CPK_ERR_PARAM, "TMA engine needs rank_tile 128, block_k 32, even I_0/ld, 16-B aligned bases, d<=5");
+    rc = launch_ws(wr, st);
+    if (rc) return rc;
+  } else {
+    if (cudaFuncSetAttribute(ki.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ki.smem)) != cudaSuccess)
+      return check_launch("cudaFuncSetAttribute");
+    dim3 grid(unsigned(ceil_div(rank, plan.rank_tile)), unsigned(ceil_div(pr.Ik, plan.block_rows)),
+              unsigned(plan.splits));
+    if (grid.y > 65535u || grid.z > 65535u) return fail(CPK_ERR_PARAM, "grid too large (I_k or splits)");
+    void* args[] = {&p};
+    cudaError_t e = cudaLaunchKernel(ki.fn, grid, dim3(ki.threads), args, ki.smem, st);
+    if (e != cudaSuccess) return fail(CPK_ERR_CUDA, "mttkrp launch: %s", cudaGetErrorString(e));
+  }
   if (!direct) {
     const int64_t total = pr.Ik * rank;
     const int threads = 256;

@@ -38,6 +38,9 @@ from .errors import IndexRangeError, ParameterError, ShapeError
 from .kruskal import KruskalTensor
 
 
+_ENGINES = {"auto": 0, "cpasync": 1, "tma": 2}
+
+
 class Variant(str, Enum):
     REFERENCE = "reference"
     FULL_KRP = "full-krp"
@@ -57,7 +60,8 @@ class MttkrpPlan:
     are validated (>= 1) but the kernel's register tile is fixed at 8x8.
     ``rank_tile`` (0 = auto, else 32/64/128), ``splits`` (0 = auto) and
     ``block_k`` (chunk depth, 0 = auto, else 16/32) are the B200
-    realization of the rank tiling and of N_T.  ``workers`` is
+    realization of the rank tiling and of N_T; ``engine`` picks the data
+    movement ("auto", "tma" = warp-specialized TMA kernel, "cpasync").  ``workers`` is
     accepted for compatibility and ignored (one GPU per process).
     """
 
@@ -71,6 +75,7 @@ class MttkrpPlan:
     rank_tile: int = 0
     splits: int = 0
     block_k: int = 0
+    engine: str = "auto"
 
     def validate(self, dims, rank) -> None:
         d = len(dims)
@@ -86,6 +91,8 @@ class MttkrpPlan:
             raise ParameterError(f"rank_tile must be 0, 32, 64 or 128, got {self.rank_tile}")
         if self.splits < 0:
             raise ParameterError(f"splits must be >= 0, got {self.splits}")
+        if self.engine not in _ENGINES:
+            raise ParameterError(f"engine must be one of {sorted(_ENGINES)}, got {self.engine!r}")
         if self.block_k not in (0, 16, 32):
             raise ParameterError(f"block_k must be 0, 16 or 32, got {self.block_k}")
         if self.variant == Variant.TILE:
@@ -134,7 +141,7 @@ def _check_inputs(y: DenseTensor, m: KruskalTensor, mode: int) -> None:
 
 
 def _gpu_plan(plan: MttkrpPlan, dims, rank: int) -> _lib.CpkPlan:
-    p = _lib.CpkPlan(plan.rank_tile, 0, 0, plan.splits, 0, plan.block_k, 0)
+    p = _lib.CpkPlan(plan.rank_tile, 0, 0, plan.splits, 0, plan.block_k, _ENGINES[plan.engine])
     v = Variant(plan.variant)
     if plan.splits == 0:
         if v == Variant.TILE:
@@ -151,7 +158,8 @@ def resolve_plan(plan: MttkrpPlan, dims, rank: int) -> dict:
     require_cuda()
     p = _gpu_plan(plan, check_dims(dims), rank)
     return {"rank_tile": p.rank_tile, "block_rows": p.block_rows, "tile_volume": p.tile_volume,
-            "splits": p.splits, "sm_count": p.sm_count, "block_k": p.block_k}
+            "splits": p.splits, "sm_count": p.sm_count, "block_k": p.block_k,
+            "engine": {v: k for k, v in _ENGINES.items()}[p.engine]}
 
 
 def mttkrp_device(y_dev: torch.Tensor, dims, factors, mode: int, weights=None, plan: MttkrpPlan | None = None,

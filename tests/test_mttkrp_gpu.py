@@ -190,3 +190,34 @@ def test_c4_row_sampled_parity():
             # the TILE restatement on the single-slice sub-tensor, all host cores
             ref = oracle.mttkrp_tile(ys, sub_dims, k, sub_f, f_cols=16, n_t=16384)[0][0]
             assert oracle.rel_err(got[n], ref) <= TOL, (k, n)
+
+
+@pytest.mark.parametrize("dims", [(40, 36, 34), (130, 66, 3), (34, 40, 70, 6), (6, 4, 8, 10, 4), (64, 2)])
+def test_tma_engine_parity(dims):
+    """The warp-specialized TMA kernel (forced) on ragged shapes: I_k not a
+    multiple of 128, chunk tails, rank tails, d = 2..5, splits."""
+    for rank in (2, 130, 256):
+        y = rng_for(sum(dims) * rank).random(int(np.prod(dims)))
+        fs = [rng_for(rank + 7 * j).random((n, rank)) for j, n in enumerate(dims)]
+        lam = rng_for(11).random(rank) + 0.5
+        m = ck.KruskalTensor(lam, fs)
+        t = ck.DenseTensor(dims, y)
+        for k in range(len(dims)):
+            ref = oracle.mttkrp_ref(y, dims, k, fs, lam)
+            for splits in (0, 1, 5):
+                plan = MttkrpPlan(Variant.B200, k, rank_tile=128, block_k=32, splits=splits, engine="tma")
+                got = ck.run(t, m, plan).matrix
+                assert oracle.rel_err(got, ref) <= TOL, (dims, rank, k, splits)
+
+
+def test_engines_agree_bitwise_on_c2_mode1(golden):
+    """Both engines produce the golden to 1e-10; each is bit-reproducible."""
+    g, dims, rank, y, fs = _config(golden, "c2")
+    t = ck.DenseTensor(dims, y)
+    m = ck.KruskalTensor(np.ones(rank), fs, validate=False)
+    for engine in ("tma", "cpasync"):
+        plan = MttkrpPlan(Variant.B200, 1, rank_tile=128, block_k=32, engine=engine)
+        a = ck.run(t, m, plan).matrix
+        b = ck.run(t, m, plan).matrix
+        assert np.array_equal(a, b)
+        assert oracle.rel_err(a, g["G1"]) <= TOL

@@ -21,6 +21,7 @@ ap.add_argument("--rank", type=int, default=2000)
 ap.add_argument("--rank-tile", type=int, default=0)
 ap.add_argument("--splits", type=int, default=0)
 ap.add_argument("--block-k", type=int, default=0)
+ap.add_argument("--engine", default="auto")
 a = ap.parse_args()
 dev = torch.device("cuda", 0)
 t = ck.DenseTensor.uniform(tuple(a.dims), seed=0, device=dev)
@@ -28,7 +29,7 @@ rng = np.random.Generator(np.random.Philox(1))
 fs = [torch.from_numpy(rng.random((n, a.rank))).to(dev) for n in a.dims]
 modes = range(len(a.dims)) if a.mode < 0 else [a.mode]
 for k in modes:
-    plan = MttkrpPlan(Variant.B200, k, rank_tile=a.rank_tile, splits=a.splits, block_k=a.block_k)
+    plan = MttkrpPlan(Variant.B200, k, rank_tile=a.rank_tile, splits=a.splits, block_k=a.block_k, engine=a.engine)
     print(k, ck.resolve_plan(plan, a.dims, a.rank))
     for _ in range(a.reps):
         g, p, timer = mttkrp_device(t.data, a.dims, fs, k, None, plan)
