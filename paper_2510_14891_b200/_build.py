@@ -43,12 +43,19 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     if not force and up_to_date():
         return LIB
     LIBDIR.mkdir(exist_ok=True)
+    objdir = LIBDIR / "obj"
+    objdir.mkdir(exist_ok=True)
     nvcc = str(CUDA_HOME / "bin" / "nvcc")
     from concurrent.futures import ThreadPoolExecutor
 
-    jobs = []
+    hdr_t = max(p.stat().st_mtime for p in headers() + [Path(__file__)])
+    jobs, objs = [], []
     for src in sources():
-        obj = LIBDIR / (src.stem + ".o")
+        obj = objdir / (src.stem + ".o")
+        objs.append(str(obj))
+        # object cache: recompile a source only when it (or any header) changed
+        if not force and obj.exists() and obj.stat().st_mtime >= max(src.stat().st_mtime, hdr_t):
+            continue
         cmd = [
             nvcc, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
             "--expt-relaxed-constexpr", "-I", str(INCLUDE), "-I", str(CSRC),
@@ -56,18 +63,15 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         ]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
-        jobs.append((cmd, str(obj)))
-    with ThreadPoolExecutor(max_workers=max(1, min(len(jobs), os.cpu_count() or 1))) as ex:
-        list(ex.map(lambda j: _run(j[0], verbose), jobs))
-    objs = [o for _, o in jobs]
+        jobs.append(cmd)
+    with ThreadPoolExecutor(max_workers=max(1, min(len(jobs) or 1, os.cpu_count() or 1))) as ex:
+        list(ex.map(lambda c: _run(c, verbose), jobs))
     link = [
         nvcc, *ARCH, "-shared", "-o", str(LIB), *objs,
         "-L", str(CUDA_HOME / "lib64"), "-lcusolver",
         "-Xlinker", f"-rpath={CUDA_HOME / 'lib64'}",
     ]
     _run(link, verbose)
-    for o in objs:
-        os.unlink(o)
     return LIB
 
 

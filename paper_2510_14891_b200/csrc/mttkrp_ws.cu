@@ -130,14 +130,16 @@ struct WsCfg {
   static constexpr int A_BYTES = A_ELEMS * 8, B_BYTES = B_ELEMS * 8, P_BYTES = P_ELEMS * 8;
   static constexpr int STAGE_BYTES = ((A_BYTES + B_BYTES + P_BYTES + 1023) / 1024) * 1024;
   static constexpr int TX_BYTES = A_BYTES + B_BYTES + P_BYTES;
-  static constexpr size_t SMEM = size_t(STAGES) * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr size_t SMEM = size_t(STAGES) * STAGE_BYTES + 256 /*barriers*/;
 };
 
 template <bool KMAJ, int NO, int STAGES>
 __global__ void __launch_bounds__(WS_THREADS, 1) mttkrp_f64_ws_sm100(const __grid_constant__ WsParams p) {
   using C = WsCfg<KMAJ, NO, STAGES>;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // dynamic shared memory starts at the CTA window base (no static smem), so
+  // it is 1024-byte aligned as the 128-byte swizzle requires; indexing the
+  // __shared__ array directly keeps every access an LDS (not a generic LD)
+  extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + STAGES * C::STAGE_BYTES);
   uint64_t* full_tma = bar;             // TMA bytes landed
   uint64_t* full = bar + STAGES;        // Khatri-Rao rows formed
@@ -238,8 +240,9 @@ __global__ void __launch_bounds__(WS_THREADS, 1) mttkrp_f64_ws_sm100(const __gri
       }
     };
     for (int t = 0; t < STAGES - 1 && t < nst; ++t) issue(t);
+    // Scale a stage as soon as its bytes land (consumers are still on the
+    // previous one), then refill the slot the consumers released last.
     for (int it = 0; it < nst; ++it) {
-      if (it + STAGES - 1 < nst) issue(it + STAGES - 1);
       const int s = it % STAGES;
       mbar_wait(&full_tma[s], (it / STAGES) & 1);
       if (NO > 0) {
@@ -276,6 +279,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) mttkrp_f64_ws_sm100(const __gri
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&full[s]);
+      if (it + STAGES - 1 < nst) issue(it + STAGES - 1);
     }
     return;
   }
@@ -395,7 +399,7 @@ static int encode(CUtensorMap* map, const void* base, int rank, const cuuint64_t
 
 template <bool KMAJ, int NO>
 static void ws_kernel(const void** fn, size_t* smem, int* stages) {
-  constexpr int S = (3 * WsCfg<KMAJ, NO, 3>::STAGE_BYTES + 1024 + 256 <= 227 * 1024) ? 3 : 2;
+  constexpr int S = (3 * WsCfg<KMAJ, NO, 3>::STAGE_BYTES + 256 <= 227 * 1024) ? 3 : 2;
   *fn = reinterpret_cast<const void*>(&mttkrp_f64_ws_sm100<KMAJ, NO, S>);
   *smem = WsCfg<KMAJ, NO, S>::SMEM;
   *stages = S;
