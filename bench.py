@@ -307,9 +307,16 @@ def run_b200(args):
         except Exception:
             traffic = None
 
+    del y, fs
+    torch.cuda.empty_cache()
     cp = None
     if args.cpals_iters > 0 and world == 1:
         cp = bench_cpals(ck, dev, args.cpals_iters)
+        torch.cuda.empty_cache()
+    c5 = None
+    if args.c5_iters > 0:
+        c5 = bench_c5(dev, args.c5_iters)
+        torch.cuda.empty_cache()
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -353,6 +360,8 @@ def run_b200(args):
         }
         if cp:
             line["cp_als"] = cp
+        if c5:
+            line["cp_als_c5"] = c5
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
@@ -376,6 +385,36 @@ def bench_cpals(ck, dev, iters):
             "fit_last": tr.fits[-1]}
 
 
+def bench_c5(dev, iters):
+    """Sharded CP-ALS at config 5 (4096 x 2048 x 2048, R = 512): seconds per
+    sweep, max over ranks.  Each rank generates its mode-0 slab on its GPU."""
+    import torch
+
+    from paper_2510_14891_b200 import sharded
+    from paper_2510_14891_b200.cpals import AlsConfig
+
+    dims, r = (4096, 2048, 2048), 512
+    comm = sharded.Comm()
+    part = sharded.partition_for(dims, comm.world)
+    y = sharded.uniform_slab(part, comm.rank, seed=SEED, device=dev)
+    sharded.cp_als_sharded(y, part, AlsConfig(rank=r, tol=0.0, max_iters=1, seed=0), comm, gather=False)
+    comm.seconds, comm.bytes = 0.0, 0
+    _, tr = sharded.cp_als_sharded(y, part, AlsConfig(rank=r, tol=0.0, max_iters=iters, seed=0), comm,
+                                   gather=False)
+    sec = statistics.median(tr.sweep_seconds)
+    mt = statistics.median(sum(s) for s in tr.mttkrp_seconds)
+    if comm.world > 1:
+        t = torch.tensor([sec, mt], dtype=torch.float64, device=dev)
+        comm.dist.all_reduce(t, op=comm.dist.ReduceOp.MAX)
+        sec, mt = (float(v) for v in t.tolist())
+    del y
+    flops = 3 * 2 * 4096 * 2048 * 2048 * r * 2
+    return {"config": "c5: 3-way 4096x2048x2048 f64, rank 512, mode-0 block partition", "gpus": comm.world,
+            "iters": iters, "sec_per_iter": sec, "mttkrp_sec_per_iter": mt,
+            "mttkrp_gflops": flops / mt / 1e9, "comm_seconds_total": comm.seconds,
+            "comm_bytes_total": comm.bytes, "fits": tr.fits}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -384,6 +423,7 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--cpals-iters", type=int, default=5)
+    ap.add_argument("--c5-iters", type=int, default=3)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()

@@ -162,6 +162,13 @@ int cpk_sumsq_f64(const double* x, int64_t n, double* work, double* out,
 int cpk_fill_uniform_f64(double* x, int64_t n, uint64_t seed, int64_t offset,
                          void* stream);
 
+/* The slab [lo, hi) along `mode` of the d-way splitmix tensor of global
+ * shape global_dims, stored as its own first-mode-fastest tensor: the
+ * per-rank shard of the sharded driver, generated on the device. */
+int cpk_fill_uniform_slab_f64(double* x, int d, const int64_t* global_dims,
+                              int mode, int64_t lo, int64_t hi, uint64_t seed,
+                              void* stream);
+
 /* Device-side DFMA throughput probe: returns achieved FP64 FLOP/s of a
  * register-resident FMA loop over the whole chip (the FP64 roofline peak;
  * MEASURED_PEAKS.json has no FP64 figure).  Synchronous. */

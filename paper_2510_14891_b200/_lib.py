@@ -76,6 +76,7 @@ _PROTOS = {
     "cpk_fit_terms_f64": (C.c_int, [_P, _P, _P, _P, _I64, _I64, _P, _P]),
     "cpk_sumsq_f64": (C.c_int, [_P, _I64, _P, _P, _P]),
     "cpk_fill_uniform_f64": (C.c_int, [_P, _I64, C.c_uint64, _I64, _P]),
+    "cpk_fill_uniform_slab_f64": (C.c_int, [_P, C.c_int, C.POINTER(_I64), C.c_int, _I64, _I64, C.c_uint64, _P]),
     "cpk_fp64_peak_probe": (C.c_int, [C.POINTER(C.c_double), C.POINTER(C.c_double)]),
 }
 

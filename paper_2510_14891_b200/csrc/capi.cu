@@ -39,6 +39,39 @@ __global__ void fill_uniform_kernel(double* __restrict__ x, int64_t n, uint64_t 
   }
 }
 
+// Slab of a larger splitmix tensor: local element (first mode fastest, local
+// dims) gets the value of its GLOBAL flat index, the shard mode offset by lo.
+struct SlabDims {
+  int64_t local[CPK_MAX_MODES];
+  int64_t gstride[CPK_MAX_MODES];
+  int d, mode;
+  int64_t lo;
+};
+
+__global__ void fill_slab_kernel(double* __restrict__ x, int64_t n, const __grid_constant__ SlabDims sd,
+                                 uint64_t key) {
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += stride) {
+    int64_t rem = i, g = 0;
+    for (int m = 0; m < sd.d; ++m) {
+      const int64_t q = rem / sd.local[m];
+      int64_t sub = rem - q * sd.local[m];
+      rem = q;
+      if (m == sd.mode) sub += sd.lo;
+      g += sub * sd.gstride[m];
+    }
+    const uint64_t z = mix64(key + (uint64_t(g) + 1) * 0x9E3779B97F4A7C15ull);
+    x[i] = double(z >> 11) * 0x1.0p-53;
+  }
+}
+
+static uint64_t seed_key(uint64_t seed) {
+  uint64_t z = seed * 0x9E3779B97F4A7C15ull + 0x632BE59BD9B4E019ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
 // Independent DFMA chains, register resident: the FP64 pipe ceiling.
 constexpr int PROBE_CHAINS = 16;
 __global__ void __launch_bounds__(256) dfma_probe_kernel(double* out, int iters, double b, double c) {
@@ -67,14 +100,34 @@ extern "C" int cpk_fill_uniform_f64(double* x, int64_t n, uint64_t seed, int64_t
   if (n < 0 || offset < 0) return fail(CPK_ERR_PARAM, "negative length or offset");
   if (n == 0) return CPK_OK;
   if (!x) return fail(CPK_ERR_PARAM, "x is NULL");
-  // key = mix64(seed): decorrelates neighbouring seeds
-  uint64_t z = seed * 0x9E3779B97F4A7C15ull + 0x632BE59BD9B4E019ull;
-  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
-  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
-  const uint64_t key = z ^ (z >> 31);
+  const uint64_t key = seed_key(seed);  // decorrelates neighbouring seeds
   const int64_t blocks = std::min<int64_t>((n + 255) / 256, 148 * 32);
   fill_uniform_kernel<<<unsigned(blocks), 256, 0, as_stream(stream)>>>(x, n, key, offset);
   return check_launch("fill_uniform");
+}
+
+extern "C" int cpk_fill_uniform_slab_f64(double* x, int d, const int64_t* global_dims, int mode, int64_t lo,
+                                         int64_t hi, uint64_t seed, void* stream) {
+  if (d < 1 || d > CPK_MAX_MODES || !global_dims) return fail(CPK_ERR_PARAM, "bad order or dims");
+  if (mode < 0 || mode >= d) return fail(CPK_ERR_INDEX, "mode %d out of range", mode);
+  if (lo < 0 || hi < lo || hi > global_dims[mode]) return fail(CPK_ERR_PARAM, "bad slab [%lld, %lld)", (long long)lo,
+                                                               (long long)hi);
+  SlabDims sd{};
+  sd.d = d;
+  sd.mode = mode;
+  sd.lo = lo;
+  int64_t g = 1, n = 1;
+  for (int m = 0; m < d; ++m) {
+    sd.local[m] = m == mode ? hi - lo : global_dims[m];
+    sd.gstride[m] = g;
+    g *= global_dims[m];
+    n *= sd.local[m];
+  }
+  if (n == 0) return CPK_OK;
+  if (!x) return fail(CPK_ERR_PARAM, "x is NULL");
+  const int64_t blocks = std::min<int64_t>((n + 255) / 256, 148 * 32);
+  fill_slab_kernel<<<unsigned(blocks), 256, 0, as_stream(stream)>>>(x, n, sd, seed_key(seed));
+  return check_launch("fill_slab");
 }
 
 extern "C" int cpk_fp64_peak_probe(double* flops_per_s, double* seconds) {
