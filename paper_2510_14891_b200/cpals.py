@@ -25,7 +25,9 @@ import numpy as np
 import torch
 
 from . import _lib
-from . import mttkrp as mt
+import importlib
+
+mt = importlib.import_module(".mttkrp", __package__)  # the submodule (the package re-exports a function of the same name)
 from ._device import EventTimer, require_cuda, stream_ptr, workspace
 from .dtensor import DenseTensor
 from .errors import ParameterError
