@@ -315,7 +315,10 @@ def run_b200(args):
         torch.cuda.empty_cache()
     c5 = None
     if args.c5_iters > 0:
-        c5 = bench_c5(dev, args.c5_iters)
+        try:
+            c5 = bench_c5(dev, args.c5_iters)
+        except Exception as exc:  # report, do not lose the headline line
+            c5 = {"error": f"{type(exc).__name__}: {exc}"[:300]}
         torch.cuda.empty_cache()
 
     cpu = None

@@ -104,9 +104,9 @@ def cp_als(y: DenseTensor, config: AlsConfig) -> tuple:
     config.validate()
     dev = require_cuda()
     y_dev = y.device_data(dev)
-    if not bool(torch.isfinite(y_dev).all().item()):
-        raise ParameterError("tensor has non-finite entries")
     norm_y = y.norm()
+    if not math.isfinite(norm_y):  # NaN/Inf anywhere make ||y|| non-finite
+        raise ParameterError("tensor has non-finite entries")
     if norm_y == 0.0:
         raise ParameterError("cannot fit an all-zero tensor (fit is undefined)")
     r = config.rank

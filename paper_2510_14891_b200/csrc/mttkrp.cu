@@ -524,7 +524,10 @@ static int resolve(const Problem& pr, cpk_plan* plan) {
   if (plan->block_k == 0) {
     // 32-deep chunks halve the per-stage overhead; they need the 16-byte
     // path (even I_0) and a fastest non-k extent that fills them
-    plan->block_k = (pr.f >= 0 && pr.dims[0] % 2 == 0 && pr.dims[pr.f] >= 32) ? 32 : 16;
+    // Only the 256-thread 128x128 tile keeps 2 warps per SMSP at the larger
+    // stage size (the 128x64 tile drops to 1 CTA/SM: measured 30 vs 45
+    // TFLOP/s on config 2, profiles/r01_sweep_c2.agg.csv).
+    plan->block_k = (plan->rank_tile == 128 && pr.f >= 0 && pr.dims[0] % 2 == 0 && pr.dims[pr.f] >= 32) ? 32 : 16;
   }
   if (plan->engine < CPK_ENGINE_AUTO || plan->engine > CPK_ENGINE_TMA)
     return fail(CPK_ERR_PARAM, "engine must be 0 (auto), 1 (cp.async) or 2 (TMA)");

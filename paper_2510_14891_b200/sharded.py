@@ -146,7 +146,9 @@ class DeviceOps:
         return a.clone()
 
     def all_finite(self, y_local) -> bool:
-        return bool(torch.isfinite(y_local).all().item())
+        # a NaN/Inf anywhere makes the sum of squares non-finite; no N-sized
+        # temporaries (c5 is 137 GB)
+        return bool(torch.isfinite(self.sumsq(y_local)).item())
 
     def sumsq(self, y_local):
         out = torch.empty(1, dtype=torch.float64, device=self.dev)
