@@ -494,45 +494,100 @@ static int auto_splits(int64_t tiles, int64_t chunks, int slots) {
   return int(best_s);
 }
 
+// Can the TMA kernel take this problem (dims-only view: the launch re-checks
+// pointer alignment and leading dimensions)?
+static bool tma_possible(const Problem& pr) {
+  if (pr.d < 2 || pr.d > 5 || pr.n_o > 3 || pr.dims[0] % 2 != 0 || pr.R % 2 != 0) return false;
+  for (int m = 0; m < pr.d; ++m)
+    if (pr.dims[m] >= (int64_t(1) << 31)) return false;
+  return true;
+}
+
+// Relative DFMA efficiency of each (engine, rank tile), from the c2/c4 sweeps
+// (profiles/r01_sweep_*.agg.csv); the auto plan minimizes padded work / rate.
+struct TileChoice {
+  int engine, rank_tile;
+  double rate;
+};
+static const TileChoice kChoices[] = {
+    {CPK_ENGINE_TMA, 256, 1.10}, {CPK_ENGINE_TMA, 128, 1.00}, {CPK_ENGINE_TMA, 64, 0.93},
+    {CPK_ENGINE_CPASYNC, 128, 0.93}, {CPK_ENGINE_CPASYNC, 64, 0.90}, {CPK_ENGINE_CPASYNC, 32, 0.60},
+};
+
+static int rows_for(int engine, int rank_tile, int* bm, int* bk_fixed) {
+  if (engine == CPK_ENGINE_TMA) {
+    int bk;
+    if (!ws_shape(rank_tile, bm, &bk)) return fail(CPK_ERR_PARAM, "TMA engine has no rank_tile %d tile", rank_tile);
+    *bk_fixed = bk;
+    return CPK_OK;
+  }
+  if (rank_tile != 32 && rank_tile != 64 && rank_tile != 128)
+    return fail(CPK_ERR_PARAM, "cp.async engine rank_tile must be 32, 64 or 128 (got %d)", rank_tile);
+  *bm = block_rows_for(rank_tile);
+  *bk_fixed = 0;
+  return CPK_OK;
+}
+
 static int resolve(const Problem& pr, cpk_plan* plan) {
-  if (plan->rank_tile == 0) {
-    // Rank tile = argmax useful/padded columns x tile efficiency: wider tiles
-    // stage fewer bytes per DFMA (BM+BN)/(BM*BN), so 128 wins unless its
-    // padding is large.  Must match mttkrp.heuristic_rank_tile.
-    const int cand[3] = {128, 64, 32};
-    const double weight[3] = {1.0, 0.93, 0.8};
-    double best_score = -1.0;
-    for (int i = 0; i < 3; ++i) {
-      const double score = double(pr.R) / double(ceil_div(pr.R, cand[i]) * cand[i]) * weight[i];
-      if (score > best_score + 1e-12) {
-        best_score = score;
-        plan->rank_tile = cand[i];
+  if (plan->engine < CPK_ENGINE_AUTO || plan->engine > CPK_ENGINE_TMA)
+    return fail(CPK_ERR_PARAM, "engine must be 0 (auto), 1 (cp.async) or 2 (TMA)");
+  const bool tma_ok = tma_possible(pr);
+  if (plan->engine == CPK_ENGINE_AUTO || plan->rank_tile == 0) {
+    // (engine, rank tile) minimizing padded rows x padded columns / rate
+    double best = 1e300;
+    int best_e = 0, best_rt = 0;
+    for (const TileChoice& c : kChoices) {
+      if (plan->engine != CPK_ENGINE_AUTO && c.engine != plan->engine) continue;
+      if (plan->rank_tile != 0 && c.rank_tile != plan->rank_tile) continue;
+      if (c.engine == CPK_ENGINE_TMA && !tma_ok) continue;
+      int bm, bk;
+      if (rows_for(c.engine, c.rank_tile, &bm, &bk)) continue;
+      const double cost =
+          double(ceil_div(pr.Ik, bm) * bm) * double(ceil_div(pr.R, c.rank_tile) * c.rank_tile) / c.rate;
+      if (cost < best * (1 - 1e-9)) {
+        best = cost;
+        best_e = c.engine;
+        best_rt = c.rank_tile;
       }
     }
+    if (best_e == 0) {
+      if (plan->engine == CPK_ENGINE_TMA && !tma_ok)
+        return fail(CPK_ERR_PARAM, "TMA engine needs 2 <= d <= 5, even I_0 and even rank");
+      return fail(CPK_ERR_PARAM, "no kernel for rank_tile %d", plan->rank_tile);
+    }
+    plan->engine = best_e;
+    plan->rank_tile = best_rt;
   }
-  if (plan->rank_tile != 32 && plan->rank_tile != 64 && plan->rank_tile != 128)
-    return fail(CPK_ERR_PARAM, "rank_tile must be 32, 64 or 128 (got %d)", plan->rank_tile);
-  const int bm = block_rows_for(plan->rank_tile);
+  if (plan->engine == CPK_ENGINE_TMA && !tma_ok)
+    return fail(CPK_ERR_PARAM, "TMA engine needs 2 <= d <= 5, even I_0 and even rank");
+  int bm, bk_fixed;
+  int rc = rows_for(plan->engine, plan->rank_tile, &bm, &bk_fixed);
+  if (rc) return rc;
   if (plan->block_rows == 0) plan->block_rows = bm;
   if (plan->block_rows != bm)
     return fail(CPK_ERR_PARAM, "block_rows %d does not match rank_tile %d (expects %d)", plan->block_rows,
                 plan->rank_tile, bm);
   if (plan->sm_count == 0) {
-    int rc = device_sms(&plan->sm_count);
+    rc = device_sms(&plan->sm_count);
     if (rc) return rc;
   }
   if (plan->block_k == 0) {
-    // 32-deep chunks halve the per-stage overhead; they need the 16-byte
-    // path (even I_0) and a fastest non-k extent that fills them
-    // Only the 256-thread 128x128 tile keeps 2 warps per SMSP at the larger
-    // stage size (the 128x64 tile drops to 1 CTA/SM: measured 30 vs 45
-    // TFLOP/s on config 2, profiles/r01_sweep_c2.agg.csv).
-    plan->block_k = (plan->rank_tile == 128 && pr.f >= 0 && pr.dims[0] % 2 == 0 && pr.dims[pr.f] >= 32) ? 32 : 16;
+    if (bk_fixed) {
+      plan->block_k = bk_fixed;
+    } else {
+      // 32-deep chunks halve the per-stage overhead, but only the 256-thread
+      // 128x128 cp.async tile keeps 2 warps per SMSP at that stage size (the
+      // 128x64 tile drops to 1 CTA/SM: 30 vs 45 TFLOP/s on config 2,
+      // profiles/r01_sweep_c2.agg.csv); needs the 16-byte path (even I_0)
+      plan->block_k =
+          (plan->rank_tile == 128 && pr.f >= 0 && pr.dims[0] % 2 == 0 && pr.dims[pr.f] >= 32) ? 32 : 16;
+    }
   }
-  if (plan->engine < CPK_ENGINE_AUTO || plan->engine > CPK_ENGINE_TMA)
-    return fail(CPK_ERR_PARAM, "engine must be 0 (auto), 1 (cp.async) or 2 (TMA)");
   if (plan->block_k != 16 && plan->block_k != 32)
     return fail(CPK_ERR_PARAM, "block_k must be 16 or 32 (got %d)", plan->block_k);
+  if (bk_fixed && plan->block_k != bk_fixed)
+    return fail(CPK_ERR_PARAM, "TMA rank_tile %d uses block_k %d (got %d)", plan->rank_tile, bk_fixed,
+                plan->block_k);
   const int64_t chunks = n_chunks_of(pr, plan->block_k);
   const int64_t cols_per_chunk = pr.f < 0 ? 1 : std::min<int64_t>(plan->block_k, pr.dims[pr.f]);
   if (plan->tile_volume < 0 || plan->tile_volume > pr.NS)
@@ -545,10 +600,12 @@ static int resolve(const Problem& pr, cpk_plan* plan) {
       plan->splits = int(std::min<int64_t>(ceil_div(chunks, cps), 1 << 20));
     } else {
       const int64_t tiles = ceil_div(pr.Ik, bm) * ceil_div(pr.R, plan->rank_tile);
-      const bool kmaj = pr.k != 0;
-      KernelInfo ki = pick_kernel(plan->rank_tile, plan->block_k, kmaj, 2, std::min(pr.n_o, 3));
-      const int slots = plan->sm_count * (ki.fn ? ctas_per_sm(ki) : 1);
-      plan->splits = auto_splits(tiles, chunks, slots);
+      int per_sm = 1;  // the TMA kernels take one CTA per SM
+      if (plan->engine == CPK_ENGINE_CPASYNC) {
+        KernelInfo ki = pick_kernel(plan->rank_tile, plan->block_k, pr.k != 0, 2, std::min(pr.n_o, 3));
+        per_sm = ki.fn ? ctas_per_sm(ki) : 1;
+      }
+      plan->splits = auto_splits(tiles, chunks, plan->sm_count * per_sm);
     }
   }
   if (plan->splits > chunks) plan->splits = int(chunks);
@@ -647,57 +704,60 @@ extern "C" int cpk_mttkrp_f64(const double* y, int d, const int64_t* dims, int m
   p.stride_k = pr.strides[pr.k];
   p.If = pr.dims[pr.f];
   p.stride_f = pr.strides[pr.f];
-  // 16-byte cp.async needs even element offsets everywhere: I_0 even, even
-  // leading dimensions, 16-byte aligned bases.
-  bool vec2 = (pr.dims[0] % 2 == 0) && aligned16(y) && aligned16(p.fac_f) && (p.ld_f % 2 == 0);
-  for (int i = 0; i < pr.n_o; ++i) vec2 = vec2 && aligned16(p.fac_o[i]) && (p.ld_o[i] % 2 == 0);
-  const int bk = (plan.block_k == 32 && vec2) ? 32 : 16;
-  p.chunks_per_f = ceil_div(p.If, bk);
-  p.n_chunks = n_chunks_of(pr, bk);
-  p.chunks_per_split = ceil_div(p.n_chunks, plan.splits);
-  p.R = rank;
-
-  const bool kmaj = pr.k != 0;
-  KernelInfo ki = pick_kernel(plan.rank_tile, bk, kmaj, vec2 ? 2 : 1, pr.n_o);
-  if (!ki.fn) return fail(CPK_ERR_PARAM, "no kernel for rank_tile %d", plan.rank_tile);
-
   const bool direct = plan.splits == 1;
-  if (direct) {
-    p.out = G;
-    p.ldo = ldg;
-    p.out_split_stride = 0;
-    p.lam = lam;
-  } else {
-    p.out = static_cast<double*>(workspace);
-    p.ldo = (rank + 1) & ~int64_t(1);
-    p.out_split_stride = pr.Ik * p.ldo;
-    p.lam = nullptr;
+  double* out = direct ? G : static_cast<double*>(workspace);
+  const int64_t ldo = direct ? ldg : ((rank + 1) & ~int64_t(1));
+  const int64_t out_split_stride = direct ? 0 : pr.Ik * ldo;
+  const double* lam_fold = direct ? lam : nullptr;
+
+  if (plan.engine == CPK_ENGINE_TMA) {
+    WsRequest wr{};
+    wr.y = y;
+    wr.d = d;
+    wr.k = mode;
+    wr.n_o = pr.n_o;
+    for (int m = 0; m < d; ++m) {
+      wr.dims[m] = pr.dims[m];
+      wr.factors[m] = factors[m];
+      wr.ld[m] = ldof(m);
+    }
+    wr.rank = rank;
+    wr.rank_tile = plan.rank_tile;
+    wr.block_k = plan.block_k;
+    wr.splits = plan.splits;
+    wr.out = out;
+    wr.ldo = ldo;
+    wr.out_split_stride = out_split_stride;
+    wr.lam = lam_fold;
+    if (ws_eligible(wr)) {
+      rc = launch_ws(wr, st);
+      if (rc) return rc;
+      goto reduce;
+    }
+    if (plan_in && plan_in->engine == CPK_ENGINE_TMA)
+      return fail(CPK_ERR_PARAM, "TMA engine needs even leading dimensions and 16-byte aligned bases");
+    // auto plan, misaligned buffers: same splits (same workspace) on cp.async
+    plan.engine = CPK_ENGINE_CPASYNC;
+    plan.rank_tile = std::min(plan.rank_tile, 128);
+    plan.block_rows = block_rows_for(plan.rank_tile);
+    plan.block_k = 16;
   }
-  WsRequest wr{};
-  wr.y = y;
-  wr.d = d;
-  wr.k = mode;
-  wr.n_o = pr.n_o;
-  for (int m = 0; m < d; ++m) {
-    wr.dims[m] = pr.dims[m];
-    wr.factors[m] = factors[m];
-    wr.ld[m] = ldof(m);
-  }
-  wr.rank = rank;
-  wr.rank_tile = plan.rank_tile;
-  wr.block_k = bk;
-  wr.splits = plan.splits;
-  wr.out = p.out;
-  wr.ldo = p.ldo;
-  wr.out_split_stride = p.out_split_stride;
-  wr.lam = p.lam;
-  const bool want_ws = plan.engine == CPK_ENGINE_TMA || (plan.engine == CPK_ENGINE_AUTO && ws_eligible(wr));
-  if (want_ws) {
-    if (!ws_eligible(wr))
-      return fail(CPK_ERR_PARAM, "TMA engine needs rank_tile 128, block_k 32, even I_0/ld, 16-B aligned bases, d<=5");
-    rc = launch_ws(wr, st);
-    if (rc) return rc;
-  } else {
+  {
+    // 16-byte cp.async needs even element offsets everywhere: I_0 even, even
+    // leading dimensions, 16-byte aligned bases.
+    bool vec2 = (pr.dims[0] % 2 == 0) && aligned16(y) && aligned16(p.fac_f) && (p.ld_f % 2 == 0);
+    for (int i = 0; i < pr.n_o; ++i) vec2 = vec2 && aligned16(p.fac_o[i]) && (p.ld_o[i] % 2 == 0);
+    const int bk = (plan.block_k == 32 && vec2) ? 32 : 16;
+    p.chunks_per_f = ceil_div(p.If, bk);
+    p.n_chunks = n_chunks_of(pr, bk);
+    p.chunks_per_split = ceil_div(p.n_chunks, plan.splits);
+    p.R = rank;
+    p.out = out;
+    p.ldo = ldo;
+    p.out_split_stride = out_split_stride;
+    p.lam = lam_fold;
+    KernelInfo ki = pick_kernel(plan.rank_tile, bk, pr.k != 0, vec2 ? 2 : 1, pr.n_o);
+    if (!ki.fn) return fail(CPK_ERR_PARAM, "no kernel for rank_tile %d", plan.rank_tile);
     if (cudaFuncSetAttribute(ki.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ki.smem)) != cudaSuccess)
       return check_launch("cudaFuncSetAttribute");
     dim3 grid(unsigned(ceil_div(rank, plan.rank_tile)), unsigned(ceil_div(pr.Ik, plan.block_rows)),
@@ -707,12 +767,13 @@ extern "C" int cpk_mttkrp_f64(const double* y, int d, const int64_t* dims, int m
     cudaError_t e = cudaLaunchKernel(ki.fn, grid, dim3(ki.threads), args, ki.smem, st);
     if (e != cudaSuccess) return fail(CPK_ERR_CUDA, "mttkrp launch: %s", cudaGetErrorString(e));
   }
+reduce:
   if (!direct) {
     const int64_t total = pr.Ik * rank;
     const int threads = 256;
     const int64_t blocks = std::min<int64_t>(ceil_div(total, threads), int64_t(plan.sm_count) * 16);
     splitk_reduce_f64<<<unsigned(std::max<int64_t>(blocks, 1)), threads, 0, st>>>(
-        p.out, plan.splits, pr.Ik, rank, p.ldo, p.out_split_stride, lam, G, ldg);
+        out, plan.splits, pr.Ik, rank, ldo, out_split_stride, lam, G, ldg);
     return check_launch("splitk_reduce");
   }
   return CPK_OK;

@@ -22,6 +22,8 @@ struct WsRequest {
   const double* lam;
 };
 
+// TMA tile for a rank tile (64 | 128 | 256): rows per CTA and chunk depth.
+bool ws_shape(int rank_tile, int* block_rows, int* block_k);
 bool ws_eligible(const WsRequest& r);
 int launch_ws(const WsRequest& r, cudaStream_t st);
 

@@ -32,13 +32,18 @@
 
 namespace cpk {
 
-constexpr int WS_BM = 128, WS_BN = 128, WS_BK = 32;
 constexpr int WS_CONSUMERS = 8;  // warps (warpgroups 0-1)
 // + one producer warpgroup (warps 8-11; warp 8 works, 9-11 retire at once).
 // setmaxnreg moves registers from the producer warpgroup to the consumers:
-// per SMSP 2 x 232 + 1 x 40 registers x 32 lanes <= 16384.
+// per SMSP 2 x 232 + 1 x 40 registers x 32 lanes <= 16384 (see WsRegs).
 constexpr int WS_THREADS = (WS_CONSUMERS + 4) * 32;
-constexpr int WS_CONSUMER_REGS = 232, WS_PRODUCER_REGS = 40;
+// 12-row tiles need 240 consumer registers (192 accumulators); their producer
+// warpgroup then runs in 24 (2 x 240 + 24 <= 512 per SMSP, x 32 lanes).
+template <int TM>
+struct WsRegs {
+  static constexpr int consumer = TM == 12 ? 240 : 232;
+  static constexpr int producer = TM == 12 ? 24 : 40;
+};
 
 struct alignas(64) WsParams {
   CUtensorMap tm_y;
@@ -121,21 +126,32 @@ __device__ __forceinline__ void tma_load(void* dst, const CUtensorMap* map, uint
 }
 
 // ---------------------------------------------------------------- kernel
-template <bool KMAJ, int NO, int STAGES>
+// Tile shapes (per-thread TM x 8 accumulators, 256 consumer threads):
+//   TM = 8,  BN = 128 -> BM = 128 (16 x 16 threads), BK = 32
+//   TM = 12, BN = 256 -> BM = 96  ( 8 x 32 threads), BK = 16
+//   TM = 8,  BN = 64  -> BM = 256 (32 x  8 threads), BK = 16
+// TM = 12 cuts shared-memory wavefronts per DFMA from 0.375 to 0.29: the A
+// fragment (lane quads share a row -> 1 wavefront per 8 B) grows, the B
+// fragment (4 distinct columns per quad -> 2 wavefronts per 8 B) does not.
+template <bool KMAJ, int NO, int TM, int BN, int BK, int STAGES>
 struct WsCfg {
-  static constexpr int D = NO + 2;                       // tensor order
-  static constexpr int A_ELEMS = WS_BM * WS_BK;          // 32 KiB
-  static constexpr int B_ELEMS = WS_BK * WS_BN;          // 32 KiB
-  static constexpr int P_ELEMS = NO * WS_BN;
+  static constexpr int D = NO + 2;  // tensor order
+  static constexpr int TX = BN / 8, TY = 256 / TX, BM = TY * TM;
+  static constexpr int A_ELEMS = BM * BK;
+  static constexpr int B_ELEMS = BK * BN;
+  static constexpr int P_ELEMS = NO * BN;
   static constexpr int A_BYTES = A_ELEMS * 8, B_BYTES = B_ELEMS * 8, P_BYTES = P_ELEMS * 8;
   static constexpr int STAGE_BYTES = ((A_BYTES + B_BYTES + P_BYTES + 1023) / 1024) * 1024;
   static constexpr int TX_BYTES = A_BYTES + B_BYTES + P_BYTES;
   static constexpr size_t SMEM = size_t(STAGES) * STAGE_BYTES + 256 /*barriers*/;
+  static_assert(TM % 2 == 0 && BK % 16 == 0 && BM <= 256 && BN <= 256, "tile shape");
+  static_assert((TX >= 8) && (TX % 8 == 0), "8 lanes per warp row");
 };
 
-template <bool KMAJ, int NO, int STAGES>
+template <bool KMAJ, int NO, int TM, int BN, int BK, int STAGES>
 __global__ void __launch_bounds__(WS_THREADS, 1) mttkrp_f64_ws_sm100(const __grid_constant__ WsParams p) {
-  using C = WsCfg<KMAJ, NO, STAGES>;
+  using C = WsCfg<KMAJ, NO, TM, BN, BK, STAGES>;
+  constexpr int BM = C::BM, TY = C::TY, TX = C::TX;
   // dynamic shared memory starts at the CTA window base (no static smem), so
   // it is 1024-byte aligned as the 128-byte swizzle requires; indexing the
   // __shared__ array directly keeps every access an LDS (not a generic LD)
@@ -148,13 +164,13 @@ __global__ void __launch_bounds__(WS_THREADS, 1) mttkrp_f64_ws_sm100(const __gri
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t q0 = int64_t(blockIdx.z) * p.chunks_per_split;
   const int nst = int(min(p.n_chunks, q0 + p.chunks_per_split) - q0);
-  const int j0 = blockIdx.x * WS_BN;
-  const int n0 = blockIdx.y * WS_BM;
+  const int j0 = blockIdx.x * BN;
+  const int n0 = blockIdx.y * BM;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full_tma[s], 1);
-      mbar_init(&full[s], 1);
+      mbar_init(&full[s], 4);  // one arrive per producer warp
       mbar_init(&empty[s], WS_CONSUMERS);
     }
     fence_barrier_init();
@@ -163,22 +179,25 @@ __global__ void __launch_bounds__(WS_THREADS, 1) mttkrp_f64_ws_sm100(const __gri
 
   if (warp >= WS_CONSUMERS) {
     // ================================================================ producer
-    setmaxnreg_dec<WS_PRODUCER_REGS>();
-    if (warp != WS_CONSUMERS) return;
-    if (lane == 0) {
+    // warp 8 issues the TMA loads; all four producer warps form the
+    // Khatri-Rao rows of a landed stage, one column pair per thread
+    setmaxnreg_dec<WsRegs<TM>::producer>();
+    const int pt = threadIdx.x - WS_CONSUMERS * 32;  // 0..127
+    const bool issuer = warp == WS_CONSUMERS;
+    if (issuer && lane == 0) {
       prefetch_tmap(&p.tm_y);
       prefetch_tmap(&p.tm_f);
 #pragma unroll
       for (int i = 0; i < NO; ++i) prefetch_tmap(&p.tm_o[i]);
     }
-    // chunk cursor for the TMA issue side (runs STAGES-1 chunks ahead)
-    int64_t qf, od[NO > 0 ? NO : 1];
+    // extents are < 2^31 (tensor-map coordinates), so the cursor is 32-bit
+    int qf, od[NO > 0 ? NO : 1];
     {
-      qf = q0 % p.chunks_per_f;
+      qf = int(q0 % p.chunks_per_f);
       int64_t rest = q0 / p.chunks_per_f;
 #pragma unroll
       for (int i = 0; i < NO; ++i) {
-        od[i] = rest % p.dim_o[i];
+        od[i] = int(rest % p.dim_o[i]);
         rest /= p.dim_o[i];
       }
     }
@@ -191,33 +210,30 @@ __global__ void __launch_bounds__(WS_THREADS, 1) mttkrp_f64_ws_sm100(const __gri
         double* b_s = reinterpret_cast<double*>(st + C::A_BYTES);
         double* p_s = reinterpret_cast<double*>(st + C::A_BYTES + C::B_BYTES);
         mbar_expect_tx(&full_tma[s], C::TX_BYTES);
-        const int if0 = int(qf) * WS_BK;
+        const int if0 = qf * BK;
+        // tensor-map coordinates, mode 0 first; o digits fill the non-k,
+        // non-f slots in ascending mode order (closed form, no local arrays)
         int c[C::D];
-        // o digits fill the non-k, non-f slots in ascending mode order
-        {
-          int oi = 0;
+        if constexpr (!KMAJ) {
+          c[0] = n0;
+          c[1] = if0;
 #pragma unroll
-          for (int m = 0; m < C::D; ++m) {
-            const bool is_k = KMAJ ? (m == p.k) : (m == 0);
-            const bool is_f = KMAJ ? (m == 0) : (m == 1);
-            if (is_k) {
-              c[m] = n0;
-            } else if (is_f) {
-              c[m] = if0;
-            } else {
-              int v = 0;
+          for (int m = 2; m < C::D; ++m) c[m] = od[m - 2];
+        } else {
+          c[0] = if0;
 #pragma unroll
-              for (int i = 0; i < NO; ++i)
-                if (i == oi) v = int(od[i]);
-              c[m] = v;
-              ++oi;
-            }
+          for (int m = 1; m < C::D; ++m) {
+            const int lo_i = m - 1 < NO ? m - 1 : NO - 1;  // o index when m < k
+            const int hi_i = m >= 2 ? m - 2 : 0;            // o index when m > k
+            c[m] = (m == p.k) ? n0 : (m > p.k ? od[hi_i] : od[lo_i]);
           }
         }
         if (KMAJ) {
-          tma_load<C::D>(a_s, &p.tm_y, &full_tma[s], c);
-          c[0] = if0 + 16;
-          tma_load<C::D>(a_s + WS_BM * 16, &p.tm_y, &full_tma[s], c);
+#pragma unroll
+          for (int pn = 0; pn < BK / 16; ++pn) {  // one 16-deep swizzled panel per box
+            c[0] = if0 + 16 * pn;
+            tma_load<C::D>(a_s + pn * (BM * 16), &p.tm_y, &full_tma[s], c);
+          }
         } else {
           tma_load<C::D>(a_s, &p.tm_y, &full_tma[s], c);
         }
@@ -225,75 +241,69 @@ __global__ void __launch_bounds__(WS_THREADS, 1) mttkrp_f64_ws_sm100(const __gri
         tma_load<2>(b_s, &p.tm_f, &full_tma[s], cf);
 #pragma unroll
         for (int i = 0; i < NO; ++i) {
-          const int co[2] = {j0, int(od[i])};
-          tma_load<2>(p_s + i * WS_BN, &p.tm_o[i], &full_tma[s], co);
+          const int co[2] = {j0, od[i]};
+          tma_load<2>(p_s + i * BN, &p.tm_o[i], &full_tma[s], co);
         }
       }
       // advance the odometer (in-slice walk, _kernels.py:135-147)
-      if (++qf == p.chunks_per_f) {
+      if (++qf == int(p.chunks_per_f)) {
         qf = 0;
 #pragma unroll
         for (int i = 0; i < NO; ++i) {
-          if (++od[i] < p.dim_o[i]) break;
+          if (++od[i] < int(p.dim_o[i])) break;
           od[i] = 0;
         }
       }
     };
-    for (int t = 0; t < STAGES - 1 && t < nst; ++t) issue(t);
+    if (issuer)
+      for (int t = 0; t < STAGES - 1 && t < nst; ++t) issue(t);
+    constexpr int PAIRS = BN / 2;                  // column pairs per row
+    constexpr int ROW_STEP = 128 / PAIRS;          // producer threads per pair
+    const int pair = pt % PAIRS, row0 = pt / PAIRS;
     // Scale a stage as soon as its bytes land (consumers are still on the
-    // previous one), then refill the slot the consumers released last.
+    // previous one), then (warp 8) refill the slot the consumers released.
     for (int it = 0; it < nst; ++it) {
       const int s = it % STAGES;
       mbar_wait(&full_tma[s], (it / STAGES) & 1);
       if (NO > 0) {
-        // Khatri-Rao rows: B[k][j] *= prod_o A_o[o][j]; lane owns column
-        // pairs 2*lane and 2*lane + 64
+        // Khatri-Rao rows: B[k][j] *= prod_o A_o[o][j]
         uint8_t* st = smem + s * C::STAGE_BYTES;
         double* b_s = reinterpret_cast<double*>(st + C::A_BYTES);
         const double* p_s = reinterpret_cast<const double*>(st + C::A_BYTES + C::B_BYTES);
-        double2 pa = *reinterpret_cast<const double2*>(p_s + 2 * lane);
-        double2 pb = *reinterpret_cast<const double2*>(p_s + 64 + 2 * lane);
+        double2 pr = *reinterpret_cast<const double2*>(p_s + 2 * pair);
 #pragma unroll
         for (int i = 1; i < NO; ++i) {
-          const double2 qa = *reinterpret_cast<const double2*>(p_s + i * WS_BN + 2 * lane);
-          const double2 qb = *reinterpret_cast<const double2*>(p_s + i * WS_BN + 64 + 2 * lane);
-          pa.x *= qa.x;
-          pa.y *= qa.y;
-          pb.x *= qb.x;
-          pb.y *= qb.y;
+          const double2 v = *reinterpret_cast<const double2*>(p_s + i * BN + 2 * pair);
+          pr.x *= v.x;
+          pr.y *= v.y;
         }
-#pragma unroll 8
-        for (int k = 0; k < WS_BK; ++k) {
-          double2* ra = reinterpret_cast<double2*>(b_s + k * WS_BN + 2 * lane);
-          double2* rb = reinterpret_cast<double2*>(b_s + k * WS_BN + 64 + 2 * lane);
-          double2 va = *ra, vb = *rb;
-          va.x *= pa.x;
-          va.y *= pa.y;
-          vb.x *= pb.x;
-          vb.y *= pb.y;
-          *ra = va;
-          *rb = vb;
+#pragma unroll 4
+        for (int k = row0; k < BK; k += ROW_STEP) {
+          double2* rp = reinterpret_cast<double2*>(b_s + k * BN + 2 * pair);
+          double2 v = *rp;
+          v.x *= pr.x;
+          v.y *= pr.y;
+          *rp = v;
         }
         // generic-proxy writes must be ordered before the next TMA into this buffer
         fence_proxy_async();
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&full[s]);
-      if (it + STAGES - 1 < nst) issue(it + STAGES - 1);
+      if (issuer && it + STAGES - 1 < nst) issue(it + STAGES - 1);
     }
     return;
   }
 
   // ================================================================== consumers
-  setmaxnreg_inc<WS_CONSUMER_REGS>();
-  constexpr int TY = WS_BM / 8, TX = WS_BN / 8;  // 16 x 16 threads, 8x8 each
+  setmaxnreg_inc<WsRegs<TM>::consumer>();
   constexpr int WX = 8, WY = 4, WARPS_X = TX / WX;
   const int ty = (warp / WARPS_X) * WY + lane / WX;
   const int tx = (warp % WARPS_X) * WX + lane % WX;
 
-  double acc[8][8];
+  double acc[TM][8];
 #pragma unroll
-  for (int r = 0; r < 8; ++r)
+  for (int r = 0; r < TM; ++r)
 #pragma unroll
     for (int c = 0; c < 8; ++c) acc[r][c] = 0.0;
 
@@ -303,42 +313,81 @@ __global__ void __launch_bounds__(WS_THREADS, 1) mttkrp_f64_ws_sm100(const __gri
     const uint8_t* st = smem + s * C::STAGE_BYTES;
     const double* a_s = reinterpret_cast<const double*>(st);
     const double* b_s = reinterpret_cast<const double*>(st + C::A_BYTES);
+    if constexpr (TM == 8) {
+      // k pairs: one LDS.128 gives (m, k..k+1) in the K-major layout
 #pragma unroll 4
-    for (int kk = 0; kk < WS_BK; kk += 2) {
-      double a[8][2];
-      if (KMAJ) {
-        const double* panel = a_s + (kk >> 4) * (WS_BM * 16);
-        const int chunk = (kk & 15) >> 1;
+      for (int kk = 0; kk < BK; kk += 2) {
+        double a[8][2];
+        if (KMAJ) {
+          const double* panel = a_s + (kk >> 4) * (BM * 16);
+          const int chunk = (kk & 15) >> 1;
 #pragma unroll
-        for (int r = 0; r < 8; ++r) {
-          const int m = 2 * ty + (r & 1) + 2 * TY * (r >> 1);
-          const double2 v = *reinterpret_cast<const double2*>(panel + m * 16 + ((chunk ^ (m & 7)) << 1));
-          a[r][0] = v.x;
-          a[r][1] = v.y;
+          for (int r = 0; r < 8; ++r) {
+            const int m = 2 * ty + (r & 1) + 2 * TY * (r >> 1);
+            const double2 v = *reinterpret_cast<const double2*>(panel + m * 16 + ((chunk ^ (m & 7)) << 1));
+            a[r][0] = v.x;
+            a[r][1] = v.y;
+          }
+        } else {
+#pragma unroll
+          for (int kq = 0; kq < 2; ++kq)
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const double2 v = *reinterpret_cast<const double2*>(a_s + (kk + kq) * BM + 2 * ty + 2 * TY * i);
+              a[2 * i][kq] = v.x;
+              a[2 * i + 1][kq] = v.y;
+            }
         }
-      } else {
 #pragma unroll
-        for (int kq = 0; kq < 2; ++kq)
+        for (int kq = 0; kq < 2; ++kq) {
+          double b[8];
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
-            const double2 v = *reinterpret_cast<const double2*>(a_s + (kk + kq) * WS_BM + 2 * ty + 2 * TY * i);
-            a[2 * i][kq] = v.x;
-            a[2 * i + 1][kq] = v.y;
+            const double2 v = *reinterpret_cast<const double2*>(b_s + (kk + kq) * BN + 2 * tx + 2 * TX * i);
+            b[2 * i] = v.x;
+            b[2 * i + 1] = v.y;
           }
-      }
 #pragma unroll
-      for (int kq = 0; kq < 2; ++kq) {
+          for (int r = 0; r < 8; ++r)
+#pragma unroll
+            for (int c = 0; c < 8; ++c) acc[r][c] = fma(a[r][kq], b[c], acc[r][c]);
+        }
+      }
+    } else {
+      // single k: B fragment first, then the TM rows streamed through.  Rows
+      // 2ty+p+2TY*i share (m & 7) across i, so the swizzled column offset is
+      // one value per (k, p) and the row offsets are compile-time strides.
+      const double* arow0 = a_s + (2 * ty) * 16;
+      const double* arow1 = arow0 + 16;
+      const int swz0 = (2 * ty) & 7, swz1 = (2 * ty + 1) & 7;
+#pragma unroll 1
+      for (int k = 0; k < BK; ++k) {
         double b[8];
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-          const double2 v = *reinterpret_cast<const double2*>(b_s + (kk + kq) * WS_BN + 2 * tx + 2 * TX * i);
+          const double2 v = *reinterpret_cast<const double2*>(b_s + k * BN + 2 * tx + 2 * TX * i);
           b[2 * i] = v.x;
           b[2 * i + 1] = v.y;
         }
 #pragma unroll
-        for (int r = 0; r < 8; ++r)
+        for (int i = 0; i < TM / 2; ++i) {
+          double a0, a1;
+          if (KMAJ) {
+            static_assert(!KMAJ || (2 * TY) % 8 == 0, "row stride keeps the swizzle phase");
+            const int pofs = (k >> 4) * (BM * 16) + 2 * TY * 16 * i;
+            const int chunk = (k & 15) >> 1, odd = k & 1;
+            a0 = arow0[pofs + ((chunk ^ swz0) << 1) + odd];
+            a1 = arow1[pofs + ((chunk ^ swz1) << 1) + odd];
+          } else {
+            const double2 v = *reinterpret_cast<const double2*>(a_s + k * BM + 2 * ty + 2 * TY * i);
+            a0 = v.x;
+            a1 = v.y;
+          }
 #pragma unroll
-          for (int c = 0; c < 8; ++c) acc[r][c] = fma(a[r][kq], b[c], acc[r][c]);
+          for (int c = 0; c < 8; ++c) acc[2 * i][c] = fma(a0, b[c], acc[2 * i][c]);
+#pragma unroll
+          for (int c = 0; c < 8; ++c) acc[2 * i + 1][c] = fma(a1, b[c], acc[2 * i + 1][c]);
+        }
       }
     }
     __syncwarp();
@@ -349,7 +398,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) mttkrp_f64_ws_sm100(const __gri
   double* out = p.out + int64_t(blockIdx.z) * p.out_split_stride;
   const bool fold = p.lam != nullptr;
 #pragma unroll
-  for (int r = 0; r < 8; ++r) {
+  for (int r = 0; r < TM; ++r) {
     const int n = n0 + 2 * ty + (r & 1) + 2 * TY * (r >> 1);
     if (n >= p.Ik) continue;
 #pragma unroll
@@ -397,17 +446,45 @@ static int encode(CUtensorMap* map, const void* base, int rank, const cuuint64_t
   return CPK_OK;
 }
 
-template <bool KMAJ, int NO>
-static void ws_kernel(const void** fn, size_t* smem, int* stages) {
-  constexpr int S = (3 * WsCfg<KMAJ, NO, 3>::STAGE_BYTES + 256 <= 227 * 1024) ? 3 : 2;
-  *fn = reinterpret_cast<const void*>(&mttkrp_f64_ws_sm100<KMAJ, NO, S>);
-  *smem = WsCfg<KMAJ, NO, S>::SMEM;
-  *stages = S;
+template <bool KMAJ, int NO, int TM, int BN, int BK>
+static void ws_kernel(const void** fn, size_t* smem) {
+  constexpr int stage = WsCfg<KMAJ, NO, TM, BN, BK, 1>::STAGE_BYTES;
+  constexpr int fit = (227 * 1024 - 256) / stage;
+  constexpr int S = fit > 4 ? 4 : fit;
+  static_assert(S >= 2, "two stages must fit");
+  *fn = reinterpret_cast<const void*>(&mttkrp_f64_ws_sm100<KMAJ, NO, TM, BN, BK, S>);
+  *smem = WsCfg<KMAJ, NO, TM, BN, BK, S>::SMEM;
+}
+
+template <int TM, int BN, int BK>
+static void ws_pick(bool kmaj, int no, const void** fn, size_t* smem) {
+  if (kmaj) {
+    if (no == 0) ws_kernel<true, 0, TM, BN, BK>(fn, smem);
+    else if (no == 1) ws_kernel<true, 1, TM, BN, BK>(fn, smem);
+    else if (no == 2) ws_kernel<true, 2, TM, BN, BK>(fn, smem);
+    else ws_kernel<true, 3, TM, BN, BK>(fn, smem);
+  } else {
+    if (no == 0) ws_kernel<false, 0, TM, BN, BK>(fn, smem);
+    else if (no == 1) ws_kernel<false, 1, TM, BN, BK>(fn, smem);
+    else if (no == 2) ws_kernel<false, 2, TM, BN, BK>(fn, smem);
+    else ws_kernel<false, 3, TM, BN, BK>(fn, smem);
+  }
+}
+
+bool ws_shape(int rank_tile, int* block_rows, int* block_k) {
+  switch (rank_tile) {
+    case 64: *block_rows = 256; *block_k = 16; return true;   // TM 8
+    case 128: *block_rows = 128; *block_k = 32; return true;  // TM 8
+    case 256: *block_rows = 96; *block_k = 16; return true;   // TM 12
+    default: return false;
+  }
 }
 
 bool ws_eligible(const WsRequest& r) {
+  int bm, bk;
+  if (!ws_shape(r.rank_tile, &bm, &bk)) return false;
   if (r.d < 2 || r.d > 5 || r.n_o > 3) return false;
-  if (r.rank_tile != WS_BN || r.block_k != WS_BK) return false;
+  if (r.block_k != bk) return false;
   if (r.dims[0] % 2 != 0) return false;
   for (int m = 0; m < r.d; ++m)
     if (r.dims[m] >= (int64_t(1) << 31)) return false;
@@ -420,6 +497,9 @@ bool ws_eligible(const WsRequest& r) {
 }
 
 int launch_ws(const WsRequest& r, cudaStream_t st) {
+  int BM, BK;
+  if (!ws_shape(r.rank_tile, &BM, &BK)) return fail(CPK_ERR_PARAM, "no TMA tile for rank_tile %d", r.rank_tile);
+  const int BN = r.rank_tile;
   WsParams p;
   memset(&p, 0, sizeof(p));
   const int d = r.d, k = r.k, f = k == 0 ? 1 : 0;
@@ -434,20 +514,20 @@ int launch_ws(const WsRequest& r, cudaStream_t st) {
   int rc;
   if (k == 0) {
     for (int m = 0; m < d; ++m) box[m] = 1;
-    box[0] = WS_BM;
-    box[1] = WS_BK;
+    box[0] = cuuint32_t(BM);
+    box[1] = cuuint32_t(BK);
     rc = encode(&p.tm_y, r.y, d, gdim, gstr, box, CU_TENSOR_MAP_SWIZZLE_NONE);
   } else {
     for (int m = 0; m < d; ++m) box[m] = 1;
     box[0] = 16;
-    box[k] = WS_BM;
+    box[k] = cuuint32_t(BM);
     rc = encode(&p.tm_y, r.y, d, gdim, gstr, box, CU_TENSOR_MAP_SWIZZLE_128B);
   }
   if (rc) return rc;
   {
     const cuuint64_t fd[2] = {cuuint64_t(r.rank), cuuint64_t(r.dims[f])};
     const cuuint64_t fs[1] = {cuuint64_t(r.ld[f] * 8)};
-    const cuuint32_t fb[2] = {WS_BN, WS_BK};
+    const cuuint32_t fb[2] = {cuuint32_t(BN), cuuint32_t(BK)};
     rc = encode(&p.tm_f, r.factors[f], 2, fd, fs, fb, CU_TENSOR_MAP_SWIZZLE_NONE);
     if (rc) return rc;
   }
@@ -456,13 +536,13 @@ int launch_ws(const WsRequest& r, cudaStream_t st) {
     if (m == k || m == f) continue;
     const cuuint64_t od[2] = {cuuint64_t(r.rank), cuuint64_t(r.dims[m])};
     const cuuint64_t os[1] = {cuuint64_t(r.ld[m] * 8)};
-    const cuuint32_t ob[2] = {WS_BN, 1};
+    const cuuint32_t ob[2] = {cuuint32_t(BN), 1};
     rc = encode(&p.tm_o[oi], r.factors[m], 2, od, os, ob, CU_TENSOR_MAP_SWIZZLE_NONE);
     if (rc) return rc;
     p.dim_o[oi] = r.dims[m];
     ++oi;
   }
-  p.chunks_per_f = (r.dims[f] + WS_BK - 1) / WS_BK;
+  p.chunks_per_f = (r.dims[f] + BK - 1) / BK;
   p.n_chunks = p.chunks_per_f;
   for (int i = 0; i < oi; ++i) p.n_chunks *= p.dim_o[i];
   p.chunks_per_split = (p.n_chunks + r.splits - 1) / r.splits;
@@ -477,22 +557,14 @@ int launch_ws(const WsRequest& r, cudaStream_t st) {
 
   const void* fn = nullptr;
   size_t smem = 0;
-  int stages = 0;
+  const bool kmaj = k != 0;
   const int no = r.n_o;
-  if (k == 0) {
-    if (no == 0) ws_kernel<false, 0>(&fn, &smem, &stages);
-    else if (no == 1) ws_kernel<false, 1>(&fn, &smem, &stages);
-    else if (no == 2) ws_kernel<false, 2>(&fn, &smem, &stages);
-    else ws_kernel<false, 3>(&fn, &smem, &stages);
-  } else {
-    if (no == 0) ws_kernel<true, 0>(&fn, &smem, &stages);
-    else if (no == 1) ws_kernel<true, 1>(&fn, &smem, &stages);
-    else if (no == 2) ws_kernel<true, 2>(&fn, &smem, &stages);
-    else ws_kernel<true, 3>(&fn, &smem, &stages);
-  }
+  if (BN == 128) ws_pick<8, 128, 32>(kmaj, no, &fn, &smem);
+  else if (BN == 256) ws_pick<12, 256, 16>(kmaj, no, &fn, &smem);
+  else ws_pick<8, 64, 16>(kmaj, no, &fn, &smem);
   if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) != cudaSuccess)
     return check_launch("ws set smem");
-  const int64_t gx = (r.rank + WS_BN - 1) / WS_BN, gy = (r.dims[k] + WS_BM - 1) / WS_BM;
+  const int64_t gx = (r.rank + BN - 1) / BN, gy = (r.dims[k] + BM - 1) / BM;
   dim3 grid(unsigned(gx), unsigned(gy), unsigned(r.splits));
   void* args[] = {&p};
   cudaError_t e = cudaLaunchKernel(fn, grid, dim3(WS_THREADS), args, smem, st);
