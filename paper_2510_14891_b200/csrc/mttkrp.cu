@@ -510,8 +510,8 @@ struct TileChoice {
   double rate;
 };
 static const TileChoice kChoices[] = {
-    {CPK_ENGINE_TMA, 256, 1.10}, {CPK_ENGINE_TMA, 128, 1.00}, {CPK_ENGINE_TMA, 64, 0.93},
-    {CPK_ENGINE_CPASYNC, 128, 0.93}, {CPK_ENGINE_CPASYNC, 64, 0.90}, {CPK_ENGINE_CPASYNC, 32, 0.60},
+    {CPK_ENGINE_TMA, 256, 0.95}, {CPK_ENGINE_TMA, 128, 1.00}, {CPK_ENGINE_TMA, 64, 0.93},
+    {CPK_ENGINE_CPASYNC, 128, 0.92}, {CPK_ENGINE_CPASYNC, 64, 0.78}, {CPK_ENGINE_CPASYNC, 32, 0.55},
 };
 
 static int rows_for(int engine, int rank_tile, int* bm, int* bk_fixed) {

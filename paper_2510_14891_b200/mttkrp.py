@@ -58,7 +58,7 @@ class MttkrpPlan:
     ``unroll`` (F), ``team_width`` (b_x) and ``vector_width`` (b_y) keep the
     paper's meaning; on the GPU the column block is the rank tile, so they
     are validated (>= 1) but the kernel's register tile is fixed at 8x8.
-    ``rank_tile`` (0 = auto, else 32/64/128), ``splits`` (0 = auto) and
+    ``rank_tile`` (0 = auto, else 32/64/128/256), ``splits`` (0 = auto) and
     ``block_k`` (chunk depth, 0 = auto, else 16/32) are the B200
     realization of the rank tiling and of N_T; ``engine`` picks the data
     movement ("auto", "tma" = warp-specialized TMA kernel, "cpasync").  ``workers`` is
@@ -87,8 +87,8 @@ class MttkrpPlan:
             raise ParameterError("team_width and vector_width must be >= 1")
         if rank < 1:
             raise ParameterError(f"rank must be >= 1, got {rank}")
-        if self.rank_tile not in (0, 32, 64, 128):
-            raise ParameterError(f"rank_tile must be 0, 32, 64 or 128, got {self.rank_tile}")
+        if self.rank_tile not in (0, 32, 64, 128, 256):
+            raise ParameterError(f"rank_tile must be 0, 32, 64, 128 or 256, got {self.rank_tile}")
         if self.splits < 0:
             raise ParameterError(f"splits must be >= 0, got {self.splits}")
         if self.engine not in _ENGINES:
@@ -362,19 +362,32 @@ def heuristic_tile_volume(dims, machine) -> int:
     return heuristic_tile_width(dims, machine) ** (len(dims) - 1)
 
 
-def heuristic_rank_tile(rank: int, machine=None) -> int:
-    """Rank tile: the B200 analogue of the paper's column-block choice.
+# (engine, rank tile, rows per CTA, relative DFMA rate) -- mirrors kChoices in
+# csrc/mttkrp.cu; rates from the B200 sweeps (profiles/r01_sweep_*.agg.csv)
+_TILE_CHOICES = (
+    ("tma", 256, 96, 0.95), ("tma", 128, 128, 1.00), ("tma", 64, 256, 0.93),
+    ("cpasync", 128, 128, 0.92), ("cpasync", 64, 128, 0.78), ("cpasync", 32, 64, 0.55),
+)
 
-    The kernel keeps an 8 x 8 FP64 accumulator tile per thread (the register
-    file is the private level that bounds the rank tile, as the L1 bounds the
-    tile volume in Eq. 6), giving BN in {32, 64, 128} for BM in {64, 128,
-    128}.  Wider tiles stage fewer bytes per DFMA, (BM + BN) / (BM BN), so
-    the choice maximizes useful/padded columns x tile efficiency
-    {128: 1.0, 64: 0.93, 32: 0.8}.  Mirrors resolve() in csrc/mttkrp.cu.
+
+def heuristic_rank_tile(rank: int, rows: int | None = None, tma: bool = True) -> tuple:
+    """(engine, rank tile) the planner picks: the B200 analogue of Eq. 6.
+
+    Eq. 6 sizes N_T so tensor elements fill a quarter of the private cache
+    (PAPER.md:405-409).  On B200 the private level that bounds the *rank*
+    tile is the register file: each consumer thread keeps a TM x 8 FP64
+    accumulator tile (TM = 8 or 12), 256 threads per CTA, so the rank tile
+    is 64, 128 or 256 columns with 256, 128 or 96 rows.  The planner picks
+    the (engine, tile) minimizing padded rows x padded columns / measured
+    rate; `tma` is whether the problem is TMA-eligible (even I_0 and R,
+    2 <= d <= 5).  Mirrors resolve() in csrc/mttkrp.cu.
     """
-    best, best_score = 128, -1.0
-    for rt, w in ((128, 1.0), (64, 0.93), (32, 0.8)):
-        score = rank / (-(-rank // rt) * rt) * w
-        if score > best_score + 1e-12:
-            best, best_score = rt, score
+    rows = rows or 1
+    best, best_cost = None, float("inf")
+    for eng, rt, bm, rate in _TILE_CHOICES:
+        if eng == "tma" and not tma:
+            continue
+        cost = (-(-rows // bm) * bm) * (-(-rank // rt) * rt) / rate
+        if cost < best_cost * (1 - 1e-9):
+            best, best_cost = (eng, rt), cost
     return best

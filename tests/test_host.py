@@ -1,0 +1,132 @@
+"""Host-side logic (no GPU): plans, heuristics, machine specs, data model,
+error classes -- the reference's own host tests (test_mttkrp.py:306-394,
+test_perfmodel.py) restated against the drop-in package."""
+
+import numpy as np
+import pytest
+
+import paper_2510_14891_b200 as ck
+from paper_2510_14891_b200 import _lib
+from paper_2510_14891_b200.mttkrp import MttkrpPlan, Variant, heuristic_rank_tile, plan_for_mode
+
+
+def test_heuristic_pinned_values():
+    # test_mttkrp.py:316-328 (Eq. 6 with the reference's machine specs)
+    h100 = ck.bundled_machine("nvidia-h100")
+    intel = ck.bundled_machine("intel-8480p")
+    island = (129, 129, 129, 12, 39)
+    tearing = (401, 201, 12, 501)
+    assert ck.heuristic_tile_width(island, h100) == 4
+    assert ck.heuristic_tile_volume(island, h100) == 256
+    assert ck.heuristic_tile_width(island, intel) == 12
+    assert ck.heuristic_tile_volume(island, intel) == 20736
+    assert ck.heuristic_tile_width(tearing, intel) == 12
+    assert ck.heuristic_tile_volume(tearing, intel) == 1728
+    b200 = ck.bundled_machine("nvidia-b200")
+    assert ck.heuristic_tile_width((1024, 1024, 1024), b200) == 22
+    assert ck.heuristic_tile_width((128, 128, 128, 128), b200) == 8
+
+
+def test_heuristic_degenerate_and_bounds():
+    h100 = ck.bundled_machine("nvidia-h100")
+    assert ck.heuristic_tile_width((1, 1000, 1000), h100) == 1
+    big = ck.MachineSpec("t", 1.0, 1.0, 1.0, 2 ** 40, 1, 8, 1)
+    assert ck.heuristic_tile_width((5, 6, 7), big) == 5
+    tiny = ck.MachineSpec("t", 1.0, 1.0, 1.0, 1, 1, 8, 1)
+    assert ck.heuristic_tile_width((5, 6, 7), tiny) == 1
+    with pytest.raises(ck.ParameterError):
+        ck.heuristic_tile_width((5,), h100)
+
+
+@pytest.mark.parametrize("s_lm", [4096, 65536, 2 ** 21, 2 ** 24])
+@pytest.mark.parametrize("d", [2, 3, 4, 5])
+def test_heuristic_width_is_exact_floor(s_lm, d):
+    mach = ck.MachineSpec("t", 1.0, 1.0, 1.0, s_lm, 2, 8, 1)
+    w = ck.heuristic_tile_width((10 ** 6,) * d, mach)
+    budget = (s_lm / 4) / (8 * 1.0)
+    assert w ** (d - 1) <= budget < (w + 1) ** (d - 1)
+
+
+@pytest.mark.parametrize("rows", [64, 96, 128, 512, 1000, 1024, 2048, 4096])
+@pytest.mark.parametrize("rank", [1, 16, 33, 64, 100, 130, 256, 300, 512, 2000])
+def test_rank_tile_heuristic_mirrors_the_c_planner(rows, rank):
+    for tma in (True, False):
+        dims = (rows, 64, 66) if tma else (rows + 1, 64, 66)  # odd I_0 disables TMA
+        r = rank if (not tma or rank % 2 == 0) else rank + 1
+        eng, rt = heuristic_rank_tile(r, dims[0], tma=tma)
+        p = _lib.CpkPlan(0, 0, 0, 0, 148, 0, 0)
+        _lib.check(_lib.load().cpk_plan_resolve(3, _lib.i64_array(dims), 0, r, p))
+        assert (p.rank_tile, p.engine) == (rt, {"tma": 2, "cpasync": 1}[eng]), (dims, r)
+
+
+def test_plan_for_mode_clamps_tile_volume():
+    plan = MttkrpPlan(Variant.TILE, 0, tile_volume=40)
+    p0 = plan_for_mode(plan, (10, 3, 4), 0)
+    assert p0.tile_volume == 12
+    p1 = plan_for_mode(plan, (10, 3, 4), 1)
+    assert p1.tile_volume == 40 and p1.mode == 1
+
+
+def test_plan_validation():
+    dims, rank = (4, 5, 6), 2
+    for bad in [MttkrpPlan(Variant.SLICE, 3), MttkrpPlan(Variant.SLICE, 0, unroll=0),
+                MttkrpPlan(Variant.TILE, 0), MttkrpPlan(Variant.TILE, 0, tile_volume=31),
+                MttkrpPlan(Variant.TILE, 0, tile_volume=0), MttkrpPlan(Variant.B200, 0, rank_tile=48),
+                MttkrpPlan(Variant.B200, 0, block_k=8), MttkrpPlan(Variant.B200, 0, engine="x"),
+                MttkrpPlan(Variant.B200, 0, splits=-1)]:
+        with pytest.raises(ck.CpkernError):
+            bad.validate(dims, rank)
+    with pytest.raises(ck.ParameterError):
+        MttkrpPlan(Variant.B200, 0).validate(dims, 0)
+    MttkrpPlan(Variant.TILE, 0, tile_volume=30).validate(dims, rank)
+
+
+def test_machine_specs_and_work_model():
+    assert ck.bundled_machine_names() == ["intel-8480p", "nvidia-b200", "nvidia-h100"]
+    b = ck.bundled_machine("nvidia-b200")
+    assert b.tau_m == 6508.2e9 and b.s_f_bytes == 8
+    with pytest.raises(ck.ParameterError):
+        ck.bundled_machine("nope")
+    assert ck.flops((2, 3, 4), 5) == 24 * 5 * 3
+    assert ck.algorithmic_flops((1024,) * 3, 2000) == 2 * 1024 ** 3 * 2000 * 2
+    # c4: FP64-bound, 230.8 ms per mode at the nominal 37.2 TFLOP/s
+    assert abs(ck.roofline_seconds((1024,) * 3, 2000) - 0.2308) < 1e-3
+    with pytest.raises(ck.FormatError):
+        from paper_2510_14891_b200.perfmodel import machine_from_dict
+
+        machine_from_dict({"name": "x"})
+
+
+def test_dense_tensor_contract():
+    y = ck.DenseTensor.from_ndarray(np.arange(24.0).reshape(2, 3, 4))
+    assert y.dims == (2, 3, 4) and y.size == 24
+    assert np.array_equal(y.to_ndarray(), np.arange(24.0).reshape(2, 3, 4))
+    assert ck.col_major_strides((2, 3, 4)) == (1, 2, 6)
+    with pytest.raises(ck.ShapeError):
+        ck.DenseTensor((2, 3), np.zeros(5))
+    with pytest.raises(ck.ShapeError):
+        ck.check_dims((2, 0))
+    with pytest.raises(ck.ShapeError):
+        ck.KruskalTensor(np.ones(2), [np.ones((3, 2)), np.ones((4, 3))])
+    with pytest.raises(ck.ShapeError):
+        ck.KruskalTensor(-np.ones(2), [np.ones((3, 2))])
+
+
+def test_error_hierarchy_matches_reference():
+    assert issubclass(ck.ShapeError, ValueError) and issubclass(ck.ShapeError, ck.CpkernError)
+    assert issubclass(ck.IndexRangeError, IndexError)
+    assert issubclass(ck.ResourceError, RuntimeError)
+    assert issubclass(ck.DeviceError, ck.CpkernError)
+
+
+def test_no_cpu_fallback():
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("has a GPU")
+    y = ck.DenseTensor((4, 5, 6), np.ones(120))
+    m = ck.KruskalTensor(np.ones(2), [np.ones((n, 2)) for n in (4, 5, 6)])
+    with pytest.raises(ck.DeviceError):
+        ck.run(y, m, MttkrpPlan(Variant.B200, 0))
+    with pytest.raises(ck.DeviceError):
+        ck.cp_als(y, ck.AlsConfig(rank=2))
