@@ -186,7 +186,7 @@ def run_b200(args):
 
     import paper_2510_14891_b200 as ck
     from paper_2510_14891_b200 import _lib
-    from paper_2510_14891_b200.mttkrp import MttkrpPlan, Variant, mttkrp_device
+    from paper_2510_14891_b200.mttkrp import MttkrpPlan, Variant, mttkrp_device, resolve_plan
     from oracle import gen
 
     # ---- inputs resident in HBM: this rank's mode-0 slab of config 4
@@ -248,6 +248,28 @@ def run_b200(args):
         elapsed = float(tt.item())
     per_mode = [statistics.median(mode_events[s][k][0].elapsed_time(mode_events[s][k][1]) for s in range(args.steps))
                 for k in range(3)]
+    plans = [resolve_plan(MttkrpPlan(Variant.B200, k), local_dims, RANK) for k in range(3)]
+
+    # ---- the same step with the DFMA (CUDA-core FMA) consumers, for the
+    # north star's literal math choice; not part of `value`
+    dfma = None
+    if args.dfma_steps > 0:
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(3)]
+        ms = [[] for _ in range(3)]
+        for it in range(args.dfma_steps + 1):
+            for k in range(3):
+                ev[k][0].record()
+                mttkrp_device(y, local_dims, fs, k, None, MttkrpPlan(Variant.B200, k, engine="tma"))
+                ev[k][1].record()
+            torch.cuda.synchronize()
+            if it > 0:  # first pass warms the kernels up
+                for k in range(3):
+                    ms[k].append(ev[k][0].elapsed_time(ev[k][1]))
+        dfma_mode = [statistics.median(m) for m in ms]
+        dplan = resolve_plan(MttkrpPlan(Variant.B200, 0, engine="tma"), local_dims, RANK)
+        dfma = {"engine": "tma (DFMA outer products, warp-specialized TMA)", "rank_tile": dplan["rank_tile"],
+                "per_mode_ms": dfma_mode,
+                "gflops": algo_flops(local_dims, RANK) * 3 / (sum(dfma_mode) * 1e-3) / 1e9}
 
     total_flops = algo_flops(DIMS, RANK) * 3 * args.steps
     value = total_flops / elapsed / 1e9
@@ -300,6 +322,8 @@ def run_b200(args):
     flops_per_launch = algo_flops(local_dims, RANK)  # one mode
     mean_launch_s = statistics.mean(per_mode) * 1e-3
     achieved = flops_per_launch / mean_launch_s
+    rt = plans[0]["rank_tile"]
+    padded_rank = -(-RANK // rt) * rt
     traffic = None
     if NCU_SUMMARY.exists():
         try:
@@ -348,14 +372,17 @@ def run_b200(args):
             "paper_gflops": int(np.prod(DIMS)) * RANK * 3 * 3 * args.steps / elapsed / 1024 ** 3,
             "roofline": {"bound": "fp64", "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "TFLOP/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "peak_source": "cpk_fp64_peak_probe (register DFMA loop, this run)" if fp64_peak else
-                         "nominal 148 SM x 64 DFMA/clk x 2 x 1.965 GHz",
+                         "peak_source": "cpk_fp64_peak_probe (max of register DFMA and DMMA loops, this run)"
+                         if fp64_peak else "nominal 148 SM x 64 FP64 FMA/clk x 2 x 1.965 GHz",
                          "nominal_peak": nominal / 1e12,
-                         "kernel": "mttkrp_f64_sm100 + splitk_reduce_f64 (per mode launch)",
+                         "kernel": "mttkrp_f64_ws_sm100 (TMA + DMMA consumers) + splitk_reduce_f64, per mode",
+                         "plans": [{key: p[key] for key in ("engine", "rank_tile", "block_rows", "block_k", "splits")}
+                                   for p in plans],
                          "flops_per_launch": flops_per_launch,
-                         "issued_dfma_frac": (int(np.prod(local_dims)) * 2 * 2048 / mean_launch_s) / peak,
+                         "issued_fp64_frac": (int(np.prod(local_dims)) * 2 * padded_rank / mean_launch_s) / peak,
                          "north_star_roofline_ms_per_mode": roof_t * 1e3,
                          "north_star_frac": roof_t * 3 * args.steps / elapsed},
+            "dfma_engine": dfma,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": 6 * args.steps,
@@ -425,6 +452,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--dfma-steps", type=int, default=2)
     ap.add_argument("--cpals-iters", type=int, default=5)
     ap.add_argument("--c5-iters", type=int, default=3)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)

@@ -64,12 +64,16 @@ typedef struct cpk_plan {
   int32_t engine;       /* CPK_ENGINE_*: data-movement engine          */
 } cpk_plan;
 
-/* engine: AUTO picks the warp-specialized TMA kernel when the problem is
- * aligned (rank tile 128, chunk depth 32, even I_0 and leading dimensions,
- * 16-byte aligned bases, d <= 5), else the cp.async kernel. */
+/* engine: AUTO picks the warp-specialized TMA kernel with DMMA consumers
+ * when the problem is aligned (even I_0 and leading dimensions, 16-byte
+ * aligned bases, d <= 5), else the cp.async kernel; the rank tile minimizes
+ * padded work / measured rate (cpk_plan_resolve). */
 #define CPK_ENGINE_AUTO 0
 #define CPK_ENGINE_CPASYNC 1
 #define CPK_ENGINE_TMA 2
+/* TMA data movement (as CPK_ENGINE_TMA) with the FP64 math on mma.sync
+ * m8n8k4 f64 (DMMA) instead of DFMA outer products; rank tiles 64/128/256. */
+#define CPK_ENGINE_DMMA 3
 
 /* Last error message of the calling thread (never NULL). */
 const char* cpk_last_error(void);
@@ -169,9 +173,10 @@ int cpk_fill_uniform_slab_f64(double* x, int d, const int64_t* global_dims,
                               int mode, int64_t lo, int64_t hi, uint64_t seed,
                               void* stream);
 
-/* Device-side DFMA throughput probe: returns achieved FP64 FLOP/s of a
- * register-resident FMA loop over the whole chip (the FP64 roofline peak;
- * MEASURED_PEAKS.json has no FP64 figure).  Synchronous. */
+/* Device-side FP64 pipe probe: the larger achieved FLOP/s of a
+ * register-resident DFMA loop and a register-resident DMMA (mma.sync
+ * m8n8k4 f64) loop over the whole chip -- the FP64 roofline peak
+ * (MEASURED_PEAKS.json has no FP64 figure).  Synchronous. */
 int cpk_fp64_peak_probe(double* flops_per_s, double* seconds);
 
 #ifdef __cplusplus

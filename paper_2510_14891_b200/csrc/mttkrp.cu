@@ -503,21 +503,26 @@ static bool tma_possible(const Problem& pr) {
   return true;
 }
 
-// Relative DFMA efficiency of each (engine, rank tile), from the c2/c4 sweeps
-// (profiles/r01_sweep_*.agg.csv); the auto plan minimizes padded work / rate.
+// Relative FP64 efficiency of each (engine, rank tile) against the DFMA TMA
+// kernel at tile 128, from the c2-c5 sweeps (profiles/r01_sweep_*.agg.csv,
+// profiles/r01_sweep_*_dmma.agg.csv); the auto plan minimizes padded work /
+// rate.  A rate of 0 would make an engine explicit-only.
 struct TileChoice {
   int engine, rank_tile;
   double rate;
 };
 static const TileChoice kChoices[] = {
     {CPK_ENGINE_TMA, 256, 0.95}, {CPK_ENGINE_TMA, 128, 1.00}, {CPK_ENGINE_TMA, 64, 0.93},
+    {CPK_ENGINE_DMMA, 256, 1.02}, {CPK_ENGINE_DMMA, 128, 1.19}, {CPK_ENGINE_DMMA, 64, 1.26},
     {CPK_ENGINE_CPASYNC, 128, 0.92}, {CPK_ENGINE_CPASYNC, 64, 0.78}, {CPK_ENGINE_CPASYNC, 32, 0.55},
 };
 
+static bool is_tma(int engine) { return engine == CPK_ENGINE_TMA || engine == CPK_ENGINE_DMMA; }
+
 static int rows_for(int engine, int rank_tile, int* bm, int* bk_fixed) {
-  if (engine == CPK_ENGINE_TMA) {
+  if (is_tma(engine)) {
     int bk;
-    if (!ws_shape(rank_tile, bm, &bk)) return fail(CPK_ERR_PARAM, "TMA engine has no rank_tile %d tile", rank_tile);
+    if (!ws_shape(rank_tile, engine == CPK_ENGINE_DMMA ? WS_MATH_DMMA : WS_MATH_DFMA, bm, &bk)) return fail(CPK_ERR_PARAM, "TMA engine has no rank_tile %d tile", rank_tile);
     *bk_fixed = bk;
     return CPK_OK;
   }
@@ -529,8 +534,8 @@ static int rows_for(int engine, int rank_tile, int* bm, int* bk_fixed) {
 }
 
 static int resolve(const Problem& pr, cpk_plan* plan) {
-  if (plan->engine < CPK_ENGINE_AUTO || plan->engine > CPK_ENGINE_TMA)
-    return fail(CPK_ERR_PARAM, "engine must be 0 (auto), 1 (cp.async) or 2 (TMA)");
+  if (plan->engine < CPK_ENGINE_AUTO || plan->engine > CPK_ENGINE_DMMA)
+    return fail(CPK_ERR_PARAM, "engine must be 0 (auto), 1 (cp.async), 2 (TMA) or 3 (TMA + DMMA)");
   const bool tma_ok = tma_possible(pr);
   if (plan->engine == CPK_ENGINE_AUTO || plan->rank_tile == 0) {
     // (engine, rank tile) minimizing padded rows x padded columns / rate
@@ -538,8 +543,9 @@ static int resolve(const Problem& pr, cpk_plan* plan) {
     int best_e = 0, best_rt = 0;
     for (const TileChoice& c : kChoices) {
       if (plan->engine != CPK_ENGINE_AUTO && c.engine != plan->engine) continue;
+      if (plan->engine == CPK_ENGINE_AUTO && c.rate <= 0) continue;  // explicit-only engines
       if (plan->rank_tile != 0 && c.rank_tile != plan->rank_tile) continue;
-      if (c.engine == CPK_ENGINE_TMA && !tma_ok) continue;
+      if (is_tma(c.engine) && !tma_ok) continue;
       int bm, bk;
       if (rows_for(c.engine, c.rank_tile, &bm, &bk)) continue;
       const double cost =
@@ -551,14 +557,14 @@ static int resolve(const Problem& pr, cpk_plan* plan) {
       }
     }
     if (best_e == 0) {
-      if (plan->engine == CPK_ENGINE_TMA && !tma_ok)
+      if (is_tma(plan->engine) && !tma_ok)
         return fail(CPK_ERR_PARAM, "TMA engine needs 2 <= d <= 5, even I_0 and even rank");
       return fail(CPK_ERR_PARAM, "no kernel for rank_tile %d", plan->rank_tile);
     }
     plan->engine = best_e;
     plan->rank_tile = best_rt;
   }
-  if (plan->engine == CPK_ENGINE_TMA && !tma_ok)
+  if (is_tma(plan->engine) && !tma_ok)
     return fail(CPK_ERR_PARAM, "TMA engine needs 2 <= d <= 5, even I_0 and even rank");
   int bm, bk_fixed;
   int rc = rows_for(plan->engine, plan->rank_tile, &bm, &bk_fixed);
@@ -710,8 +716,9 @@ extern "C" int cpk_mttkrp_f64(const double* y, int d, const int64_t* dims, int m
   const int64_t out_split_stride = direct ? 0 : pr.Ik * ldo;
   const double* lam_fold = direct ? lam : nullptr;
 
-  if (plan.engine == CPK_ENGINE_TMA) {
+  if (is_tma(plan.engine)) {
     WsRequest wr{};
+    wr.math = plan.engine == CPK_ENGINE_DMMA ? WS_MATH_DMMA : WS_MATH_DFMA;
     wr.y = y;
     wr.d = d;
     wr.k = mode;
@@ -734,7 +741,7 @@ extern "C" int cpk_mttkrp_f64(const double* y, int d, const int64_t* dims, int m
       if (rc) return rc;
       goto reduce;
     }
-    if (plan_in && plan_in->engine == CPK_ENGINE_TMA)
+    if (plan_in && is_tma(plan_in->engine))
       return fail(CPK_ERR_PARAM, "TMA engine needs even leading dimensions and 16-byte aligned bases");
     // auto plan, misaligned buffers: same splits (same workspace) on cp.async
     plan.engine = CPK_ENGINE_CPASYNC;

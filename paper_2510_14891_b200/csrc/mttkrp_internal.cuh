@@ -9,6 +9,9 @@
 
 namespace cpk {
 
+// FP64 math of the warp-specialized kernel's consumers.
+enum { WS_MATH_DFMA = 0, WS_MATH_DMMA = 1 };
+
 struct WsRequest {
   const double* y;
   int d, k, n_o;
@@ -17,13 +20,14 @@ struct WsRequest {
   int64_t ld[CPK_MAX_MODES];
   int64_t rank;
   int rank_tile, block_k, splits;
+  int math;  // WS_MATH_*
   double* out;
   int64_t ldo, out_split_stride;
   const double* lam;
 };
 
-// TMA tile for a rank tile (64 | 128 | 256): rows per CTA and chunk depth.
-bool ws_shape(int rank_tile, int* block_rows, int* block_k);
+// TMA tile for a rank tile (64 | 128 | 256) and math: rows per CTA and chunk depth.
+bool ws_shape(int rank_tile, int math, int* block_rows, int* block_k);
 bool ws_eligible(const WsRequest& r);
 int launch_ws(const WsRequest& r, cudaStream_t st);
 

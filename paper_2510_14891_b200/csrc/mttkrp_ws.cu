@@ -105,6 +105,15 @@ __device__ __forceinline__ void dfma_ordered(double& d, double a, double b) {
   asm volatile("fma.rn.f64 %0, %1, %2, %0;" : "+d"(d) : "d"(a), "d"(b));
 }
 
+// D += A (8x4, row) * B (4x8, col) on the FP64 tensor path.  Fragments
+// (PTX ISA, mma.m8n8k4 .f64): a = A[lane / 4][lane % 4],
+// b = B[lane % 4][lane / 4], d = D[lane / 4][2 (lane % 4) + {0, 1}].
+__device__ __forceinline__ void dmma_8x8x4(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
+}
+
 template <int RANK>
 __device__ __forceinline__ void tma_load(void* dst, const CUtensorMap* map, uint64_t* bar, const int (&c)[RANK]) {
   const unsigned d = smem_u32(dst), b = smem_u32(bar);
@@ -131,6 +140,117 @@ __device__ __forceinline__ void tma_load(void* dst, const CUtensorMap* map, uint
         : "memory");
 }
 
+// DMMA consumer (TM == 0): warp tile 32 rows x 64 rank columns = 4 x 8
+// m8n8k4 fragments, 64 accumulators per thread.  A DMMA moves 256 FMA per
+// warp instruction against 32 for a DFMA, and its fragments are spread over
+// the lanes without replication, so shared-memory wavefronts per flop fall
+// ~6x below the DFMA outer product and the FP64 pipe (the same pipe: a mixed
+// DFMA + DMMA stream never exceeds the DMMA peak, tools/microbench4.cu)
+// becomes the only limit.  Each 8-deep k block runs as two k-steps, even k
+// then odd k (the contraction order is free), so on the K-major swizzled
+// panels one LDS.128 yields a thread's A fragments for both steps.
+// The main loop over a CTA's chunks.  TAIL: the warp's 64 columns straddle
+// the rank R, so only the first nf_act 8-column fragments do math (the rank
+// tail of R = 2000 at tile 64 is 16 columns: 2 of 8 fragments).
+template <bool KMAJ, bool TAIL, int BM, int BN, int BK, int STAGE_BYTES, int A_BYTES>
+__device__ __forceinline__ void ws_dmma_loop(double (&acc)[4][8][2], const uint8_t* smem, uint64_t* full,
+                                             uint64_t* empty, int nst, int stages, int wm0, int wn0, int lane,
+                                             int nf_act) {
+  const int lr = lane >> 2, lk = lane & 3;
+  for (int it = 0; it < nst; ++it) {
+    const int s = it % stages;
+    mbar_wait(&full[s], (it / stages) & 1);
+    const uint8_t* st = smem + s * STAGE_BYTES;
+    const double* a_s = reinterpret_cast<const double*>(st);
+    const double* b_s = reinterpret_cast<const double*>(st + A_BYTES) + wn0 + lr;
+#pragma unroll 2
+    for (int kk = 0; kk < BK; kk += 8) {
+      double a[4][2], b[8][2];
+      if constexpr (KMAJ) {
+        const double* panel = a_s + (kk >> 4) * (BM * 16) + (wm0 + lr) * 16;
+        const int chunk = ((((kk & 15) >> 1) + lk) ^ lr) << 1;  // (m & 7) == lr
+#pragma unroll
+        for (int mf = 0; mf < 4; ++mf) {
+          const double2 v = *reinterpret_cast<const double2*>(panel + mf * 8 * 16 + chunk);
+          a[mf][0] = v.x;
+          a[mf][1] = v.y;
+        }
+      } else {
+        const double* col = a_s + (kk + 2 * lk) * BM + wm0 + lr;
+#pragma unroll
+        for (int mf = 0; mf < 4; ++mf) {
+          a[mf][0] = col[mf * 8];
+          a[mf][1] = col[BM + mf * 8];
+        }
+      }
+      const double* brow = b_s + (kk + 2 * lk) * BN;
+#pragma unroll
+      for (int nf = 0; nf < 8; ++nf) {
+        if (TAIL && nf >= nf_act) break;
+        b[nf][0] = brow[nf * 8];
+        b[nf][1] = brow[BN + nf * 8];
+      }
+#pragma unroll
+      for (int ph = 0; ph < 2; ++ph)
+#pragma unroll
+        for (int mf = 0; mf < 4; ++mf)
+#pragma unroll
+          for (int nf = 0; nf < 8; ++nf) {
+            if (TAIL && nf >= nf_act) break;
+            dmma_8x8x4(acc[mf][nf], a[mf][ph], b[nf][ph]);
+          }
+    }
+    __syncwarp();
+    if ((lane & 31) == 0) mbar_arrive(&empty[s]);
+  }
+}
+
+template <bool KMAJ, int BM, int BN, int BK, int STAGE_BYTES, int A_BYTES>
+__device__ __forceinline__ void ws_consume_dmma(const uint8_t* smem, uint64_t* full, uint64_t* empty, int nst,
+                                                const WsParams& p, int n0, int j0, int warp, int lane,
+                                                int stages) {
+  constexpr int WARPS_N = BN / 64;
+  const int wm0 = (warp / WARPS_N) * 32, wn0 = (warp % WARPS_N) * 64;
+  const int lr = lane >> 2, lk = lane & 3;
+  double acc[4][8][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  const int nf_act = (p.R - j0 - wn0 + 7) >> 3;  // warp-uniform
+  if (nf_act >= 8)
+    ws_dmma_loop<KMAJ, false, BM, BN, BK, STAGE_BYTES, A_BYTES>(acc, smem, full, empty, nst, stages, wm0, wn0, lane,
+                                                                8);
+  else
+    ws_dmma_loop<KMAJ, true, BM, BN, BK, STAGE_BYTES, A_BYTES>(acc, smem, full, empty, nst, stages, wm0, wn0, lane,
+                                                               nf_act);
+
+  double* out = p.out + int64_t(blockIdx.z) * p.out_split_stride;
+  const bool fold = p.lam != nullptr;
+#pragma unroll
+  for (int mf = 0; mf < 4; ++mf) {
+    const int n = n0 + wm0 + mf * 8 + lr;
+    if (n >= p.Ik) continue;
+#pragma unroll
+    for (int nf = 0; nf < 8; ++nf) {
+      const int j = j0 + wn0 + nf * 8 + 2 * lk;
+      double v0 = acc[mf][nf][0], v1 = acc[mf][nf][1];
+      if (fold) {
+        if (j < p.R) v0 *= p.lam[j];
+        if (j + 1 < p.R) v1 *= p.lam[j + 1];
+      }
+      double* dst = out + int64_t(n) * p.ldo + j;
+      if (j + 1 < p.R && ((p.ldo & 1) == 0)) {
+        *reinterpret_cast<double2*>(dst) = make_double2(v0, v1);
+      } else {
+        if (j < p.R) dst[0] = v0;
+        if (j + 1 < p.R) dst[1] = v1;
+      }
+    }
+  }
+}
+
 // ---------------------------------------------------------------- kernel
 // Tile shapes (per-thread TM x 8 accumulators, 256 consumer threads):
 //   TM = 8,  BN = 128 -> BM = 128 (16 x 16 threads), BK = 32
@@ -139,10 +259,23 @@ __device__ __forceinline__ void tma_load(void* dst, const CUtensorMap* map, uint
 // TM = 12 cuts shared-memory wavefronts per DFMA from 0.375 to 0.29: the A
 // fragment (lane quads share a row -> 1 wavefront per 8 B) grows, the B
 // fragment (4 distinct columns per quad -> 2 wavefronts per 8 B) does not.
+// TM = 0 selects the DMMA consumer (mma.sync m8n8k4 f64): 8 warps of 32 x 64
+// warp tiles, BN / 64 warps across the rank tile -> BM = 32 * 8 / (BN / 64):
+//   BN = 64 -> BM = 256, BN = 128 -> BM = 128, BN = 256 -> BM = 64.
+template <int TM, int BN>
+struct WsTile {
+  static constexpr int TX = BN / 8, TY = 256 / TX, BM = TY * TM;
+};
+template <int BN>
+struct WsTile<0, BN> {
+  static constexpr int WARPS_N = BN / 64, WARPS_M = 8 / WARPS_N;
+  static constexpr int TX = 8, TY = 0, BM = 32 * WARPS_M;
+};
+
 template <bool KMAJ, int NO, int TM, int BN, int BK, int STAGES>
 struct WsCfg {
   static constexpr int D = NO + 2;  // tensor order
-  static constexpr int TX = BN / 8, TY = 256 / TX, BM = TY * TM;
+  static constexpr int TX = WsTile<TM, BN>::TX, TY = WsTile<TM, BN>::TY, BM = WsTile<TM, BN>::BM;
   static constexpr int A_ELEMS = BM * BK;
   static constexpr int B_ELEMS = BK * BN;
   static constexpr int P_ELEMS = NO * BN;
@@ -151,6 +284,7 @@ struct WsCfg {
   static constexpr int TX_BYTES = A_BYTES + B_BYTES + P_BYTES;
   static constexpr size_t SMEM = size_t(STAGES) * STAGE_BYTES + 256 /*barriers*/;
   static_assert(TM % 2 == 0 && BK % 16 == 0 && BM <= 256 && BN <= 256, "tile shape");
+  static_assert(TM != 0 || (BN >= 64 && BN % 64 == 0), "DMMA rank tile is a multiple of 64");
   static_assert((TX >= 8) && (TX % 8 == 0), "8 lanes per warp row");
 };
 
@@ -303,11 +437,17 @@ __global__ void __launch_bounds__(WS_THREADS, 1) mttkrp_f64_ws_sm100(const __gri
 
   // ================================================================== consumers
   setmaxnreg_inc<WsRegs<TM>::consumer>();
+  if constexpr (TM == 0) {
+    ws_consume_dmma<KMAJ, BM, BN, BK, C::STAGE_BYTES, C::A_BYTES>(smem, full, empty, nst, p, n0, j0, warp, lane,
+                                                                  STAGES);
+    return;
+  }
+  if constexpr (TM != 0) {
   constexpr int WX = 8, WY = 4, WARPS_X = TX / WX;
   const int ty = (warp / WARPS_X) * WY + lane / WX;
   const int tx = (warp % WARPS_X) * WX + lane % WX;
 
-  double acc[TM][8];
+  double acc[TM > 0 ? TM : 1][8];
 #pragma unroll
   for (int r = 0; r < TM; ++r)
 #pragma unroll
@@ -431,6 +571,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) mttkrp_f64_ws_sm100(const __gri
       }
     }
   }
+  }  // TM != 0
 }
 
 // ---------------------------------------------------------------- host side
@@ -484,7 +625,15 @@ static void ws_pick(bool kmaj, int no, const void** fn, size_t* smem) {
   }
 }
 
-bool ws_shape(int rank_tile, int* block_rows, int* block_k) {
+bool ws_shape(int rank_tile, int math, int* block_rows, int* block_k) {
+  if (math == WS_MATH_DMMA) {
+    switch (rank_tile) {
+      case 64: *block_rows = 256; *block_k = 16; return true;
+      case 128: *block_rows = 128; *block_k = 32; return true;
+      case 256: *block_rows = 64; *block_k = 16; return true;
+      default: return false;
+    }
+  }
   switch (rank_tile) {
     case 64: *block_rows = 256; *block_k = 16; return true;   // TM 8
     case 128: *block_rows = 128; *block_k = 32; return true;  // TM 8
@@ -495,7 +644,7 @@ bool ws_shape(int rank_tile, int* block_rows, int* block_k) {
 
 bool ws_eligible(const WsRequest& r) {
   int bm, bk;
-  if (!ws_shape(r.rank_tile, &bm, &bk)) return false;
+  if (!ws_shape(r.rank_tile, r.math, &bm, &bk)) return false;
   if (r.d < 2 || r.d > 5 || r.n_o > 3) return false;
   if (r.block_k != bk) return false;
   if (r.dims[0] % 2 != 0) return false;
@@ -511,7 +660,7 @@ bool ws_eligible(const WsRequest& r) {
 
 int launch_ws(const WsRequest& r, cudaStream_t st) {
   int BM, BK;
-  if (!ws_shape(r.rank_tile, &BM, &BK)) return fail(CPK_ERR_PARAM, "no TMA tile for rank_tile %d", r.rank_tile);
+  if (!ws_shape(r.rank_tile, r.math, &BM, &BK)) return fail(CPK_ERR_PARAM, "no TMA tile for rank_tile %d", r.rank_tile);
   const int BN = r.rank_tile;
   WsParams p;
   memset(&p, 0, sizeof(p));
@@ -572,7 +721,11 @@ int launch_ws(const WsRequest& r, cudaStream_t st) {
   size_t smem = 0;
   const bool kmaj = k != 0;
   const int no = r.n_o;
-  if (BN == 128) ws_pick<8, 128, 32>(kmaj, no, &fn, &smem);
+  if (r.math == WS_MATH_DMMA) {
+    if (BN == 128) ws_pick<0, 128, 32>(kmaj, no, &fn, &smem);
+    else if (BN == 256) ws_pick<0, 256, 16>(kmaj, no, &fn, &smem);
+    else ws_pick<0, 64, 16>(kmaj, no, &fn, &smem);
+  } else if (BN == 128) ws_pick<8, 128, 32>(kmaj, no, &fn, &smem);
   else if (BN == 256) ws_pick<12, 256, 16>(kmaj, no, &fn, &smem);
   else ws_pick<8, 64, 16>(kmaj, no, &fn, &smem);
   if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) != cudaSuccess)

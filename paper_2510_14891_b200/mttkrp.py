@@ -38,7 +38,7 @@ from .errors import IndexRangeError, ParameterError, ShapeError
 from .kruskal import KruskalTensor
 
 
-_ENGINES = {"auto": 0, "cpasync": 1, "tma": 2}
+_ENGINES = {"auto": 0, "cpasync": 1, "tma": 2, "dmma": 3}
 
 
 class Variant(str, Enum):
@@ -367,6 +367,7 @@ def heuristic_tile_volume(dims, machine) -> int:
 _TILE_CHOICES = (
     ("tma", 256, 96, 0.95), ("tma", 128, 128, 1.00), ("tma", 64, 256, 0.93),
     ("cpasync", 128, 128, 0.92), ("cpasync", 64, 128, 0.78), ("cpasync", 32, 64, 0.55),
+    ("dmma", 256, 64, 1.02), ("dmma", 128, 128, 1.19), ("dmma", 64, 256, 1.26),
 )
 
 
@@ -385,7 +386,9 @@ def heuristic_rank_tile(rank: int, rows: int | None = None, tma: bool = True) ->
     rows = rows or 1
     best, best_cost = None, float("inf")
     for eng, rt, bm, rate in _TILE_CHOICES:
-        if eng == "tma" and not tma:
+        if eng in ("tma", "dmma") and not tma:
+            continue
+        if rate <= 0:  # explicit-only engine
             continue
         cost = (-(-rows // bm) * bm) * (-(-rank // rt) * rt) / rate
         if cost < best_cost * (1 - 1e-9):

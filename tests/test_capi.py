@@ -49,12 +49,13 @@ def plan(dims, mode, rank, **kw):
 
 
 def test_plan_resolution_fills_waves():
-    # c4: 1024^3, R=2000: 8 row tiles x 16 rank tiles = 128 tiles; the split
-    # count is the smallest one whose CTAs fill >= 99% of their waves
+    # c4: 1024^3, R=2000: DMMA tile 256 x 64 -> 4 row tiles x 32 rank tiles =
+    # 128 tiles; the split count is the smallest one whose CTAs fill >= 99%
+    # of their waves
     rc, p = plan((1024, 1024, 1024), 0, 2000)
     assert rc == 0
-    assert p.rank_tile == 128 and p.block_rows == 128
-    ctas = 8 * 16 * p.splits
+    assert p.rank_tile == 64 and p.block_rows == 256 and p.engine == 3
+    ctas = 4 * 32 * p.splits
     assert ctas / (148 * -(-ctas // 148)) >= 0.99
     # c2: R=64 -> rank tile 64
     rc, p = plan((512, 512, 512), 1, 64)

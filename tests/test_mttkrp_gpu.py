@@ -192,11 +192,13 @@ def test_c4_row_sampled_parity():
             assert oracle.rel_err(got[n], ref) <= TOL, (k, n)
 
 
+@pytest.mark.parametrize("engine", ["tma", "dmma"])
 @pytest.mark.parametrize("rank_tile", [64, 128, 256])
 @pytest.mark.parametrize("dims", [(40, 36, 34), (130, 66, 3), (34, 40, 70, 6), (6, 4, 8, 10, 4), (64, 2)])
-def test_tma_engine_parity(dims, rank_tile):
-    """The warp-specialized TMA kernels (forced) on ragged shapes: I_k not a
-    multiple of the row tile, chunk tails, rank tails, d = 2..5, splits."""
+def test_tma_engine_parity(dims, rank_tile, engine):
+    """The warp-specialized TMA kernels (forced; DFMA and DMMA consumers) on
+    ragged shapes: I_k not a multiple of the row tile, chunk tails, rank
+    tails, d = 2..5, splits."""
     for rank in (2, 130, 300):
         y = rng_for(sum(dims) * rank).random(int(np.prod(dims)))
         fs = [rng_for(rank + 7 * j).random((n, rank)) for j, n in enumerate(dims)]
@@ -206,7 +208,7 @@ def test_tma_engine_parity(dims, rank_tile):
         for k in range(len(dims)):
             ref = oracle.mttkrp_ref(y, dims, k, fs, lam)
             for splits in (0, 1, 5):
-                plan = MttkrpPlan(Variant.B200, k, rank_tile=rank_tile, splits=splits, engine="tma")
+                plan = MttkrpPlan(Variant.B200, k, rank_tile=rank_tile, splits=splits, engine=engine)
                 got = ck.run(t, m, plan).matrix
                 assert oracle.rel_err(got, ref) <= TOL, (dims, rank, k, splits)
 
@@ -216,7 +218,7 @@ def test_engines_agree_bitwise_on_c2_mode1(golden):
     g, dims, rank, y, fs = _config(golden, "c2")
     t = ck.DenseTensor(dims, y)
     m = ck.KruskalTensor(np.ones(rank), fs, validate=False)
-    for engine in ("tma", "cpasync"):
+    for engine in ("tma", "cpasync", "dmma"):
         plan = MttkrpPlan(Variant.B200, 1, rank_tile=128, block_k=32, engine=engine)
         a = ck.run(t, m, plan).matrix
         b = ck.run(t, m, plan).matrix

@@ -25,6 +25,7 @@ KEYS = [
     "lts__t_bytes.sum",
     "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
     "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_tensor_subpipe_dmma.avg.pct_of_peak_sustained_active",
     "smsp__issue_active.avg.pct_of_peak_sustained_active", "sm__warps_active.avg.pct_of_peak_sustained_active",
     "l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed",
     "l1tex__data_pipe_lsu_wavefronts_mem_shared_op_ld.sum", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum",
@@ -95,7 +96,11 @@ def summarize_report(path: Path, tag: str) -> dict:
     rd = num("dram__bytes_read.sum") * scale.get(m["dram__bytes_read.sum"][1], 1)
     wr = num("dram__bytes_write.sum") * scale.get(m["dram__bytes_write.sum"][1], 1)
     return {"report": path.name, "dram_bytes_per_launch": rd + wr,
-            "fp64_pipe_pct": num("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"),
+            # DFMA issues on the fp64 pipe, DMMA on the tensor pipe's dmma
+            # subpipe (the same FP64 datapath, tools/microbench4.cu)
+            "fp64_pipe_pct": max(num("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active") or 0.0,
+                                 num("sm__inst_executed_pipe_tensor_subpipe_dmma.avg.pct_of_peak_sustained_active")
+                                 or 0.0),
             "duration_ms": num("gpu__time_duration.sum")}
 
 
