@@ -111,6 +111,20 @@ int cpk_mttkrp_f64(const double* y, int d, const int64_t* dims, int mode,
                    const cpk_plan* plan, void* workspace, size_t ws_bytes,
                    void* stream);
 
+/* The same MTTKRP, launched piecewise while the tensor streams in: only
+ * the work whose tensor slices along the slowest mode (d-1) all lie in
+ * [0, landed_hi) and not all in [0, landed_lo).  Calling it with
+ * (0, h_1), (h_1, h_2), ..., (h_{n-1}, dims[d-1]) in stream order launches
+ * every work item exactly once; the last call also runs the split-K merge,
+ * so G is bit-identical to cpk_mttkrp_f64's.  Same plan, workspace and
+ * pointers on every call (the workspace carries the partial sums). */
+int cpk_mttkrp_f64_landed(const double* y, int d, const int64_t* dims,
+                          int mode, const double* const* factors,
+                          const int64_t* ld, const double* lam, int64_t rank,
+                          double* G, int64_t ldg, const cpk_plan* plan,
+                          void* workspace, size_t ws_bytes, void* stream,
+                          int64_t landed_lo, int64_t landed_hi);
+
 /* Gram matrix A^T A (R x R), symmetrized exactly: upper triangle computed,
  * lower mirrored -- kruskal.gram (kruskal.py:110-114). */
 int cpk_gram_f64(const double* A, int64_t rows, int64_t rank, int64_t lda,

@@ -65,6 +65,7 @@ struct MttkrpParams {
   int64_t ldo;
   int64_t out_split_stride;
   const double* lam;         // folded in the epilogue only when direct
+  int32_t y0, z0;            // first row block / split of this launch
 };
 
 // Loader state: the chunk being staged next, as an odometer over
@@ -151,8 +152,8 @@ __global__ void __launch_bounds__((BM / 8) * (BN / 8), 1)
   const int tx = (warp % WARPS_X) * C::WX + lane % C::WX;
 
   const int64_t j0 = int64_t(blockIdx.x) * BN;
-  const int64_t n0 = int64_t(blockIdx.y) * BM;
-  const int64_t q0 = int64_t(blockIdx.z) * p.chunks_per_split;
+  const int64_t n0 = int64_t(blockIdx.y + p.y0) * BM;
+  const int64_t q0 = int64_t(blockIdx.z + p.z0) * p.chunks_per_split;
   const int64_t q1 = min(p.n_chunks, q0 + p.chunks_per_split);
   const int nst = int(q1 - q0);
 
@@ -295,7 +296,7 @@ __global__ void __launch_bounds__((BM / 8) * (BN / 8), 1)
   cp_async_wait<0>();
 
   // --- epilogue: partial (or final, lam-folded) tile -> out --------------
-  double* out = p.out + int64_t(blockIdx.z) * p.out_split_stride;
+  double* out = p.out + int64_t(blockIdx.z + p.z0) * p.out_split_stride;
   const bool fold = p.lam != nullptr;
 #pragma unroll
   for (int r = 0; r < 8; ++r) {
@@ -477,12 +478,25 @@ static int64_t n_chunks_of(const Problem& pr, int bk) {
   return n;
 }
 
-// Choose the split count so that (tiles x splits) CTAs fill whole waves.
-static int auto_splits(int64_t tiles, int64_t chunks, int slots) {
-  const int64_t max_s = std::max<int64_t>(1, std::min<int64_t>(chunks / 4, 1024));
+// Choose the split count.  Two pressures:
+//  * CTAs that share a tensor tile (the rank tiles of one row tile) read it
+//    through L2 only while they stay close in time; long-running CTAs drift
+//    apart and re-read it from HBM.  At c4 DRAM reads fall from 3.0x to
+//    1.2x the tensor going from 15 to 148 splits (profiles/
+//    r01_exp_splits.log), so each CTA walks at most kChunksPerCta chunks.
+//  * the split-K workspace (splits x I_k x R doubles, read back once by the
+//    reduction) stays under kWorkspaceBudget.
+// Within those bounds, the first split count whose CTAs fill whole waves.
+constexpr int64_t kChunksPerCta = 512;
+constexpr double kWorkspaceBudget = 2.0 * (1 << 30);
+
+static int auto_splits(int64_t tiles, int64_t chunks, int slots, double bytes_per_split) {
+  const int64_t cap = std::max<int64_t>(1, int64_t(kWorkspaceBudget / std::max(bytes_per_split, 1.0)));
+  const int64_t max_s = std::max<int64_t>(1, std::min<int64_t>({chunks / 4, int64_t(4096), cap}));
+  const int64_t lo = std::min<int64_t>(max_s, std::max<int64_t>(1, ceil_div(chunks, kChunksPerCta)));
   double best = -1.0;
-  int64_t best_s = 1;
-  for (int64_t s = 1; s <= max_s; ++s) {
+  int64_t best_s = lo;
+  for (int64_t s = lo; s <= max_s; ++s) {
     const int64_t work = tiles * s;
     const int64_t waves = ceil_div(work, slots);
     const double eff = double(work) / double(waves * slots);
@@ -611,7 +625,8 @@ static int resolve(const Problem& pr, cpk_plan* plan) {
         KernelInfo ki = pick_kernel(plan->rank_tile, plan->block_k, pr.k != 0, 2, std::min(pr.n_o, 3));
         per_sm = ki.fn ? ctas_per_sm(ki) : 1;
       }
-      plan->splits = auto_splits(tiles, chunks, plan->sm_count * per_sm);
+      const double ldw = double((pr.R + 1) & ~int64_t(1));
+      plan->splits = auto_splits(tiles, chunks, plan->sm_count * per_sm, double(pr.Ik) * ldw * sizeof(double));
     }
   }
   if (plan->splits > chunks) plan->splits = int(chunks);
@@ -665,16 +680,44 @@ __global__ static void mttkrp_order1(const double* y, int64_t I, int64_t R, cons
   }
 }
 
-extern "C" int cpk_mttkrp_f64(const double* y, int d, const int64_t* dims, int mode, const double* const* factors,
-                              const int64_t* ld, const double* lam, int64_t rank, double* G, int64_t ldg,
-                              const cpk_plan* plan_in, void* workspace, size_t ws_bytes, void* stream) {
+// Work items of a launch that are complete once the slices [0, h) of the
+// slowest mode (d-1) are in memory.  mode == d-1: row blocks (each needs its
+// own BM slices); else splits (split z needs the slices its last chunk
+// touches; chunks run f fastest, then the o modes ascending).
+struct Landed {
+  int64_t bm, bk, n_chunks, cps;
+  int64_t rows_ready(const Problem& pr, int64_t h) const {
+    return h >= pr.Ik ? ceil_div(pr.Ik, bm) : h / bm;
+  }
+  int64_t need(const Problem& pr, int64_t z) const {
+    const int64_t qe = std::min((z + 1) * cps, n_chunks) - 1;
+    const int last = pr.d - 1;
+    if (pr.f == last) return std::min((qe + 1) * bk, pr.dims[last]);  // d == 2, mode 0
+    return qe / (n_chunks / pr.dims[last]) + 1;
+  }
+  int64_t splits_ready(const Problem& pr, int64_t splits, int64_t h) const {
+    int64_t z = 0;
+    while (z < splits && need(pr, z) <= h) ++z;
+    return z;
+  }
+};
+
+static int mttkrp_impl(const double* y, int d, const int64_t* dims, int mode, const double* const* factors,
+                       const int64_t* ld, const double* lam, int64_t rank, double* G, int64_t ldg,
+                       const cpk_plan* plan_in, void* workspace, size_t ws_bytes, void* stream, int64_t landed_lo,
+                       int64_t landed_hi) {
+  const bool ranged = landed_hi >= 0;
   Problem pr;
   int rc = make_problem(d, dims, mode, rank, &pr);
   if (rc) return rc;
   if (!y || !G) return fail(CPK_ERR_PARAM, "tensor or output pointer is NULL");
   if (ldg < rank) return fail(CPK_ERR_PARAM, "ldg %lld < rank %lld", (long long)ldg, (long long)rank);
   cudaStream_t st = as_stream(stream);
+  if (ranged && (landed_lo < 0 || landed_hi < landed_lo || landed_hi > dims[d - 1]))
+    return fail(CPK_ERR_PARAM, "landed range [%lld, %lld) not within [0, %lld]", (long long)landed_lo,
+                (long long)landed_hi, (long long)dims[d - 1]);
   if (d == 1) {
+    if (ranged && landed_hi < dims[0]) return CPK_OK;  // rows all land together: run once at the end
     mttkrp_order1<<<256, 256, 0, st>>>(y, pr.Ik, rank, lam, G, ldg);
     return check_launch("mttkrp_order1");
   }
@@ -737,8 +780,24 @@ extern "C" int cpk_mttkrp_f64(const double* y, int d, const int64_t* dims, int m
     wr.out_split_stride = out_split_stride;
     wr.lam = lam_fold;
     if (ws_eligible(wr)) {
-      rc = launch_ws(wr, st);
-      if (rc) return rc;
+      Landed ld_{plan.block_rows, plan.block_k, 0, 0};
+      ld_.n_chunks = n_chunks_of(pr, plan.block_k);
+      ld_.cps = ceil_div(ld_.n_chunks, plan.splits);
+      wr.y1 = int32_t(ceil_div(pr.Ik, plan.block_rows));
+      wr.z1 = plan.splits;
+      if (ranged) {
+        if (mode == d - 1) {
+          wr.y0 = int32_t(ld_.rows_ready(pr, landed_lo));
+          wr.y1 = int32_t(ld_.rows_ready(pr, landed_hi));
+        } else {
+          wr.z0 = int32_t(ld_.splits_ready(pr, plan.splits, landed_lo));
+          wr.z1 = int32_t(ld_.splits_ready(pr, plan.splits, landed_hi));
+        }
+      }
+      if (wr.y1 > wr.y0 && wr.z1 > wr.z0) {
+        rc = launch_ws(wr, st);
+        if (rc) return rc;
+      }
       goto reduce;
     }
     if (plan_in && is_tma(plan_in->engine))
@@ -767,15 +826,29 @@ extern "C" int cpk_mttkrp_f64(const double* y, int d, const int64_t* dims, int m
     if (!ki.fn) return fail(CPK_ERR_PARAM, "no kernel for rank_tile %d", plan.rank_tile);
     if (cudaFuncSetAttribute(ki.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ki.smem)) != cudaSuccess)
       return check_launch("cudaFuncSetAttribute");
-    dim3 grid(unsigned(ceil_div(rank, plan.rank_tile)), unsigned(ceil_div(pr.Ik, plan.block_rows)),
-              unsigned(plan.splits));
+    int64_t y0 = 0, y1 = ceil_div(pr.Ik, plan.block_rows), z0 = 0, z1 = plan.splits;
+    if (ranged) {
+      const Landed ld_{plan.block_rows, bk, p.n_chunks, p.chunks_per_split};
+      if (mode == d - 1) {
+        y0 = ld_.rows_ready(pr, landed_lo);
+        y1 = ld_.rows_ready(pr, landed_hi);
+      } else {
+        z0 = ld_.splits_ready(pr, plan.splits, landed_lo);
+        z1 = ld_.splits_ready(pr, plan.splits, landed_hi);
+      }
+    }
+    p.y0 = int32_t(y0);
+    p.z0 = int32_t(z0);
+    dim3 grid(unsigned(ceil_div(rank, plan.rank_tile)), unsigned(y1 - y0), unsigned(z1 - z0));
     if (grid.y > 65535u || grid.z > 65535u) return fail(CPK_ERR_PARAM, "grid too large (I_k or splits)");
-    void* args[] = {&p};
-    cudaError_t e = cudaLaunchKernel(ki.fn, grid, dim3(ki.threads), args, ki.smem, st);
-    if (e != cudaSuccess) return fail(CPK_ERR_CUDA, "mttkrp launch: %s", cudaGetErrorString(e));
+    if (grid.y > 0 && grid.z > 0) {
+      void* args[] = {&p};
+      cudaError_t e = cudaLaunchKernel(ki.fn, grid, dim3(ki.threads), args, ki.smem, st);
+      if (e != cudaSuccess) return fail(CPK_ERR_CUDA, "mttkrp launch: %s", cudaGetErrorString(e));
+    }
   }
 reduce:
-  if (!direct) {
+  if (!direct && (!ranged || landed_hi == dims[d - 1])) {
     const int64_t total = pr.Ik * rank;
     const int threads = 256;
     const int64_t blocks = std::min<int64_t>(ceil_div(total, threads), int64_t(plan.sm_count) * 16);
@@ -784,4 +857,19 @@ reduce:
     return check_launch("splitk_reduce");
   }
   return CPK_OK;
+}
+
+extern "C" int cpk_mttkrp_f64(const double* y, int d, const int64_t* dims, int mode, const double* const* factors,
+                              const int64_t* ld, const double* lam, int64_t rank, double* G, int64_t ldg,
+                              const cpk_plan* plan_in, void* workspace, size_t ws_bytes, void* stream) {
+  return mttkrp_impl(y, d, dims, mode, factors, ld, lam, rank, G, ldg, plan_in, workspace, ws_bytes, stream, -1, -1);
+}
+
+extern "C" int cpk_mttkrp_f64_landed(const double* y, int d, const int64_t* dims, int mode,
+                                     const double* const* factors, const int64_t* ld, const double* lam,
+                                     int64_t rank, double* G, int64_t ldg, const cpk_plan* plan_in, void* workspace,
+                                     size_t ws_bytes, void* stream, int64_t landed_lo, int64_t landed_hi) {
+  if (landed_hi < 0) return fail(CPK_ERR_PARAM, "landed_hi must be >= 0");
+  return mttkrp_impl(y, d, dims, mode, factors, ld, lam, rank, G, ldg, plan_in, workspace, ws_bytes, stream,
+                     landed_lo, landed_hi);
 }

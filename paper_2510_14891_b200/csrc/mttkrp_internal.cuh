@@ -21,6 +21,7 @@ struct WsRequest {
   int64_t rank;
   int rank_tile, block_k, splits;
   int math;  // WS_MATH_*
+  int32_t y0, y1, z0, z1;  // row blocks / splits of this launch (y1, z1 exclusive)
   double* out;
   int64_t ldo, out_split_stride;
   const double* lam;

@@ -55,6 +55,7 @@ struct alignas(64) WsParams {
   double* out;
   int64_t ldo, out_split_stride;
   const double* lam;
+  int32_t y0, z0;  // first row block / split of this launch
 };
 
 // ---------------------------------------------------------------- PTX wrappers
@@ -226,7 +227,7 @@ __device__ __forceinline__ void ws_consume_dmma(const uint8_t* smem, uint64_t* f
     ws_dmma_loop<KMAJ, true, BM, BN, BK, STAGE_BYTES, A_BYTES>(acc, smem, full, empty, nst, stages, wm0, wn0, lane,
                                                                nf_act);
 
-  double* out = p.out + int64_t(blockIdx.z) * p.out_split_stride;
+  double* out = p.out + int64_t(blockIdx.z + p.z0) * p.out_split_stride;
   const bool fold = p.lam != nullptr;
 #pragma unroll
   for (int mf = 0; mf < 4; ++mf) {
@@ -302,10 +303,10 @@ __global__ void __launch_bounds__(WS_THREADS, 1) mttkrp_f64_ws_sm100(const __gri
   uint64_t* empty = bar + 2 * STAGES;   // consumers done
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t q0 = int64_t(blockIdx.z) * p.chunks_per_split;
+  const int64_t q0 = int64_t(blockIdx.z + p.z0) * p.chunks_per_split;
   const int nst = int(min(p.n_chunks, q0 + p.chunks_per_split) - q0);
   const int j0 = blockIdx.x * BN;
-  const int n0 = blockIdx.y * BM;
+  const int n0 = (blockIdx.y + p.y0) * BM;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -548,7 +549,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) mttkrp_f64_ws_sm100(const __gri
   }
 
   // epilogue: partial (or final, lam-folded) tile -> out
-  double* out = p.out + int64_t(blockIdx.z) * p.out_split_stride;
+  double* out = p.out + int64_t(blockIdx.z + p.z0) * p.out_split_stride;
   const bool fold = p.lam != nullptr;
 #pragma unroll
   for (int r = 0; r < TM; ++r) {
@@ -716,6 +717,8 @@ int launch_ws(const WsRequest& r, cudaStream_t st) {
   p.ldo = r.ldo;
   p.out_split_stride = r.out_split_stride;
   p.lam = r.lam;
+  p.y0 = r.y0;
+  p.z0 = r.z0;
 
   const void* fn = nullptr;
   size_t smem = 0;
@@ -730,8 +733,8 @@ int launch_ws(const WsRequest& r, cudaStream_t st) {
   else ws_pick<8, 64, 16>(kmaj, no, &fn, &smem);
   if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) != cudaSuccess)
     return check_launch("ws set smem");
-  const int64_t gx = (r.rank + BN - 1) / BN, gy = (r.dims[k] + BM - 1) / BM;
-  dim3 grid(unsigned(gx), unsigned(gy), unsigned(r.splits));
+  const int64_t gx = (r.rank + BN - 1) / BN;
+  dim3 grid(unsigned(gx), unsigned(r.y1 - r.y0), unsigned(r.z1 - r.z0));
   void* args[] = {&p};
   cudaError_t e = cudaLaunchKernel(fn, grid, dim3(WS_THREADS), args, smem, st);
   if (e != cudaSuccess) return fail(CPK_ERR_CUDA, "ws launch: %s", cudaGetErrorString(e));

@@ -139,6 +139,22 @@ class DenseTensor:
         self._dev = t
         return t
 
+    def needs_upload(self, device=None) -> bool:
+        """True when the payload lives on the host and no device copy is cached."""
+        dev = require_cuda(device)
+        return not (self._dev is not None and self._dev.device == dev)
+
+    def host_view(self) -> torch.Tensor:
+        """The host payload as a flat float64 torch tensor (no copy when the
+        payload is already contiguous; pinned if the caller pinned it)."""
+        if _is_torch(self.data):
+            return self.data.reshape(-1)
+        return torch.from_numpy(np.ascontiguousarray(self.data).reshape(-1))
+
+    def cache_device(self, t: torch.Tensor) -> None:
+        """Adopt `t` (flat float64 CUDA, same contents) as the device copy."""
+        self._dev = t
+
     def to_ndarray(self) -> np.ndarray:
         """The data as a numpy array with axis 0 fastest (host copy if on device)."""
         host = self.data.detach().cpu().numpy() if _is_torch(self.data) else self.data

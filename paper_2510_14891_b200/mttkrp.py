@@ -163,9 +163,12 @@ def resolve_plan(plan: MttkrpPlan, dims, rank: int) -> dict:
 
 
 def mttkrp_device(y_dev: torch.Tensor, dims, factors, mode: int, weights=None, plan: MttkrpPlan | None = None,
-                  out: torch.Tensor | None = None):
+                  out: torch.Tensor | None = None, landed=None):
     """Low-level device entry: y_dev flat CUDA float64, factors CUDA (I_m, R).
 
+    ``landed = (lo, hi)`` runs only the work whose slices along the slowest
+    mode lie in [0, hi) and not all in [0, lo) (cpk_mttkrp_f64_landed): the
+    streaming building block; the call with hi = dims[-1] completes G.
     Returns (G, resolved CpkPlan, EventTimer).  G is (I_k, R) row-major CUDA.
     """
     dims = check_dims(dims)
@@ -187,10 +190,12 @@ def mttkrp_device(y_dev: torch.Tensor, dims, factors, mode: int, weights=None, p
     lds = _lib.i64_array([f.stride(0) for f in factors])
     lam_ptr = weights.data_ptr() if weights is not None else None
     timer = EventTimer(dev)
-    rc = lib.cpk_mttkrp_f64(
-        y_dev.data_ptr(), d, dims_c, mode, ptrs, lds, lam_ptr, rank, out.data_ptr(), out.stride(0),
-        p, ws.data_ptr() if ws is not None else None, nbytes.value, stream_ptr(dev),
-    )
+    args = (y_dev.data_ptr(), d, dims_c, mode, ptrs, lds, lam_ptr, rank, out.data_ptr(), out.stride(0),
+            p, ws.data_ptr() if ws is not None else None, nbytes.value, stream_ptr(dev))
+    if landed is None:
+        rc = lib.cpk_mttkrp_f64(*args)
+    else:
+        rc = lib.cpk_mttkrp_f64_landed(*args, int(landed[0]), int(landed[1]))
     timer.stop(dev)
     _lib.check(rc, "mttkrp")
     return out, p, timer
@@ -202,15 +207,59 @@ def _unit_weights(w) -> bool:
     return bool(np.all(np.asarray(w) == 1.0))
 
 
+# A host-resident tensor at least this large is streamed to the device in
+# slabs, each slab's MTTKRP overlapping the copy of the next.
+STREAM_MIN_BYTES = 256 << 20
+STREAM_SLABS = 8
+
+
 def _run_gpu(y: DenseTensor, m: KruskalTensor, plan: MttkrpPlan):
     dev = require_cuda()
-    y_dev = y.device_data(dev)
     fac = m.device_factors(dev)
     lam = None if _unit_weights(m.weights) else m.device_weights(dev)
-    g, p, timer = mttkrp_device(y_dev, y.dims, fac, plan.mode, lam, plan)
+    if y.needs_upload(dev) and y.size * 8 >= STREAM_MIN_BYTES and y.ndim >= 2 and y.dims[-1] >= 2:
+        g, p, timer = _mttkrp_streamed(y, fac, plan, lam, dev)
+    else:
+        g, p, timer = mttkrp_device(y.device_data(dev), y.dims, fac, plan.mode, lam, plan)
     host = not isinstance(y.data, torch.Tensor)
     matrix = np.ascontiguousarray(g.cpu().numpy()) if host else g
     return matrix, p, timer
+
+
+def _mttkrp_streamed(y: DenseTensor, fac, plan: MttkrpPlan, lam, dev):
+    """First touch of a large host tensor: copy it to the device in slabs
+    along its slowest mode on a side stream while, on the current stream,
+    the MTTKRP work items whose slices have landed run
+    (cpk_mttkrp_f64_landed).  Same plan, work items and split-K merge as a
+    call on the resident tensor, so G is bit-identical to it.  The device
+    copy is cached on `y` for later modes (DenseTensor.device_data)."""
+    dims, mode = y.dims, plan.mode
+    per_slice = num_elements(dims[:-1])
+    host = y.host_view()
+    y_dev = torch.empty(y.size, dtype=torch.float64, device=dev)
+    rank = next(int(f.shape[1]) for f in fac if f is not None)
+    out = torch.empty((dims[mode], rank), dtype=torch.float64, device=dev)
+    compute = torch.cuda.current_stream(dev)
+    copy = torch.cuda.Stream(dev)
+    copy.wait_stream(compute)  # y_dev's allocation is ordered on `compute`
+    n = min(STREAM_SLABS, dims[-1])
+    bounds = [(dims[-1] * i // n, dims[-1] * (i + 1) // n) for i in range(n)]
+    landed = []
+    with torch.cuda.stream(copy):
+        for lo, hi in bounds:
+            y_dev[lo * per_slice:hi * per_slice].copy_(host[lo * per_slice:hi * per_slice], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(copy)
+            landed.append(ev)
+    timer = EventTimer(dev)
+    p = None
+    for (lo, hi), ev in zip(bounds, landed):
+        compute.wait_event(ev)
+        _, p, _ = mttkrp_device(y_dev, dims, fac, mode, lam, plan, out=out, landed=(lo, hi))
+    timer.stop(dev)
+    y_dev.record_stream(copy)
+    y.cache_device(y_dev)
+    return out, p, timer
 
 
 def _stats(variant, y, m, plan, p, timer, *, element_visits, atomic_updates, tile_volume=None, unroll=None,
