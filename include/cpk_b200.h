@@ -148,6 +148,15 @@ int cpk_solve_normal_f64(const double* gamma, double* G, int64_t rows,
                          int64_t rank, void* work, size_t work_bytes,
                          void* stream);
 
+/* Speculative, sync-free form of the same solve for graph-captured sweeps:
+ * rung 0 only (plain Cholesky + solve), the potrf info flag written to the
+ * DEVICE int *info_out and never read back here.  A nonzero flag means G
+ * holds garbage; the caller (cp_als) then restores the sweep's inputs and
+ * reruns it through cpk_solve_normal_f64's full ladder. */
+int cpk_solve_normal_spec_f64(const double* gamma, double* G, int64_t rows,
+                              int64_t rank, void* work, size_t work_bytes,
+                              int* info_out, void* stream);
+
 /* Column 2-norms of A (rows x rank), A[:, nz] /= nrm, lam = where(nz, nrm, 0)
  * -- cpals.py:134-137.  Split in two so the sharded driver can allreduce the
  * squared norms of a row-partitioned factor in between:

@@ -75,6 +75,7 @@ _PROTOS = {
     "cpk_hadamard_f64": (C.c_int, [C.POINTER(_P), C.c_int, C.c_int, _I64, _P, _P]),
     "cpk_solve_workspace_bytes": (C.c_int, [_I64, _I64, C.POINTER(C.c_size_t)]),
     "cpk_solve_normal_f64": (C.c_int, [_P, _P, _I64, _I64, _P, C.c_size_t, _P]),
+    "cpk_solve_normal_spec_f64": (C.c_int, [_P, _P, _I64, _I64, _P, C.c_size_t, _P, _P]),
     "cpk_colnorms_sq_f64": (C.c_int, [_P, _I64, _I64, _I64, _P, _P]),
     "cpk_scale_columns_f64": (C.c_int, [_P, _I64, _I64, _I64, _P, _P, _P]),
     "cpk_normalize_columns_f64": (C.c_int, [_P, _I64, _I64, _I64, _P, _P, _P]),

@@ -9,10 +9,17 @@ initialization order, so a fixed seed gives the reference's trajectory up to
 floating-point reassociation.
 
 Everything between two MTTKRPs stays on the device (Gram, Hadamard,
-Cholesky via cuSOLVER, normalization, fit terms).  Host syncs per sweep: one
-per mode for the Cholesky info flag (the regularization ladder branches on
-it, cpals.py:78-88) and one for the two fit scalars (the stopping rule needs
-them on the host, cpals.py:157).
+Cholesky via cuSOLVER, normalization, fit terms), in fixed buffers: the
+MTTKRP of mode k is written straight into A_k's buffer (mode k's own factor
+is not read by its MTTKRP) and solved in place.  The first sweep runs
+eagerly with the full regularization ladder (cpals.py:78-88; one host sync
+per mode for the Cholesky flag).  Every later sweep is one CUDA-graph
+replay: a snapshot of (factors, Grams, lam), the d modes with a
+*speculative* rung-0 solve whose Cholesky flags stay on the device, and the
+fit terms; the only host sync per sweep is one 2 + d scalar readback (fit
+terms + flags) for the stopping rule (cpals.py:157).  If a flag shows a
+failed Cholesky, the snapshot is restored and that sweep reruns eagerly
+through the ladder, so the trajectory is the eager one either way.
 """
 
 from __future__ import annotations
@@ -99,9 +106,31 @@ class _Solver:
         return g
 
 
-def cp_als(y: DenseTensor, config: AlsConfig) -> tuple:
-    """Run CP-ALS; returns (KruskalTensor with CUDA factors, AlsTrace)."""
+def _solve_spec(solver: "_Solver", gamma: torch.Tensor, g: torch.Tensor, info: torch.Tensor) -> None:
+    rows, r = g.shape
+    _lib.check(
+        _lib.load().cpk_solve_normal_spec_f64(gamma.data_ptr(), g.data_ptr(), rows, r, solver.work.data_ptr(),
+                                              solver.nbytes, info.data_ptr(), stream_ptr(solver.dev)),
+        "solve (speculative)",
+    )
+
+
+# Capturing a sweep costs ~15-20 ms once and saves ~1 ms of launch overhead
+# per sweep (c3, profiles/r01_bench.jsonl), so the auto mode captures only
+# runs that may go this long.
+GRAPH_MIN_ITERS = 24
+
+
+def cp_als(y: DenseTensor, config: AlsConfig, graph: bool | None = None) -> tuple:
+    """Run CP-ALS; returns (KruskalTensor with CUDA factors, AlsTrace).
+
+    ``graph``: True replays sweeps 2.. as one captured CUDA graph (see the
+    module doc); False runs every sweep eagerly with the ladder solve; None
+    (default) captures when max_iters >= GRAPH_MIN_ITERS.
+    """
     config.validate()
+    if graph is None:
+        graph = config.max_iters >= GRAPH_MIN_ITERS
     dev = require_cuda()
     y_dev = y.device_data(dev)
     norm_y = y.norm()
@@ -113,9 +142,9 @@ def cp_als(y: DenseTensor, config: AlsConfig) -> tuple:
     d = y.ndim
     dims = y.dims
     lib = _lib.load()
-    sp = stream_ptr(dev)
 
     t_start = time.perf_counter()
+    # fixed buffers: every sweep (eager or replayed) reads and writes these
     factors = [torch.from_numpy(a).to(dev) for a in init_factors(dims, r, config.seed)]
     grams = [gram(a) for a in factors]
     lam = torch.ones(r, dtype=torch.float64, device=dev)
@@ -123,46 +152,99 @@ def cp_als(y: DenseTensor, config: AlsConfig) -> tuple:
     gamma = torch.empty((r, r), dtype=torch.float64, device=dev)
     h = torch.empty((r, r), dtype=torch.float64, device=dev)
     normsq = torch.empty(r, dtype=torch.float64, device=dev)
-    terms = torch.empty(2, dtype=torch.float64, device=dev)
+    g_last = torch.empty((dims[d - 1], r), dtype=torch.float64, device=dev)
+    stats = torch.zeros(2 + d, dtype=torch.float64, device=dev)  # fit terms, Cholesky flags
+    info = torch.zeros(d, dtype=torch.int32, device=dev)
+    stats_host = torch.zeros(2 + d, dtype=torch.float64, pin_memory=True)
+    plans = [mt.plan_for_mode(config.plan, dims, k) for k in range(d)]
+    ev = [torch.cuda.Event(enable_timing=True, external=True) for _ in range(d + 2)]
 
-    fits, mttkrp_seconds, other_seconds = [], [], []
-    converged = False
-    for _ in range(config.max_iters):
-        sweep_timers, other_timers = [], []
-        g = None
+    def sweep(spec: bool) -> None:
+        sp = stream_ptr(dev)
+        ev[0].record()
         for k in range(d):
-            plan_k = mt.plan_for_mode(config.plan, dims, k)
-            g, _, timer = mt.mttkrp_device(y_dev, dims, factors, k, None, plan_k)
-            sweep_timers.append(timer)
-            t_other = EventTimer(dev)
+            mt.mttkrp_device(y_dev, dims, factors, k, None, plans[k], out=factors[k])
+            ev[k + 1].record()
+            if k == d - 1:  # the fit needs the last mode's G itself
+                g_last.copy_(factors[k])
             hadamard(grams, skip=k, out=gamma)
-            # the solve is in place; the fit needs the last mode's G itself
-            a_hat = solver(gamma, g.clone() if k == d - 1 else g)
+            if spec:
+                _solve_spec(solver, gamma, factors[k], info[k:k + 1])
+            else:
+                x = solver(gamma, factors[k])
+                if x is not factors[k]:  # least-squares last rung
+                    factors[k].copy_(x)
             _lib.check(
-                lib.cpk_normalize_columns_f64(a_hat.data_ptr(), a_hat.shape[0], r, a_hat.stride(0),
+                lib.cpk_normalize_columns_f64(factors[k].data_ptr(), dims[k], r, factors[k].stride(0),
                                               lam.data_ptr(), normsq.data_ptr(), sp),
                 "normalize",
             )
-            factors[k] = a_hat
-            grams[k] = gram(a_hat)
-            other_timers.append(t_other.stop(dev))
-
-        t_fit = EventTimer(dev)
+            gram(factors[k], out=grams[k])
         hadamard(grams, skip=-1, out=h)
-        # g is the unit-weight mode-(d-1) MTTKRP and A_{d-1} was solved from it
+        # g_last is the unit-weight mode-(d-1) MTTKRP and A_{d-1} was solved from it
         _lib.check(
-            lib.cpk_fit_terms_f64(h.data_ptr(), lam.data_ptr(), g.data_ptr(), factors[d - 1].data_ptr(),
-                                  g.shape[0], r, terms.data_ptr(), sp),
+            lib.cpk_fit_terms_f64(h.data_ptr(), lam.data_ptr(), g_last.data_ptr(), factors[d - 1].data_ptr(),
+                                  dims[d - 1], r, stats.data_ptr(), sp),
             "fit terms",
         )
-        other_timers.append(t_fit.stop(dev))
-        norm_m_sq, iprod = (float(v) for v in terms.cpu().tolist())
+        stats[2:].copy_(info)
+        stats_host.copy_(stats, non_blocking=True)
+        ev[d + 1].record()  # after the readback: waiting on it makes stats_host valid
+
+    saved = None
+    captured = None
+
+    def snapshot():
+        for dst, src in zip(saved, factors + grams + [lam]):
+            dst.copy_(src)
+
+    def restore():
+        for dst, src in zip(factors + grams + [lam], saved):
+            dst.copy_(src)
+
+    fits, mttkrp_seconds, other_seconds = [], [], []
+    converged = False
+    for it in range(config.max_iters):
+        if it == 0 or not graph:
+            info.zero_()
+            sweep(spec=False)
+        else:
+            if captured is None:
+                saved = [torch.empty_like(t) for t in factors + grams + [lam]]
+                keep = list(_device_workspaces(dev))  # captured pointers stay alive
+                info.zero_()
+                captured = torch.cuda.CUDAGraph()
+                side = torch.cuda.Stream(dev)
+                side.wait_stream(torch.cuda.current_stream(dev))
+                # capture_begin/end directly: torch.cuda.graph() would also
+                # gc.collect() and empty the allocator cache on entry
+                with torch.cuda.stream(side):
+                    captured.capture_begin()
+                    try:
+                        snapshot()
+                        info.zero_()
+                        sweep(spec=True)
+                    finally:
+                        captured.capture_end()
+                torch.cuda.current_stream(dev).wait_stream(side)
+                captured.keep = keep
+            captured.replay()
+        ev[d + 1].synchronize()
+        if it > 0 and graph and bool((stats_host[2:] != 0).any()):
+            # a speculative Cholesky failed: roll the sweep back, rerun it
+            # through the ladder
+            restore()
+            info.zero_()
+            sweep(spec=False)
+            ev[d + 1].synchronize()
+        norm_m_sq, iprod = float(stats_host[0]), float(stats_host[1])
         resid_sq = max(0.0, norm_y ** 2 - 2.0 * iprod + norm_m_sq)
         fit = 1.0 - math.sqrt(resid_sq) / norm_y
 
         fits.append(float(fit))
-        mttkrp_seconds.append([t.seconds for t in sweep_timers])
-        other_seconds.append(sum(t.seconds for t in other_timers))
+        mts = [ev[k].elapsed_time(ev[k + 1]) * 1e-3 for k in range(d)]
+        mttkrp_seconds.append(mts)
+        other_seconds.append(ev[0].elapsed_time(ev[d + 1]) * 1e-3 - sum(mts))
         if len(fits) >= 2 and abs(fits[-1] - fits[-2]) < config.tol:
             converged = True
             break
@@ -179,3 +261,10 @@ def cp_als(y: DenseTensor, config: AlsConfig) -> tuple:
         converged=converged,
     )
     return model, trace
+
+
+def _device_workspaces(dev):
+    from . import _device
+
+    with _device._ws_lock:
+        return [t for (idx, _), t in _device._workspaces.items() if idx == dev.index]

@@ -116,12 +116,13 @@ def _to_device(x, dev) -> torch.Tensor:
     return torch.from_numpy(np.ascontiguousarray(x, dtype=np.float64)).to(dev)
 
 
-def gram(a) -> torch.Tensor:
+def gram(a, out: torch.Tensor | None = None) -> torch.Tensor:
     """A^T A on the device, symmetrized exactly (kruskal.py:110-114)."""
     dev = require_cuda()
     a = _to_device(_as_factor(a), dev)
     r = a.shape[1]
-    out = torch.empty((r, r), dtype=torch.float64, device=dev)
+    if out is None:
+        out = torch.empty((r, r), dtype=torch.float64, device=dev)
     _lib.check(
         _lib.load().cpk_gram_f64(a.data_ptr(), a.shape[0], r, a.stride(0), out.data_ptr(), stream_ptr(dev)),
         "gram",
