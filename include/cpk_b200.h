@@ -38,9 +38,9 @@ extern "C" {
  * (the reference has no device) and surface as CpkernError subclasses. */
 enum {
   CPK_OK = 0,
-  CPK_ERR_SHAPE = 1,     /* ShapeError      (mttkrp.py:294-296)          */
-  CPK_ERR_INDEX = 2,     /* IndexRangeError (mttkrp.py:297-298, 248-249) */
-  CPK_ERR_PARAM = 3,     /* ParameterError  (mttkrp.py:250-263)          */
+  CPK_ERR_SHAPE = 1,     /* ShapeError      (mttkrp.py:120-122)          */
+  CPK_ERR_INDEX = 2,     /* IndexRangeError (mttkrp.py:123-124, 248-249) */
+  CPK_ERR_PARAM = 3,     /* ParameterError  (mttkrp.py:76-89)          */
   CPK_ERR_RESOURCE = 4,  /* ResourceError   (workspace too small)        */
   CPK_ERR_CUDA = 5,      /* launch / runtime failure                     */
   CPK_ERR_NOT_PD = 6,    /* Cholesky failed: Gamma not positive definite */
@@ -49,11 +49,11 @@ enum {
 
 #define CPK_MAX_MODES 8
 
-/* Kernel knobs.  Mirrors MttkrpPlan (mttkrp.py:227-263): `unroll` (F) and
+/* Kernel knobs.  Mirrors MttkrpPlan (mttkrp.py:53-89): `unroll` (F) and
  * `tile_volume` (N_T) keep their meaning; `rank_tile` is the GPU rank tile
  * (the paper's F*b_y column block); `splits` is the number of CTAs sharing
  * one output tile along the contraction (the reference's tiles-per-slice,
- * mttkrp.py:528-529).  Zero in any field means "choose" (cpk_plan_resolve). */
+ * mttkrp.py:354-355).  Zero in any field means "choose" (cpk_plan_resolve). */
 typedef struct cpk_plan {
   int32_t rank_tile;    /* 0 | 32 | 64 | 128                          */
   int32_t block_rows;   /* 0 | 64 | 128 (mode-k rows per CTA)          */
@@ -82,7 +82,7 @@ const char* cpk_version(void);
 
 /* Fill every zero field of *plan for this problem; validates the problem.
  * Replaces the CPU worker-pool / tile-volume resolution of
- * mttkrp.py:301-318 and plan_for_mode's clamp (mttkrp.py:568-575). */
+ * mttkrp.py:127-144 and plan_for_mode's clamp (mttkrp.py:394-401). */
 int cpk_plan_resolve(int d, const int64_t* dims, int mode, int64_t rank,
                      cpk_plan* plan);
 
@@ -94,8 +94,8 @@ int cpk_mttkrp_workspace_bytes(int d, const int64_t* dims, int mode,
 /*
  * G = Y_(mode) (A_{d-1} (.) ... (.) A_{mode+1} (.) A_{mode-1} (.) ... (.) A_0) diag(lam)
  *
- * Replaces mttkrp_tile / tile_kernel (mttkrp.py:519-549, _kernels.py:96-174)
- * and, with splits == 1, mttkrp_slice (mttkrp.py:491-516).
+ * Replaces mttkrp_tile / tile_kernel (mttkrp.py:345-375, _kernels.py:96-174)
+ * and, with splits == 1, mttkrp_slice (mttkrp.py:317-342).
  *   y        device, N = prod(dims) float64, first mode fastest
  *   factors  host array of d device pointers; factors[m] is dims[m] x ld[m]
  *            row-major (ld[m] >= rank); factors[mode] is not read

@@ -11,7 +11,7 @@
  *                       columns, p = lam[j]*y*A_0*A_1*... (modes ascending,
  *                       k skipped), out[row, j] += p.  The canonical order.
  *   orc_mttkrp_tile  -- tile_kernel + accum_tile (_kernels.py:96-174) with the
- *                       reference's private-copy merge (mttkrp.py:453-460):
+ *                       reference's private-copy merge (mttkrp.py:279-286):
  *                       tiles enumerated slice-major, odometer walk, column
  *                       blocks of width F, per-thread private output copies
  *                       summed in thread order.  OpenMP replaces numba's prange.
@@ -100,7 +100,7 @@ static void accum_tile(const double* data, int d, const int64_t* dims, const int
   }
 }
 
-/* tile_kernel (_kernels.py:162-174) + _run_private_copy (mttkrp.py:453-460).
+/* tile_kernel (_kernels.py:162-174) + _run_private_copy (mttkrp.py:279-286).
  * workers <= 0: all OpenMP threads.  Returns the worker count used. */
 int orc_mttkrp_tile(const double* data, int d, const int64_t* dims, int k, const double* const* fac,
                     const double* lam, int64_t R, int64_t f_cols, int64_t n_t, int workers, double* out) {

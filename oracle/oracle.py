@@ -4,9 +4,9 @@ CPU restatement of the reference's MTTKRP / CP-ALS path:
 
 * ctypes access to oracle/liboracle.so (mttkrp_ref.c): the serial reference
   kernel (_kernels.py:39-57), the TILE kernel with private-copy merge
-  (_kernels.py:96-174, mttkrp.py:453-460) and a row-restricted reference.
+  (_kernels.py:96-174, mttkrp.py:279-286) and a row-restricted reference.
 * `mttkrp_gemm`: numpy restatement of the Phan partial-KRP baseline
-  (mttkrp.py:404-450, dtensor.py:305-331) -- the fast oracle at c2/c3 sizes.
+  (mttkrp.py:230-276, dtensor.py:305-331) -- the fast oracle at c2/c3 sizes.
 * `cp_als`: numpy/scipy restatement of cpals.cp_als (cpals.py:75-171).
 """
 
@@ -117,7 +117,7 @@ def khatri_rao_chain(mats):
 
 
 def mttkrp_gemm(data, dims, k, factors, lam=None) -> np.ndarray:
-    """Phan partial-KRP GEMM baseline (mttkrp.py:404-450), lam applied once."""
+    """Phan partial-KRP GEMM baseline (mttkrp.py:230-276), lam applied once."""
     dims = tuple(int(x) for x in dims)
     d = len(dims)
     r = factors[0].shape[1]

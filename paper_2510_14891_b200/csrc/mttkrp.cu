@@ -1,7 +1,7 @@
 // Matrix-free dense MTTKRP for B200 (sm_100a), FP64 on the CUDA-core DFMA pipe.
 //
 // What it computes (reference: mttkrp_tile / tile_kernel / accum_tile,
-// pkg/src/cpkern/mttkrp.py:519-549 and _kernels.py:96-174):
+// pkg/src/cpkern/mttkrp.py:345-375 and _kernels.py:96-174):
 //
 //     G[n, j] = lam[j] * sum_{i : i_k = n} y[i] * prod_{m != k} A_m[i_m, j]
 //
@@ -33,7 +33,7 @@
 // Parallelism: grid = (rank tiles, row tiles, splits).  Rank tiles are the
 // fastest grid index so the CTAs that share one tensor tile run together and
 // the tile is read from HBM once and from L2 R/BN times.  `splits` cuts the
-// chunk sequence (the reference's tiles-per-slice, mttkrp.py:528-529) into
+// chunk sequence (the reference's tiles-per-slice, mttkrp.py:354-355) into
 // contiguous ranges; partials land in a [splits, I_k, R] workspace that one
 // deterministic kernel sums in split order -- no floating-point atomics, so
 // results are bit-reproducible run to run.
@@ -322,7 +322,7 @@ __global__ void __launch_bounds__((BM / 8) * (BN / 8), 1)
 }
 
 // Deterministic split-K reduction (the private-copy merge of
-// mttkrp._run_private_copy, mttkrp.py:453-460: partials summed in a fixed
+// mttkrp._run_private_copy, mttkrp.py:279-286: partials summed in a fixed
 // order, then lam folded once).
 __global__ void splitk_reduce_f64(const double* __restrict__ w, int splits, int64_t Ik, int64_t R,
                                   int64_t ldw, int64_t split_stride, const double* __restrict__ lam,

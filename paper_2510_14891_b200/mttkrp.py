@@ -2,8 +2,8 @@
 
 Drop-in for the cpkern.mttkrp dispatcher (pkg/src/cpkern/mttkrp.py): the same
 Variant / MttkrpPlan / MttkrpStats / MttkrpOutput types, `run(y, m, plan)`
-(mttkrp.py:552-565), the per-variant entry points, `plan_for_mode`
-(mttkrp.py:568-575) and the Eq. 6 tile heuristic (mttkrp.py:578-602), plus
+(mttkrp.py:378-391), the per-variant entry points, `plan_for_mode`
+(mttkrp.py:394-401) and the Eq. 6 tile heuristic (mttkrp.py:404-428), plus
 the north-star convenience `mttkrp(tensor, factors, mode)`.
 
 Every variant executes the hand-written sm_100a kernel behind
@@ -19,7 +19,7 @@ variants keep from the reference is their *partitioning* and *accounting*:
 Stats (element_visits, atomic_updates, ...) follow the reference formulas so
 reports stay comparable; `seconds` is the CUDA-event time of the kernel plus
 the split-K merge on the launching stream (the reference times kernel +
-private-copy merge, mttkrp.py:453-460), read lazily so timing adds no sync.
+private-copy merge, mttkrp.py:279-286), read lazily so timing adds no sync.
 """
 
 from __future__ import annotations
@@ -53,7 +53,7 @@ class Variant(str, Enum):
 
 @dataclass(frozen=True)
 class MttkrpPlan:
-    """How to run one MTTKRP (mttkrp.py:227-263), with the GPU knobs added.
+    """How to run one MTTKRP (mttkrp.py:53-89), with the GPU knobs added.
 
     ``unroll`` (F), ``team_width`` (b_x) and ``vector_width`` (b_y) keep the
     paper's meaning; on the GPU the column block is the rank tile, so they
@@ -105,7 +105,7 @@ class MttkrpPlan:
 
 @dataclass
 class MttkrpStats:
-    """Work accounting and timing for one MTTKRP (mttkrp.py:266-285)."""
+    """Work accounting and timing for one MTTKRP (mttkrp.py:92-111)."""
 
     variant: Variant
     mode: int
@@ -272,7 +272,7 @@ def _stats(variant, y, m, plan, p, timer, *, element_visits, atomic_updates, til
 
 
 def mttkrp_reference(y: DenseTensor, m: KruskalTensor, mode: int) -> MttkrpOutput:
-    """mttkrp.py:328-339 signature; runs the sm_100a kernel with one split."""
+    """mttkrp.py:154-165 signature; runs the sm_100a kernel with one split."""
     _check_inputs(y, m, mode)
     plan = MttkrpPlan(Variant.REFERENCE, int(mode), splits=1)
     plan.validate(y.dims, m.rank)
@@ -337,7 +337,7 @@ def mttkrp_b200(y: DenseTensor, m: KruskalTensor, plan: MttkrpPlan) -> MttkrpOut
 
 
 def run(y: DenseTensor, m: KruskalTensor, plan: MttkrpPlan, **kwargs) -> MttkrpOutput:
-    """Dispatch one MTTKRP according to the plan's variant (mttkrp.py:552-565).
+    """Dispatch one MTTKRP according to the plan's variant (mttkrp.py:378-391).
 
     Budget kwargs of the CPU oracles (budget_bytes, scratch_cap_bytes) are
     accepted and ignored: the matrix-free kernel allocates no KRP.
@@ -381,7 +381,7 @@ def mttkrp(tensor, factors, mode: int, weights=None, plan: MttkrpPlan | None = N
 
 def plan_for_mode(plan: MttkrpPlan, dims, mode: int) -> MttkrpPlan:
     """Copy of ``plan`` retargeted at ``mode``; tile volume clamped to N_S
-    (mttkrp.py:568-575)."""
+    (mttkrp.py:394-401)."""
     p = replace(plan, mode=mode)
     if p.variant == Variant.TILE and p.tile_volume is not None:
         n_s = num_elements(dims) // dims[mode]
@@ -390,7 +390,7 @@ def plan_for_mode(plan: MttkrpPlan, dims, mode: int) -> MttkrpPlan:
 
 
 def heuristic_tile_width(dims, machine) -> int:
-    """Eq. 6 (mttkrp.py:578-597): w^(d-1) s_f c/2 = s_LM/4."""
+    """Eq. 6 (mttkrp.py:404-423): w^(d-1) s_f c/2 = s_LM/4."""
     dims = tuple(int(x) for x in dims)
     d = len(dims)
     if d < 2:
@@ -407,7 +407,7 @@ def heuristic_tile_width(dims, machine) -> int:
 
 
 def heuristic_tile_volume(dims, machine) -> int:
-    """N_T = w^(d-1) for the heuristic width (mttkrp.py:600-602)."""
+    """N_T = w^(d-1) for the heuristic width (mttkrp.py:426-428)."""
     return heuristic_tile_width(dims, machine) ** (len(dims) - 1)
 
 

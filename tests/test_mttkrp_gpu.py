@@ -86,7 +86,7 @@ def test_zero_tensor_and_stats():
     assert np.array_equal(out.matrix, np.zeros((4, 3)))
     assert out.stats.element_visits == 24 and out.stats.atomic_updates == 0
     assert out.stats.seconds > 0
-    # TILE atomic-count accounting follows mttkrp.py:539-549 exactly
+    # TILE atomic-count accounting follows mttkrp.py:365-375 exactly
     dims = (5, 4, 6)
     y = ck.DenseTensor(dims, rng_for(17).random(120))
     m = ck.KruskalTensor(np.ones(7), [rng_for(18).random((n, 7)) for n in dims])
