@@ -279,3 +279,20 @@ def test_landed_pieces_are_bit_identical(dims):
             for lo, hi in zip(cuts[:-1], cuts[1:]):
                 mttkrp_device(y, dims, fs, k, None, plan, out=out, landed=(lo, hi))
             assert torch.equal(out, ref), (dims, k, plan)
+
+
+@pytest.mark.parametrize("dims", [(12, 7, 9), (5, 6, 4, 7), (9, 13)])
+def test_cublas_gemm_baseline_parity(dims):
+    """The library comparison baseline (partial KRPs + cuBLAS DGEMM,
+    mttkrp.py:230-276) is itself checked against the oracle."""
+    from paper_2510_14891_b200.baselines import mttkrp_gemm_cublas
+
+    rank = 11
+    y = rng_for(21).random(int(np.prod(dims)))
+    fs = [rng_for(22 + j).random((n, rank)) for j, n in enumerate(dims)]
+    lam = rng_for(23).random(rank) + 0.5
+    yd = torch.from_numpy(y).cuda()
+    fd = [torch.from_numpy(a).cuda() for a in fs]
+    for k in range(len(dims)):
+        got = mttkrp_gemm_cublas(yd, dims, fd, k, torch.from_numpy(lam).cuda()).cpu().numpy()
+        assert oracle.rel_err(got, oracle.mttkrp_ref(y, dims, k, fs, lam)) <= TOL, (dims, k)
