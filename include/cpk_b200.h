@@ -44,7 +44,8 @@ enum {
   CPK_ERR_RESOURCE = 4,  /* ResourceError   (workspace too small)        */
   CPK_ERR_CUDA = 5,      /* launch / runtime failure                     */
   CPK_ERR_NOT_PD = 6,    /* Cholesky failed: Gamma not positive definite */
-  CPK_ERR_LIB = 7        /* cuSOLVER failure                             */
+  CPK_ERR_LIB = 7,       /* cuSOLVER failure                             */
+  CPK_ERR_FORMAT = 8     /* FormatError     (dtensor.py:359-382)         */
 };
 
 #define CPK_MAX_MODES 8
@@ -195,6 +196,22 @@ int cpk_fill_uniform_f64(double* x, int64_t n, uint64_t seed, int64_t offset,
 int cpk_fill_uniform_slab_f64(double* x, int d, const int64_t* global_dims,
                               int mode, int64_t lo, int64_t hi, uint64_t seed,
                               void* stream);
+
+/* DTEN v1 files (dtensor.py:334-382): shape of the file's tensor (header
+ * validated as the reference does; FormatError -> CPK_ERR_FORMAT).  dims
+ * must hold CPK_MAX_MODES entries. */
+int cpk_dten_read_header(const char* path, int* d, int64_t* dims);
+
+/* Load the slab [lo, hi) along `mode` of a DTEN file straight into device
+ * memory `dst` (dst_elems = the slab's volume), as its own first-mode-fastest
+ * tensor: pread through `threads` reader threads (0 = host cores, 8..32) into two pinned
+ * staging buffers, each streamed with cudaMemcpyAsync on `stream` while the
+ * other fills.  (lo, hi) = (0, dims[mode]) loads the whole tensor; the
+ * sharded driver loads only its rows.  Returns after the last copy has
+ * been enqueued and the staging buffers have drained. */
+int cpk_dten_load_slab_f64(const char* path, int mode, int64_t lo, int64_t hi,
+                           double* dst, int64_t dst_elems, int threads,
+                           void* stream);
 
 /* Device-side FP64 pipe probe: the larger achieved FLOP/s of a
  * register-resident DFMA loop and a register-resident DMMA (mma.sync

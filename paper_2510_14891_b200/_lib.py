@@ -17,6 +17,7 @@ from .errors import (
     DeviceError,
     IndexRangeError,
     ParameterError,
+    FormatError,
     ResourceError,
     ShapeError,
 )
@@ -32,6 +33,7 @@ _CODE_TO_EXC = {
     5: DeviceError,
     6: DeviceError,
     7: DeviceError,
+    8: FormatError,
 }
 CPK_ERR_NOT_PD = 6
 CPK_MAX_MODES = 8
@@ -84,6 +86,8 @@ _PROTOS = {
     "cpk_fill_uniform_f64": (C.c_int, [_P, _I64, C.c_uint64, _I64, _P]),
     "cpk_fill_uniform_slab_f64": (C.c_int, [_P, C.c_int, C.POINTER(_I64), C.c_int, _I64, _I64, C.c_uint64, _P]),
     "cpk_fp64_peak_probe": (C.c_int, [C.POINTER(C.c_double), C.POINTER(C.c_double)]),
+    "cpk_dten_read_header": (C.c_int, [C.c_char_p, C.POINTER(C.c_int), C.POINTER(_I64)]),
+    "cpk_dten_load_slab_f64": (C.c_int, [C.c_char_p, C.c_int, _I64, _I64, _P, _I64, C.c_int, _P]),
 }
 
 _lock = threading.Lock()

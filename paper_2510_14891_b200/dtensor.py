@@ -15,7 +15,7 @@ import numpy as np
 import torch
 
 from ._device import require_cuda
-from .errors import IndexRangeError, ShapeError
+from .errors import IndexRangeError, ParameterError, ShapeError
 
 
 def check_dims(dims) -> tuple:
@@ -194,3 +194,80 @@ def check_mode(ndim: int, mode: int) -> int:
     if not 0 <= mode < ndim:
         raise IndexRangeError(f"mode {mode} out of range [0, {ndim - 1}]")
     return mode
+
+
+# ------------------------------------------------------------------ DTEN v1
+# dtensor.py:334-382: "DTEN", u32 version 1, u32 d, u64 dims[d], u32 element
+# type 1 (float64), then the float64 payload first mode fastest.
+DTEN_MAGIC = b"DTEN"
+DTEN_VERSION = 1
+DTEN_FLOAT64 = 1
+
+
+def write_dten(path, t: DenseTensor) -> None:
+    """Write a tensor as a DTEN v1 file (dtensor.py:334-340)."""
+    import struct
+
+    data = t.data.detach().cpu().numpy() if isinstance(t.data, torch.Tensor) else t.data
+    with open(path, "wb") as f:
+        f.write(struct.pack("<4sII", DTEN_MAGIC, DTEN_VERSION, t.ndim))
+        f.write(struct.pack(f"<{t.ndim}Q", *t.dims))
+        f.write(struct.pack("<I", DTEN_FLOAT64))
+        f.write(np.ascontiguousarray(data, dtype="<f8").tobytes())
+
+
+def read_dten_header(path) -> tuple:
+    """Shape recorded in a DTEN file, without reading the payload
+    (dtensor.py:343-347); parsed and validated by the native reader."""
+    import ctypes
+
+    from . import _lib
+
+    d = ctypes.c_int(0)
+    dims = (ctypes.c_int64 * _lib.CPK_MAX_MODES)()
+    _lib.check(_lib.load().cpk_dten_read_header(str(path).encode(), ctypes.byref(d), dims), "DTEN header")
+    return tuple(int(dims[i]) for i in range(d.value))
+
+
+def read_dten(path, device=None, mode: int = 0, lo: int | None = None, hi: int | None = None) -> DenseTensor:
+    """Read a DTEN file (dtensor.py:350-357).
+
+    ``device=None``: host payload, like the reference.  With a CUDA device
+    the payload goes straight to HBM through the native loader
+    (cpk_dten_load_slab_f64: threaded preads into pinned staging buffers,
+    double-buffered async copies) and, with ``lo``/``hi``, only the slab
+    [lo, hi) along ``mode`` is read -- one rank's shard of the sharded
+    CP-ALS driver, as its own first-mode-fastest tensor.
+    """
+    from . import _lib
+    from ._device import stream_ptr
+
+    dims = read_dten_header(path)
+    mode = check_mode(len(dims), mode)
+    lo = 0 if lo is None else int(lo)
+    hi = dims[mode] if hi is None else int(hi)
+    if not 0 <= lo <= hi <= dims[mode]:
+        raise IndexRangeError(f"slab [{lo}, {hi}) outside [0, {dims[mode]})")
+    sub = tuple(hi - lo if m == mode else e for m, e in enumerate(dims))
+    n = num_elements(sub) if hi > lo else 0
+    if device is None:
+        if (lo, hi) != (0, dims[mode]):
+            raise ParameterError("host reads load the whole tensor; pass a CUDA device for a slab")
+        off = 12 + 8 * len(dims) + 4
+        data = np.fromfile(path, dtype="<f8", offset=off).astype(np.float64)
+        if data.size != num_elements(dims):
+            from .errors import FormatError
+
+            raise FormatError(f"payload holds {8 * data.size} bytes, shape {dims} needs {8 * num_elements(dims)}")
+        return DenseTensor(dims, data)
+    dev = require_cuda(device)
+    if n == 0:
+        raise ShapeError(f"empty slab [{lo}, {hi}) of mode {mode}")
+    buf = torch.empty(n, dtype=torch.float64, device=dev)
+    with torch.cuda.device(dev):
+        _lib.check(
+            _lib.load().cpk_dten_load_slab_f64(str(path).encode(), mode, lo, hi, buf.data_ptr(), n, 0,
+                                               stream_ptr(dev)),
+            "DTEN load",
+        )
+    return DenseTensor(sub, buf)

@@ -255,6 +255,18 @@ def uniform_slab(part: Partition, rank: int, seed: int = 0, device=None) -> Dens
     return DenseTensor(local, buf)
 
 
+def dten_slab(path, part: Partition, rank: int, device=None) -> DenseTensor:
+    """This rank's slab of a DTEN file, read straight into its GPU
+    (cpk_dten_load_slab_f64): only rows [lo, hi) of the partition mode are
+    read from disk, so ingest needs no redistribution."""
+    from .dtensor import read_dten, read_dten_header
+
+    if tuple(read_dten_header(path)) != tuple(part.dims):
+        raise ShapeError(f"{path} holds {read_dten_header(path)}, partition is for {part.dims}")
+    lo, hi = part.bounds(rank)
+    return read_dten(path, device=require_cuda(device), mode=part.mode, lo=lo, hi=hi)
+
+
 def cp_als_sharded(y_local, part: Partition, config: AlsConfig, comm: Comm | None = None, ops=None,
                    gather: bool = True):
     """CP-ALS over a row-partitioned tensor; every rank returns the same

@@ -17,6 +17,9 @@ Fixtures (numpy .npz, float64):
                 plus 8 rows per mode from mttkrp_reference on single-slice
                 sub-tensors
   c3.npz     -- config 3 (128^4, R=256): G for all modes (mttkrp_gemm)
+  dten/      -- DTEN v1 files written by cpkern.dtensor.write_dten (a 4-way
+                Philox tensor and a 1-way one) and the reference's verdict
+                (shape, or the FormatError message) on malformed variants
   als.npz    -- cp_als fit trajectories: the planted suites of test_cpals.py
                 (REFERENCE and GEMM plans), and config 3 for 10 sweeps (GEMM)
 Inputs for c1-c3 follow the reference CLI recipe (cli.py:133-141):
@@ -159,8 +162,46 @@ def make_als():
     np.savez_compressed(OUT / "als.npz", **store)
 
 
+def make_dten():
+    import json
+
+    from cpkern.dtensor import read_dten, read_dten_header, write_dten
+    from cpkern.errors import FormatError
+
+    d = OUT / "dten"
+    d.mkdir(exist_ok=True)
+    good = {"t4.dten": (6, 5, 4, 3), "t1.dten": (7,)}
+    for name, dims in good.items():
+        write_dten(d / name, ck.DenseTensor(dims, random_tensor(dims, 5).data))
+    raw = (d / "t4.dten").read_bytes()
+    bad = {
+        "bad_magic.dten": b"DTEX" + raw[4:],
+        "bad_version.dten": raw[:4] + (2).to_bytes(4, "little") + raw[8:],
+        "zero_modes.dten": raw[:8] + (0).to_bytes(4, "little") + raw[12:],
+        "bad_etype.dten": raw[:12 + 32] + (2).to_bytes(4, "little") + raw[12 + 36:],
+        "zero_extent.dten": raw[:12] + (0).to_bytes(8, "little") + raw[20:],
+        "truncated_header.dten": raw[:10],
+        "truncated_dims.dten": raw[:30],
+        "short_payload.dten": raw[:-8],
+        "long_payload.dten": raw + bytes(8),
+    }
+    verdict = {}
+    for name, blob in bad.items():
+        (d / name).write_bytes(blob)
+    for name in list(good) + list(bad):
+        try:
+            shape = read_dten_header(d / name)
+            read_dten(d / name)
+            verdict[name] = {"dims": list(shape)}
+        except FormatError as exc:
+            verdict[name] = {"error": str(exc)}
+    (d / "verdict.json").write_text(json.dumps(verdict, indent=1) + "\n")
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["small", "c1", "c2", "c3", "als"]
+    which = sys.argv[1:] or ["small", "c1", "c2", "c3", "als", "dten"]
+    if "dten" in which:
+        make_dten()
     if "small" in which:
         make_small()
     if "c1" in which:

@@ -130,3 +130,30 @@ def test_no_cpu_fallback():
         ck.run(y, m, MttkrpPlan(Variant.B200, 0))
     with pytest.raises(ck.DeviceError):
         ck.cp_als(y, ck.AlsConfig(rank=2))
+
+
+def test_dten_reader_matches_reference_verdicts(tmp_path):
+    """DTEN v1 (dtensor.py:334-382): files written by the reference's
+    write_dten, and malformed variants, get the reference's verdict (shape,
+    or FormatError with its message) from the native header reader; our
+    writer reproduces the reference's bytes."""
+    import json
+    from pathlib import Path
+
+    gdir = Path(__file__).resolve().parent / "golden" / "dten"
+    verdict = json.loads((gdir / "verdict.json").read_text())
+    for name, v in verdict.items():
+        if "dims" in v:
+            assert ck.read_dten_header(gdir / name) == tuple(v["dims"])
+            t = ck.read_dten(gdir / name)
+            assert t.dims == tuple(v["dims"]) and t.data.dtype == np.float64
+            out = tmp_path / name
+            ck.write_dten(out, t)
+            assert out.read_bytes() == (gdir / name).read_bytes()
+        else:
+            with pytest.raises(ck.FormatError) as exc:
+                ck.read_dten_header(gdir / name)
+                ck.read_dten(gdir / name)
+            assert str(exc.value).endswith(v["error"]), (name, str(exc.value), v["error"])
+    with pytest.raises(ck.FormatError):
+        ck.read_dten_header(tmp_path / "missing.dten")
