@@ -20,6 +20,7 @@ Fixtures (numpy .npz, float64):
   dten/      -- DTEN v1 files written by cpkern.dtensor.write_dten (a 4-way
                 Philox tensor and a 1-way one) and the reference's verdict
                 (shape, or the FormatError message) on malformed variants
+  model.json -- cpkern.perfmodel traffic models / predicted times (sweep columns)
   als.npz    -- cp_als fit trajectories: the planted suites of test_cpals.py
                 (REFERENCE and GEMM plans), and config 3 for 10 sweeps (GEMM)
 Inputs for c1-c3 follow the reference CLI recipe (cli.py:133-141):
@@ -162,6 +163,28 @@ def make_als():
     np.savez_compressed(OUT / "als.npz", **store)
 
 
+def make_model():
+    """Traffic-model values from cpkern.perfmodel on a few shapes/specs."""
+    import json
+
+    from cpkern import perfmodel as pmr
+
+    cases = []
+    for dims, rank, mode, nt in [((401, 201, 12, 501), 32, 0, 256), ((129, 129, 129, 12, 39), 32, 2, 4096),
+                                 ((1024, 1024, 1024), 2000, 1, 131044), ((64, 64, 64), 16, 2, 1)]:
+        for mach in ("nvidia-h100", "intel-8480p"):
+            ms = pmr.bundled_machine(mach)
+            f = pmr.flops(dims, rank)
+            m0 = pmr.mem_zero(dims, rank, mode, nt)
+            m0lm = pmr.mem_zero_lm(dims, rank, mode, nt, ms.l)
+            minf = pmr.mem_infty(dims, rank)
+            cases.append({"dims": list(dims), "rank": rank, "mode": mode, "nt": nt, "machine": mach, "f": f,
+                          "mem_zero": m0, "mem_zero_lm": m0lm, "mem_infty": minf,
+                          "T0": pmr.predict_seconds(f, m0, ms), "T0LM": pmr.predict_seconds(f, m0lm, ms),
+                          "TInf": pmr.predict_seconds(f, minf, ms), "gbps": pmr.gbytes_per_s(m0, 0.37)})
+    (OUT / "model.json").write_text(json.dumps(cases, indent=1) + "\n")
+
+
 def make_dten():
     import json
 
@@ -199,7 +222,9 @@ def make_dten():
 
 
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["small", "c1", "c2", "c3", "als", "dten"]
+    which = sys.argv[1:] or ["small", "c1", "c2", "c3", "als", "dten", "model"]
+    if "model" in which:
+        make_model()
     if "dten" in which:
         make_dten()
     if "small" in which:

@@ -157,3 +157,26 @@ def test_dten_reader_matches_reference_verdicts(tmp_path):
             assert str(exc.value).endswith(v["error"]), (name, str(exc.value), v["error"])
     with pytest.raises(ck.FormatError):
         ck.read_dten_header(tmp_path / "missing.dten")
+
+
+def test_traffic_models_match_reference():
+    """The sweep harness's model columns (perfmodel.py:121-210) reproduce the
+    reference's numbers exactly (tests/golden/model.json)."""
+    import json
+    from pathlib import Path
+
+    from paper_2510_14891_b200 import perfmodel as pm
+
+    cases = json.loads((Path(__file__).resolve().parent / "golden" / "model.json").read_text())
+    for c in cases:
+        ms = pm.bundled_machine(c["machine"])
+        dims, r, k, nt = tuple(c["dims"]), c["rank"], c["mode"], c["nt"]
+        f = pm.flops(dims, r)
+        assert f == c["f"]
+        assert pm.mem_zero(dims, r, k, nt) == c["mem_zero"]
+        assert pm.mem_zero_lm(dims, r, k, nt, ms.l) == c["mem_zero_lm"]
+        assert pm.mem_infty(dims, r) == c["mem_infty"]
+        assert pm.predict_seconds(f, c["mem_zero"], ms) == c["T0"]
+        assert pm.predict_seconds(f, c["mem_zero_lm"], ms) == c["T0LM"]
+        assert pm.predict_seconds(f, c["mem_infty"], ms) == c["TInf"]
+        assert pm.gbytes_per_s(c["mem_zero"], 0.37) == c["gbps"]
