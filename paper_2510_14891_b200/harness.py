@@ -29,11 +29,14 @@ import statistics
 
 import numpy as np
 
-from . import mttkrp as mt
+import importlib
+
 from . import perfmodel as pm
 from .dtensor import DenseTensor, num_elements
 from .errors import ParameterError
 from .kruskal import KruskalTensor
+
+mt = importlib.import_module(".mttkrp", __package__)  # the module (the package re-exports a function of this name)
 
 COLUMNS = ["variant", "mode", "rank", "tile_width", "N_T", "rep", "time_s", "gflops",
            "mops0", "mopsInf", "T0", "T0LM", "TInf", "atomic_updates"]
