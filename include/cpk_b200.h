@@ -63,7 +63,19 @@ typedef struct cpk_plan {
   int32_t sm_count;     /* 0 = query the device                        */
   int32_t block_k;      /* 0 | 16 | 32: chunk depth (contraction tile) */
   int32_t engine;       /* CPK_ENGINE_*: data-movement engine          */
+  int32_t merge;        /* CPK_MERGE_*: small-mode merging              */
 } cpk_plan;
+
+/* merge: a mode far smaller than the row tile can run as the (d-1)-way
+ * problem with its neighbour (mode-1 or mode+1) merged into the output rows,
+ * plus a small contraction with that neighbour's factor.  AUTO decides (only
+ * when rank_tile, block_rows, tile_volume, splits and block_k are all 0);
+ * cpk_plan_resolve then reports PREV/NEXT and the other fields describe the
+ * merged problem, so passing the resolved plan back runs the same thing. */
+#define CPK_MERGE_AUTO 0
+#define CPK_MERGE_NONE (-1)
+#define CPK_MERGE_PREV 1
+#define CPK_MERGE_NEXT 2
 
 /* engine: AUTO picks the warp-specialized TMA kernel with DMMA consumers
  * when the problem is aligned (even I_0 and leading dimensions, 16-byte

@@ -49,6 +49,7 @@ class CpkPlan(C.Structure):
         ("sm_count", C.c_int32),
         ("block_k", C.c_int32),
         ("engine", C.c_int32),
+        ("merge", C.c_int32),
     ]
 
 

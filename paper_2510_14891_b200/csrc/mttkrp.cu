@@ -488,11 +488,12 @@ static int64_t n_chunks_of(const Problem& pr, int bk) {
 //    reduction) stays under kWorkspaceBudget.
 // Within those bounds, the first split count whose CTAs fill whole waves.
 constexpr int64_t kChunksPerCta = 512;
+constexpr int64_t kMaxSplits = 4096;
 constexpr double kWorkspaceBudget = 2.0 * (1 << 30);
 
 static int auto_splits(int64_t tiles, int64_t chunks, int slots, double bytes_per_split) {
   const int64_t cap = std::max<int64_t>(1, int64_t(kWorkspaceBudget / std::max(bytes_per_split, 1.0)));
-  const int64_t max_s = std::max<int64_t>(1, std::min<int64_t>({chunks / 4, int64_t(4096), cap}));
+  const int64_t max_s = std::max<int64_t>(1, std::min<int64_t>({chunks / 4, kMaxSplits, cap}));
   const int64_t lo = std::min<int64_t>(max_s, std::max<int64_t>(1, ceil_div(chunks, kChunksPerCta)));
   double best = -1.0;
   int64_t best_s = lo;
@@ -616,8 +617,13 @@ static int resolve(const Problem& pr, cpk_plan* plan) {
   if (plan->splits < 0) return fail(CPK_ERR_PARAM, "splits must be >= 0");
   if (plan->splits == 0) {
     if (plan->tile_volume > 0) {
+      // N_T -> chunks per split; the reference's tiles land in W private
+      // copies (mttkrp.py:279-286), so the split count (= partial copies)
+      // is capped like the auto plan's: <= kMaxSplits and the workspace budget
       const int64_t cps = std::max<int64_t>(1, plan->tile_volume / cols_per_chunk);
-      plan->splits = int(std::min<int64_t>(ceil_div(chunks, cps), 1 << 20));
+      const double per_split = double(pr.Ik) * double((pr.R + 1) & ~int64_t(1)) * sizeof(double);
+      const int64_t cap = std::max<int64_t>(1, std::min<int64_t>(kMaxSplits, int64_t(kWorkspaceBudget / per_split)));
+      plan->splits = int(std::min<int64_t>(ceil_div(chunks, cps), cap));
     } else {
       const int64_t tiles = ceil_div(pr.Ik, bm) * ceil_div(pr.R, plan->rank_tile);
       int per_sm = 1;  // the TMA kernels take one CTA per SM
@@ -649,11 +655,128 @@ static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 
 
 using namespace cpk;
 
+// ---- small-extent modes: merge the output mode with an adjacent one
+// A mode of extent I_k far below the row tile (paper tensor A: I_2 = 12 in
+// 64-row tiles) wastes most of every CTA.  Merging it with a neighbour a
+// (adjacent in memory, so the tensor is simply reinterpreted as (d-1)-way)
+// gives I_k * I_a output rows: the kernel computes the partial MTTKRP
+// G'[(i_a, i_k), :] without A_a, and a small contraction finishes
+// G[i_k, :] = sum_{i_a} G'[(i_a, i_k), :] * A_a[i_a, :] (the same split the
+// reference's GEMM baseline makes for interior modes, mttkrp.py:257-265).
+// Only for auto plans (no rank tile / split / N_T / chunk depth forced).
+struct Merge {
+  int a = -1;                         // merged neighbour, -1 = none
+  int d2 = 0, mode2 = 0;
+  int64_t dims2[CPK_MAX_MODES] = {};
+  int64_t scale_last = 1;             // merged-mode slices per original last-mode slice
+};
+
+static double rate_of(int engine, int rank_tile) {
+  for (const TileChoice& c : kChoices)
+    if (c.engine == engine && c.rank_tile == rank_tile) return c.rate;
+  return 1.0;
+}
+
+// issued work per output row for the resolved plan (padded rows x padded
+// rank / rate / rows)
+static bool padded_cost(const Problem& pr, const cpk_plan& in, double* cost) {
+  cpk_plan p = in;
+  if (resolve(pr, &p) != CPK_OK) return false;
+  *cost = double(ceil_div(pr.Ik, p.block_rows) * p.block_rows) * double(ceil_div(pr.R, p.rank_tile) * p.rank_tile) /
+          rate_of(p.engine, p.rank_tile) / double(pr.Ik);
+  return true;
+}
+
+static bool plan_is_auto(const cpk_plan* p) {
+  return !p || (p->rank_tile == 0 && p->splits == 0 && p->tile_volume == 0 && p->block_rows == 0 && p->block_k == 0);
+}
+
+static bool merged_problem(const Problem& pr, int a, Merge* m) {
+  if (pr.d < 3 || a < 0 || a >= pr.d || (a != pr.k - 1 && a != pr.k + 1)) return false;
+  m->a = a;
+  m->d2 = pr.d - 1;
+  const int lo = std::min(a, pr.k);
+  for (int i = 0, j = 0; i < pr.d; ++i) {
+    if (i == lo + 1) continue;
+    m->dims2[j++] = i == lo ? pr.dims[lo] * pr.dims[lo + 1] : pr.dims[i];
+  }
+  m->mode2 = lo;
+  m->scale_last = (lo + 1 == pr.d - 1) ? pr.dims[pr.d - 2] : 1;
+  return true;
+}
+
+// The merge a plan asks for: forced PREV/NEXT, NONE, or (AUTO with an
+// otherwise automatic plan) the neighbour that cuts the padding overhead by
+// more than 15 %.
+static Merge choose_merge(const Problem& pr, const cpk_plan* plan_in) {
+  Merge best;
+  const int want = plan_in ? plan_in->merge : CPK_MERGE_AUTO;
+  if (want == CPK_MERGE_PREV || want == CPK_MERGE_NEXT) {
+    Merge m;
+    if (merged_problem(pr, want == CPK_MERGE_PREV ? pr.k - 1 : pr.k + 1, &m)) best = m;
+    return best;
+  }
+  if (want != CPK_MERGE_AUTO || pr.d < 3 || !plan_is_auto(plan_in)) return best;
+  cpk_plan base = plan_in ? *plan_in : cpk_plan{0, 0, 0, 0, 0, 0, 0, 0};
+  base.merge = CPK_MERGE_NONE;
+  double c_direct;
+  if (!padded_cost(pr, base, &c_direct)) return best;
+  double c_best = 0.85 * c_direct;  // merge only for a clear win
+  for (int a : {pr.k - 1, pr.k + 1}) {
+    Merge m;
+    if (!merged_problem(pr, a, &m)) continue;
+    Problem p2;
+    if (make_problem(m.d2, m.dims2, m.mode2, pr.R, &p2) != CPK_OK || p2.n_o > 3) continue;
+    double c;
+    if (!padded_cost(p2, base, &c)) continue;
+    // both costs are padding overheads (issued / useful work): the merged
+    // problem does the same useful work, N x R per mode
+    if (c < c_best) {
+      c_best = c;
+      best = m;
+    }
+  }
+  return best;
+}
+
+static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+// bytes of G' (merged rows x rank) placed after the inner workspace
+static size_t merged_out_bytes(const Problem& pr, const Merge& m) {
+  return size_t(pr.Ik) * size_t(pr.dims[m.a]) * size_t(pr.R) * sizeof(double);
+}
+
+__global__ static void merged_contract_f64(const double* __restrict__ gp, int64_t Ik, int64_t Ia, int64_t R,
+                                           int a_faster, const double* __restrict__ A, int64_t lda,
+                                           double* __restrict__ G, int64_t ldg) {
+  for (int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; idx < Ik * R;
+       idx += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t n = idx / R, j = idx - n * R;
+    double s = 0.0;
+    for (int64_t ia = 0; ia < Ia; ++ia) {
+      const int64_t row = a_faster ? ia + Ia * n : n + Ik * ia;
+      s = fma(gp[row * R + j], A[ia * lda + j], s);
+    }
+    G[n * ldg + j] = s;
+  }
+}
+
 extern "C" int cpk_plan_resolve(int d, const int64_t* dims, int mode, int64_t rank, cpk_plan* plan) {
   if (!plan) return fail(CPK_ERR_PARAM, "plan is NULL");
   Problem pr;
   int rc = make_problem(d, dims, mode, rank, &pr);
   if (rc) return rc;
+  const Merge mg = choose_merge(pr, plan);
+  if (mg.a >= 0) {  // the plan of the merged (d-1)-way problem the kernel runs
+    Problem p2;
+    rc = make_problem(mg.d2, mg.dims2, mg.mode2, rank, &p2);
+    if (rc) return rc;
+    plan->merge = mg.a < mode ? CPK_MERGE_PREV : CPK_MERGE_NEXT;
+    return resolve(p2, plan);
+  }
+  if (plan->merge != CPK_MERGE_AUTO && plan->merge != CPK_MERGE_NONE)
+    return fail(CPK_ERR_PARAM, "merge %d impossible for mode %d of a %d-way tensor", plan->merge, mode, d);
+  plan->merge = CPK_MERGE_NONE;
   return resolve(pr, plan);
 }
 
@@ -663,6 +786,17 @@ extern "C" int cpk_mttkrp_workspace_bytes(int d, const int64_t* dims, int mode, 
   Problem pr;
   int rc = make_problem(d, dims, mode, rank, &pr);
   if (rc) return rc;
+  const Merge mg = choose_merge(pr, plan);
+  if (mg.a >= 0) {
+    Problem p2;
+    rc = make_problem(mg.d2, mg.dims2, mg.mode2, rank, &p2);
+    if (rc) return rc;
+    cpk_plan q = *plan;
+    rc = resolve(p2, &q);
+    if (rc) return rc;
+    *bytes = align256(ws_bytes_for(p2, q)) + merged_out_bytes(pr, mg);
+    return CPK_OK;
+  }
   cpk_plan p = *plan;
   rc = resolve(pr, &p);
   if (rc) return rc;
@@ -705,7 +839,7 @@ struct Landed {
 static int mttkrp_impl(const double* y, int d, const int64_t* dims, int mode, const double* const* factors,
                        const int64_t* ld, const double* lam, int64_t rank, double* G, int64_t ldg,
                        const cpk_plan* plan_in, void* workspace, size_t ws_bytes, void* stream, int64_t landed_lo,
-                       int64_t landed_hi) {
+                       int64_t landed_hi, bool allow_merge = true) {
   const bool ranged = landed_hi >= 0;
   Problem pr;
   int rc = make_problem(d, dims, mode, rank, &pr);
@@ -727,10 +861,45 @@ static int mttkrp_impl(const double* y, int d, const int64_t* dims, int mode, co
     if (!factors[m]) return fail(CPK_ERR_PARAM, "factor %d is NULL", m);
     if (ld && ld[m] < rank) return fail(CPK_ERR_PARAM, "ld[%d] < rank", m);
   }
+  const Merge mg = allow_merge ? choose_merge(pr, plan_in) : Merge{};
+  if (allow_merge && mg.a < 0 && plan_in && (plan_in->merge == CPK_MERGE_PREV || plan_in->merge == CPK_MERGE_NEXT))
+    return fail(CPK_ERR_PARAM, "merge %d impossible for mode %d of a %d-way tensor", plan_in->merge, mode, d);
+  if (mg.a >= 0) {
+    Problem p2;
+    rc = make_problem(mg.d2, mg.dims2, mg.mode2, rank, &p2);
+    if (rc) return rc;
+    cpk_plan q = plan_in ? *plan_in : cpk_plan{0, 0, 0, 0, 0, 0, 0, 0};
+    rc = resolve(p2, &q);
+    if (rc) return rc;
+    const size_t inner = align256(ws_bytes_for(p2, q));
+    if (!workspace || ws_bytes < inner + merged_out_bytes(pr, mg))
+      return fail(CPK_ERR_RESOURCE, "merged-mode workspace needs %zu bytes, got %zu", inner + merged_out_bytes(pr, mg),
+                  ws_bytes);
+    double* gp = reinterpret_cast<double*>(static_cast<char*>(workspace) + inner);
+    const double* f2[CPK_MAX_MODES];
+    int64_t ld2[CPK_MAX_MODES];
+    const int lo = std::min(mg.a, mode);
+    for (int i = 0, j = 0; i < d; ++i) {
+      if (i == lo + 1) continue;
+      f2[j] = (i == lo) ? nullptr : factors[i];
+      ld2[j] = (i == lo) ? rank : (ld ? ld[i] : rank);
+      ++j;
+    }
+    const int64_t l_lo = ranged ? landed_lo * mg.scale_last : -1, l_hi = ranged ? landed_hi * mg.scale_last : -1;
+    rc = mttkrp_impl(y, mg.d2, mg.dims2, mg.mode2, f2, ld2, lam, rank, gp, rank, &q, workspace, inner, stream, l_lo,
+                     l_hi, false);
+    if (rc) return rc;
+    if (ranged && landed_hi < dims[d - 1]) return CPK_OK;  // contraction once everything landed
+    const int64_t total = pr.Ik * rank;
+    const unsigned blocks = unsigned(std::max<int64_t>(1, std::min<int64_t>(ceil_div(total, 256), 148 * 8)));
+    merged_contract_f64<<<blocks, 256, 0, st>>>(gp, pr.Ik, pr.dims[mg.a], rank, mg.a < mode ? 1 : 0, factors[mg.a],
+                                                ld ? ld[mg.a] : rank, G, ldg);
+    return check_launch("merged_contract");
+  }
   if (pr.n_o > 3)
     return fail(CPK_ERR_PARAM, "order d=%d > 5 is not supported by the sm_100a kernel", d);
 
-  cpk_plan plan = plan_in ? *plan_in : cpk_plan{0, 0, 0, 0, 0, 0, 0};
+  cpk_plan plan = plan_in ? *plan_in : cpk_plan{0, 0, 0, 0, 0, 0, 0, 0};
   rc = resolve(pr, &plan);
   if (rc) return rc;
   const size_t need = ws_bytes_for(pr, plan);

@@ -140,7 +140,9 @@ def _check_inputs(y: DenseTensor, m: KruskalTensor, mode: int) -> None:
         raise IndexRangeError(f"mode {mode} out of range [0, {y.ndim - 1}]")
 
 
-def _gpu_plan(plan: MttkrpPlan, dims, rank: int) -> _lib.CpkPlan:
+def _plan_request(plan: MttkrpPlan) -> _lib.CpkPlan:
+    """The CpkPlan the C side resolves itself: zero fields mean "choose"
+    (a fully automatic request may also merge a small mode with a neighbour)."""
     p = _lib.CpkPlan(plan.rank_tile, 0, 0, plan.splits, 0, plan.block_k, _ENGINES[plan.engine])
     v = Variant(plan.variant)
     if plan.splits == 0:
@@ -148,6 +150,12 @@ def _gpu_plan(plan: MttkrpPlan, dims, rank: int) -> _lib.CpkPlan:
             p.tile_volume = int(plan.tile_volume)
         elif v == Variant.SLICE:
             p.splits = 1
+    return p
+
+
+def _gpu_plan(plan: MttkrpPlan, dims, rank: int) -> _lib.CpkPlan:
+    """The resolved plan (for stats and validation; cpk_plan_resolve)."""
+    p = _plan_request(plan)
     dims_c = _lib.i64_array(dims)
     _lib.check(_lib.load().cpk_plan_resolve(len(dims), dims_c, int(plan.mode), int(rank), p), "plan")
     return p
@@ -179,10 +187,11 @@ def mttkrp_device(y_dev: torch.Tensor, dims, factors, mode: int, weights=None, p
     if plan is None:
         plan = MttkrpPlan(Variant.B200, mode)
     p = _gpu_plan(plan, dims, rank)
+    req = _plan_request(plan)  # the C side resolves (and may merge) from the request
     dims_c = _lib.i64_array(dims)
     nbytes = _lib.C.c_size_t(0)
     lib = _lib.load()
-    _lib.check(lib.cpk_mttkrp_workspace_bytes(d, dims_c, mode, rank, p, _lib.C.byref(nbytes)), "workspace")
+    _lib.check(lib.cpk_mttkrp_workspace_bytes(d, dims_c, mode, rank, req, _lib.C.byref(nbytes)), "workspace")
     ws = workspace(dev, nbytes.value)
     if out is None:
         out = torch.empty((dims[mode], rank), dtype=torch.float64, device=dev)
@@ -191,7 +200,7 @@ def mttkrp_device(y_dev: torch.Tensor, dims, factors, mode: int, weights=None, p
     lam_ptr = weights.data_ptr() if weights is not None else None
     timer = EventTimer(dev)
     args = (y_dev.data_ptr(), d, dims_c, mode, ptrs, lds, lam_ptr, rank, out.data_ptr(), out.stride(0),
-            p, ws.data_ptr() if ws is not None else None, nbytes.value, stream_ptr(dev))
+            req, ws.data_ptr() if ws is not None else None, nbytes.value, stream_ptr(dev))
     if landed is None:
         rc = lib.cpk_mttkrp_f64(*args)
     else:

@@ -65,6 +65,14 @@ def test_plan_resolution_fills_waves():
     assert rc == 0 and p.rank_tile == 32 and p.block_rows == 64
 
 
+def test_tiny_tile_volume_is_capped():
+    # paper tensor A with N_T = 2^3: one chunk per split would be 78k splits;
+    # the partial copies are capped like the auto plan's (<= 4096, <= 2 GiB)
+    rc, p = plan((401, 201, 12, 501), 0, 32, tile_volume=8)
+    assert rc == 0 and 1 <= p.splits <= 4096
+    assert p.splits * 401 * 32 * 8 <= 2 * 2 ** 30
+
+
 def test_plan_tile_volume_maps_to_splits():
     # N_S = 4096 in-slice elements, chunk = 16 of them: N_T = 256 -> 16 chunks/split
     rc, p = plan((64, 64, 64), 0, 16, tile_volume=256)
@@ -114,3 +122,19 @@ def test_mttkrp_rejects_bad_arguments_before_touching_the_device():
     assert rc == 3  # NULL tensor -> ParameterError
     rc = lib.cpk_mttkrp_f64(None, 3, dims, 5, ptrs, None, None, 2, None, 2, None, None, 0, None)
     assert rc == 2
+
+
+def test_small_mode_merge_is_reported_and_round_trips():
+    # paper tensor A, mode 2 (I = 12): merged with a neighbour; the resolved
+    # plan says which and describes the merged problem, and resolving the
+    # resolved plan again is a fixed point
+    rc, p = plan((401, 201, 12, 501), 2, 32)
+    assert rc == 0 and p.merge in (1, 2)
+    q = _lib.CpkPlan(p.rank_tile, p.block_rows, p.tile_volume, p.splits, p.sm_count, p.block_k, p.engine, p.merge)
+    assert _lib.load().cpk_plan_resolve(4, _lib.i64_array((401, 201, 12, 501)), 2, 32, q) == 0
+    assert (q.rank_tile, q.block_rows, q.splits, q.merge) == (p.rank_tile, p.block_rows, p.splits, p.merge)
+    # big modes stay unmerged; impossible forced merges are rejected
+    rc, p = plan((1024, 1024, 1024), 0, 2000)
+    assert rc == 0 and p.merge == -1
+    bad = _lib.CpkPlan(0, 0, 0, 0, 148, 0, 0, 1)  # PREV of mode 0
+    assert _lib.load().cpk_plan_resolve(3, _lib.i64_array((8, 8, 8)), 0, 4, bad) == 3

@@ -51,11 +51,12 @@ def test_heuristic_width_is_exact_floor(s_lm, d):
 @pytest.mark.parametrize("rank", [1, 16, 33, 64, 100, 130, 256, 300, 512, 2000])
 def test_rank_tile_heuristic_mirrors_the_c_planner(rows, rank):
     for tma in (True, False):
-        dims = (rows, 64, 66) if tma else (rows + 1, 64, 66)  # odd I_0 disables TMA
+        # 2-way: no small-mode merging, so the planner's rank tile is the table's
+        dims = (rows, 4224) if tma else (rows + 1, 4224)  # odd I_0 disables TMA
         r = rank if (not tma or rank % 2 == 0) else rank + 1
         eng, rt = heuristic_rank_tile(r, dims[0], tma=tma)
         p = _lib.CpkPlan(0, 0, 0, 0, 148, 0, 0)
-        _lib.check(_lib.load().cpk_plan_resolve(3, _lib.i64_array(dims), 0, r, p))
+        _lib.check(_lib.load().cpk_plan_resolve(len(dims), _lib.i64_array(dims), 0, r, p))
         assert (p.rank_tile, p.engine) == (rt, {"tma": 2, "cpasync": 1, "dmma": 3}[eng]), (dims, r)
 
 

@@ -296,3 +296,31 @@ def test_cublas_gemm_baseline_parity(dims):
     for k in range(len(dims)):
         got = mttkrp_gemm_cublas(yd, dims, fd, k, torch.from_numpy(lam).cuda()).cpu().numpy()
         assert oracle.rel_err(got, oracle.mttkrp_ref(y, dims, k, fs, lam)) <= TOL, (dims, k)
+
+
+@pytest.mark.parametrize("dims", [(41, 23, 3, 17), (300, 3, 40), (6, 50, 7, 2, 9), (17, 19, 2)])
+def test_small_modes_merge_with_a_neighbour(dims):
+    """Modes far smaller than the row tile run as the merged (d-1)-way
+    problem plus a contraction; results match the oracle, weights folded
+    once, for resident and streamed (landed) tensors."""
+    from paper_2510_14891_b200.mttkrp import mttkrp_device
+
+    rank = 33
+    y = rng_for(31).random(int(np.prod(dims)))
+    fs = [rng_for(32 + j).random((n, rank)) for j, n in enumerate(dims)]
+    lam = rng_for(30).random(rank) + 0.5
+    m = ck.KruskalTensor(lam, fs)
+    dev = torch.device("cuda", 0)
+    yd = torch.from_numpy(y).to(dev)
+    fd = [torch.from_numpy(a).to(dev) for a in fs]
+    lamd = torch.from_numpy(lam).to(dev)
+    for k in range(len(dims)):
+        ref = oracle.mttkrp_ref(y, dims, k, fs, lam)
+        got = ck.run(ck.DenseTensor(dims, y), m, MttkrpPlan(Variant.B200, k)).matrix
+        assert oracle.rel_err(got, ref) <= TOL, (dims, k)
+        whole, _, _ = mttkrp_device(yd, dims, fd, k, lamd)
+        out = torch.full_like(whole, float("nan"))
+        cuts = [0, 1, dims[-1] // 2, dims[-1]]
+        for lo, hi in zip(cuts[:-1], cuts[1:]):
+            mttkrp_device(yd, dims, fd, k, lamd, out=out, landed=(lo, hi))
+        assert torch.equal(out, whole), (dims, k)
