@@ -138,6 +138,16 @@ int cpk_mttkrp_f64_landed(const double* y, int d, const int64_t* dims,
                           void* workspace, size_t ws_bytes, void* stream,
                           int64_t landed_lo, int64_t landed_hi);
 
+/* The paper's baseline matrix-free GPU kernel MTTKRP-ELEM (PAPER.md:203-243,
+ * _kernels.py:60-93): one FP64 atomic per element and column (N R logical
+ * atomics).  For Fig. 4-style comparisons only: zero-fills G, then adds in
+ * atomic order (not bit-reproducible).  Same argument meaning as
+ * cpk_mttkrp_f64, no plan or workspace. */
+int cpk_mttkrp_elem_f64(const double* y, int d, const int64_t* dims, int mode,
+                        const double* const* factors, const int64_t* ld,
+                        const double* lam, int64_t rank, double* G,
+                        int64_t ldg, void* stream);
+
 /* Gram matrix A^T A (R x R), symmetrized exactly: upper triangle computed,
  * lower mirrored -- kruskal.gram (kruskal.py:110-114). */
 int cpk_gram_f64(const double* A, int64_t rows, int64_t rank, int64_t lda,

@@ -74,6 +74,10 @@ _PROTOS = {
         [_P, C.c_int, C.POINTER(_I64), C.c_int, C.POINTER(_P), C.POINTER(_I64), _P, _I64, _P, _I64,
          C.POINTER(CpkPlan), _P, C.c_size_t, _P, _I64, _I64],
     ),
+    "cpk_mttkrp_elem_f64": (
+        C.c_int,
+        [_P, C.c_int, C.POINTER(_I64), C.c_int, C.POINTER(_P), C.POINTER(_I64), _P, _I64, _P, _I64, _P],
+    ),
     "cpk_gram_f64": (C.c_int, [_P, _I64, _I64, _I64, _P, _P]),
     "cpk_hadamard_f64": (C.c_int, [C.POINTER(_P), C.c_int, C.c_int, _I64, _P, _P]),
     "cpk_solve_workspace_bytes": (C.c_int, [_I64, _I64, C.POINTER(C.c_size_t)]),

@@ -66,3 +66,21 @@ def mttkrp_gemm_cublas(y_dev: torch.Tensor, dims, factors, mode: int, weights=No
     c = y3.reshape(i_r, i_k * i_l).t() @ z_r  # (i_k i_l, R), i_l fastest in the row index
     z_l = _krp(factors[:mode])
     return torch.einsum("klj,lj->kj", c.view(i_k, i_l, -1), z_l)
+
+
+def mttkrp_elem_atomic(y_dev: torch.Tensor, dims, factors, mode: int, weights=None) -> torch.Tensor:
+    """The paper's baseline matrix-free GPU kernel, MTTKRP-ELEM: N R FP64
+    atomics into G (cpk_mttkrp_elem_f64).  Comparison only."""
+    from . import _lib
+    from ._device import stream_ptr
+
+    d = len(dims)
+    rank = next(int(f.shape[1]) for f in factors if f is not None)
+    out = torch.empty((dims[mode], rank), dtype=torch.float64, device=y_dev.device)
+    ptrs = _lib.ptr_array([f.data_ptr() if m != mode else 0 for m, f in enumerate(factors)])
+    lds = _lib.i64_array([f.stride(0) for f in factors])
+    _lib.check(_lib.load().cpk_mttkrp_elem_f64(
+        y_dev.data_ptr(), d, _lib.i64_array(dims), int(mode), ptrs, lds,
+        weights.data_ptr() if weights is not None else None, rank, out.data_ptr(), out.stride(0),
+        stream_ptr(y_dev.device)), "mttkrp elem")
+    return out

@@ -189,3 +189,76 @@ extern "C" int cpk_fp64_peak_probe(double* flops_per_s, double* seconds) {
   if (flops_per_s) *flops_per_s = std::max(f_f, f_m);
   return CPK_OK;
 }
+
+// ---------------------------------------------------------------- ELEM
+// The paper's baseline matrix-free GPU MTTKRP, MTTKRP-ELEM (
+// CPU restatement _kernels.py:60-93): every element adds lam_j y prod_m
+// A_m(i_m, j) into its output row with one FP64 atomic per column -- N R
+// logical atomics (mttkrp.py:309).  One warp per element, lanes over the
+// rank columns (coalesced factor rows and atomics).  A comparison variant
+// only: results are not bit-reproducible (atomic order).
+namespace cpk {
+struct ElemParams {
+  const double* y;
+  const double* fac[CPK_MAX_MODES];
+  int64_t ld[CPK_MAX_MODES];
+  int64_t dims[CPK_MAX_MODES];
+  int d, k;
+  int64_t n, R, ldg;
+  const double* lam;
+  double* G;
+};
+
+__global__ void __launch_bounds__(256) mttkrp_elem_atomic_f64(const __grid_constant__ ElemParams p) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
+  for (int64_t i = int64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); i < p.n; i += warps) {
+    int64_t sub[CPK_MAX_MODES], rem = i;
+    for (int m = 0; m < p.d; ++m) {
+      sub[m] = rem % p.dims[m];
+      rem /= p.dims[m];
+    }
+    const double yv = p.y[i];
+    double* grow = p.G + sub[p.k] * p.ldg;
+    for (int64_t j = lane; j < p.R; j += 32) {
+      double v = p.lam ? p.lam[j] * yv : yv;
+      for (int m = 0; m < p.d; ++m)
+        if (m != p.k) v *= p.fac[m][sub[m] * p.ld[m] + j];
+      atomicAdd(grow + j, v);
+    }
+  }
+}
+}  // namespace cpk
+
+extern "C" int cpk_mttkrp_elem_f64(const double* y, int d, const int64_t* dims, int mode,
+                                   const double* const* factors, const int64_t* ld, const double* lam, int64_t rank,
+                                   double* G, int64_t ldg, void* stream) {
+  if (!y || !dims || !factors || !G) return fail(CPK_ERR_PARAM, "NULL argument");
+  if (d < 1 || d > CPK_MAX_MODES) return fail(CPK_ERR_PARAM, "order d=%d unsupported", d);
+  if (mode < 0 || mode >= d) return fail(CPK_ERR_INDEX, "mode %d out of range [0, %d]", mode, d - 1);
+  if (rank < 1 || ldg < rank) return fail(CPK_ERR_PARAM, "bad rank / ldg");
+  ElemParams p{};
+  p.y = y;
+  p.d = d;
+  p.k = mode;
+  p.n = 1;
+  for (int m = 0; m < d; ++m) {
+    if (dims[m] < 1) return fail(CPK_ERR_SHAPE, "extent %d is %lld", m, (long long)dims[m]);
+    p.dims[m] = dims[m];
+    p.n *= dims[m];
+    p.fac[m] = m == mode ? nullptr : factors[m];
+    p.ld[m] = ld ? ld[m] : rank;
+    if (m != mode && !factors[m]) return fail(CPK_ERR_PARAM, "factor %d is NULL", m);
+  }
+  p.R = rank;
+  p.ldg = ldg;
+  p.lam = lam;
+  p.G = G;
+  cudaStream_t st = as_stream(stream);
+  if (cudaMemset2DAsync(G, size_t(ldg) * sizeof(double), 0, size_t(rank) * sizeof(double), size_t(dims[mode]), st) !=
+      cudaSuccess)
+    return fail(CPK_ERR_CUDA, "memset G");
+  const int64_t blocks = std::min<int64_t>((p.n + 7) / 8, 148 * 16);
+  mttkrp_elem_atomic_f64<<<unsigned(std::max<int64_t>(blocks, 1)), 256, 0, st>>>(p);
+  return check_launch("mttkrp_elem_atomic");
+}

@@ -285,7 +285,7 @@ def test_landed_pieces_are_bit_identical(dims):
 def test_cublas_gemm_baseline_parity(dims):
     """The library comparison baseline (partial KRPs + cuBLAS DGEMM,
     mttkrp.py:230-276) is itself checked against the oracle."""
-    from paper_2510_14891_b200.baselines import mttkrp_gemm_cublas
+    from paper_2510_14891_b200.baselines import mttkrp_elem_atomic, mttkrp_gemm_cublas
 
     rank = 11
     y = rng_for(21).random(int(np.prod(dims)))
@@ -294,8 +294,11 @@ def test_cublas_gemm_baseline_parity(dims):
     yd = torch.from_numpy(y).cuda()
     fd = [torch.from_numpy(a).cuda() for a in fs]
     for k in range(len(dims)):
+        ref = oracle.mttkrp_ref(y, dims, k, fs, lam)
         got = mttkrp_gemm_cublas(yd, dims, fd, k, torch.from_numpy(lam).cuda()).cpu().numpy()
-        assert oracle.rel_err(got, oracle.mttkrp_ref(y, dims, k, fs, lam)) <= TOL, (dims, k)
+        assert oracle.rel_err(got, ref) <= TOL, (dims, k)
+        got = mttkrp_elem_atomic(yd, dims, fd, k, torch.from_numpy(lam).cuda()).cpu().numpy()
+        assert oracle.rel_err(got, ref) <= TOL, (dims, k, "elem")
 
 
 @pytest.mark.parametrize("dims", [(41, 23, 3, 17), (300, 3, 40), (6, 50, 7, 2, 9), (17, 19, 2)])
