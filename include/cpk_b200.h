@@ -138,6 +138,20 @@ int cpk_mttkrp_f64_landed(const double* y, int d, const int64_t* dims,
                           void* workspace, size_t ws_bytes, void* stream,
                           int64_t landed_lo, int64_t landed_hi);
 
+/* Float32 MTTKRP (the north star's optional float32 path, <= 1e-4 relative
+ * Frobenius): tcgen05.mma kind::tf32 with a 3xTF32 split (hi*hi + hi*lo +
+ * lo*hi) so results keep fp32 accuracy; fp32 accumulation in TMEM, split-K
+ * partials merged in FP64.  Needs 2 <= d <= 5, a 16-byte aligned tensor
+ * with I_0 % 4 == 0, and 16-byte aligned factors with ld % 4 == 0 (TMA
+ * strides).  splits = 0 chooses; the workspace holds splits x I_k x
+ * round4(R) floats (0 bytes when splits == 1). */
+int cpk_mttkrp_f32_workspace_bytes(int d, const int64_t* dims, int mode,
+                                   int64_t rank, int splits, size_t* bytes);
+int cpk_mttkrp_f32(const float* y, int d, const int64_t* dims, int mode,
+                   const float* const* factors, const int64_t* ld,
+                   const float* lam, int64_t rank, float* G, int64_t ldg,
+                   int splits, void* workspace, size_t ws_bytes, void* stream);
+
 /* The paper's baseline matrix-free GPU kernel MTTKRP-ELEM (PAPER.md:203-243,
  * _kernels.py:60-93): one FP64 atomic per element and column (N R logical
  * atomics).  For Fig. 4-style comparisons only: zero-fills G, then adds in

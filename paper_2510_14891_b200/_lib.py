@@ -74,6 +74,13 @@ _PROTOS = {
         [_P, C.c_int, C.POINTER(_I64), C.c_int, C.POINTER(_P), C.POINTER(_I64), _P, _I64, _P, _I64,
          C.POINTER(CpkPlan), _P, C.c_size_t, _P, _I64, _I64],
     ),
+    "cpk_mttkrp_f32_workspace_bytes": (C.c_int, [C.c_int, C.POINTER(_I64), C.c_int, _I64, C.c_int,
+                                                  C.POINTER(C.c_size_t)]),
+    "cpk_mttkrp_f32": (
+        C.c_int,
+        [_P, C.c_int, C.POINTER(_I64), C.c_int, C.POINTER(_P), C.POINTER(_I64), _P, _I64, _P, _I64, C.c_int,
+         _P, C.c_size_t, _P],
+    ),
     "cpk_mttkrp_elem_f64": (
         C.c_int,
         [_P, C.c_int, C.POINTER(_I64), C.c_int, C.POINTER(_P), C.POINTER(_I64), _P, _I64, _P, _I64, _P],

@@ -186,6 +186,10 @@ def mttkrp_device(y_dev: torch.Tensor, dims, factors, mode: int, weights=None, p
     rank = next(int(f.shape[1]) for f in factors if f is not None)
     if plan is None:
         plan = MttkrpPlan(Variant.B200, mode)
+    if y_dev.dtype == torch.float32:
+        if landed is not None:
+            raise ParameterError("the float32 path has no streamed (landed) form")
+        return _mttkrp_device_f32(y_dev, dims, factors, mode, weights, plan, out)
     p = _gpu_plan(plan, dims, rank)
     req = _plan_request(plan)  # the C side resolves (and may merge) from the request
     dims_c = _lib.i64_array(dims)
@@ -195,8 +199,8 @@ def mttkrp_device(y_dev: torch.Tensor, dims, factors, mode: int, weights=None, p
     ws = workspace(dev, nbytes.value)
     if out is None:
         out = torch.empty((dims[mode], rank), dtype=torch.float64, device=dev)
-    ptrs = _lib.ptr_array([f.data_ptr() if m != mode else 0 for m, f in enumerate(factors)])
-    lds = _lib.i64_array([f.stride(0) for f in factors])
+    ptrs = _lib.ptr_array([f.data_ptr() if (m != mode and f is not None) else 0 for m, f in enumerate(factors)])
+    lds = _lib.i64_array([f.stride(0) if f is not None else rank for f in factors])
     lam_ptr = weights.data_ptr() if weights is not None else None
     timer = EventTimer(dev)
     args = (y_dev.data_ptr(), d, dims_c, mode, ptrs, lds, lam_ptr, rank, out.data_ptr(), out.stride(0),
@@ -207,6 +211,57 @@ def mttkrp_device(y_dev: torch.Tensor, dims, factors, mode: int, weights=None, p
         rc = lib.cpk_mttkrp_f64_landed(*args, int(landed[0]), int(landed[1]))
     timer.stop(dev)
     _lib.check(rc, "mttkrp")
+    return out, p, timer
+
+
+def f32_eligible(dims, factors=None) -> bool:
+    """Shapes the tcgen05 float32 kernel takes (TMA needs 16-byte strides:
+    I_0 % 4 == 0; factors are re-laid out with ld % 4 == 0 when needed)."""
+    return 2 <= len(dims) <= 5 and dims[0] % 4 == 0 and max(dims) < 2 ** 31
+
+
+def _ld4(f: torch.Tensor) -> torch.Tensor:
+    """f with a 16-byte aligned base and a leading dimension that is a
+    multiple of 4 floats (a padded copy only when f is not already so)."""
+    if f.stride(1) == 1 and f.stride(0) % 4 == 0 and f.data_ptr() % 16 == 0:
+        return f
+    r = f.shape[1]
+    buf = torch.zeros((f.shape[0], (r + 3) // 4 * 4), dtype=torch.float32, device=f.device)
+    buf[:, :r] = f
+    return buf[:, :r]
+
+
+def _mttkrp_device_f32(y_dev, dims, factors, mode, weights, plan, out):
+    """Optional float32 path (north star: <= 1e-4): cpk_mttkrp_f32, the
+    tcgen05 kind::tf32 kernel with a 3xTF32 split.  Shapes TMA cannot
+    describe run the FP64 kernel on float64 copies (still on the device)."""
+    d = len(dims)
+    dev = y_dev.device
+    fac = [None if m == mode else _ld4(f.to(device=dev, dtype=torch.float32)) for m, f in enumerate(factors)]
+    rank = next(int(f.shape[1]) for f in fac if f is not None)
+    lam = None if weights is None else weights.to(device=dev, dtype=torch.float32).contiguous()
+    if out is None:
+        out = torch.empty((dims[mode], rank), dtype=torch.float32, device=dev)
+    if not f32_eligible(dims, fac) or y_dev.data_ptr() % 16:
+        g64, p, timer = mttkrp_device(y_dev.double(), dims, [None if f is None else f.double() for f in fac], mode,
+                                      None if lam is None else lam.double(), replace(plan, engine="auto"))
+        out.copy_(g64)
+        return out, p, timer
+    splits = int(plan.splits or 0)
+    dims_c = _lib.i64_array(dims)
+    nbytes = _lib.C.c_size_t(0)
+    lib = _lib.load()
+    _lib.check(lib.cpk_mttkrp_f32_workspace_bytes(d, dims_c, mode, rank, splits, _lib.C.byref(nbytes)), "workspace")
+    ws = workspace(dev, nbytes.value, tag="mttkrp_f32")
+    ptrs = _lib.ptr_array([0 if f is None else f.data_ptr() for f in fac])
+    lds = _lib.i64_array([rank if f is None else f.stride(0) for f in fac])
+    timer = EventTimer(dev)
+    rc = lib.cpk_mttkrp_f32(y_dev.data_ptr(), d, dims_c, mode, ptrs, lds, None if lam is None else lam.data_ptr(),
+                            rank, out.data_ptr(), out.stride(0), splits, ws.data_ptr() if ws is not None else None,
+                            nbytes.value, stream_ptr(dev))
+    timer.stop(dev)
+    _lib.check(rc, "mttkrp f32")
+    p = _lib.CpkPlan(128, 128, 0, splits, 0, 32, -1, -1)  # engine -1: the fp32 tcgen05 kernel
     return out, p, timer
 
 
@@ -371,6 +426,15 @@ def mttkrp(tensor, factors, mode: int, weights=None, plan: MttkrpPlan | None = N
     matrices or a KruskalTensor (its weights are folded once).  Returns an
     (I_k, R) matrix of the input's kind (numpy for host, torch for CUDA).
     """
+    if isinstance(tensor, torch.Tensor) and tensor.is_cuda and tensor.dtype == torch.float32:
+        # optional float32 path: device in, device out (float32)
+        fs = list(factors.factors if isinstance(factors, KruskalTensor) else factors)
+        dims = tuple(int(f.shape[0]) for f in fs)
+        w = factors.weights if isinstance(factors, KruskalTensor) else weights
+        if w is not None and not isinstance(w, torch.Tensor):
+            w = torch.as_tensor(np.asarray(w), device=tensor.device)
+        return mttkrp_device(tensor.reshape(-1), dims, [torch.as_tensor(f, device=tensor.device) for f in fs],
+                             int(mode), w, plan)[0]
     if isinstance(factors, KruskalTensor):
         m = factors
     else:
