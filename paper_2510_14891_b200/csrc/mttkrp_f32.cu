@@ -9,19 +9,21 @@
 //
 //   warp 0 (one lane)  TMA: tensor tile, 32 rows of A_f, the o-rows -> raw
 //                      stage (2 stages)
-//   warp 1             TMEM allocation (2 x 128 columns: two fp32 accumulators);
+//   warp 1             TMEM allocation (two fp32 group accumulators + the
+//                      running sum, 384 of 512 columns);
 //                      one lane issues the UMMAs
-//   warps 2-5          transform: Y and Z into "3xTF32" operands, each value
+//   warps 2-9          transform: Y and Z into "3xTF32" operands, each value
 //                      v split as hi = rna_tf32(v), lo = rna_tf32(v - hi), in
 //                      the K-major SWIZZLE_128B layout UMMA reads (2 operand
 //                      stages)
-//   warps 6-9          drain: the tensor core's fp32 accumulation truncates,
+//   warps 10-17        drain: the tensor core's fp32 accumulation truncates,
 //                      a bias that grows with the number of accumulations
 //                      (1.1e-4 after ~4k MMAs into one accumulator), so the
 //                      MMAs of every F_GROUP chunks go to one of two TMEM
 //                      accumulators (ping-pong) and these warps add each
-//                      finished group into fp32 registers (round to nearest)
-//                      while the other accumulator fills; then the epilogue
+//                      finished group into a running sum kept in TMEM
+//                      (round-to-nearest fp32 adds) while the other
+//                      accumulator fills; then the epilogue
 //
 // Each chunk is 4 k-steps x {Yhi.Zhi, Yhi.Zlo, Ylo.Zhi} = 12
 // tcgen05.mma.cta_group::1.kind::tf32 (M = 128, N = 128, K = 8) into one fp32
@@ -43,8 +45,12 @@ namespace cpk {
 namespace {
 
 constexpr int F_BM = 128, F_BN = 128, F_BK = 32;  // rows, rank columns, chunk depth (128 B of fp32)
-constexpr int F_THREADS = 10 * 32;
+// warp 0 TMA, warp 1 MMA, warps 2-9 transform, warps 10-17 drain
+constexpr int F_XFORM_WARPS = 8, F_DRAIN_WARPS = 8;
+constexpr int F_THREADS = (2 + F_XFORM_WARPS + F_DRAIN_WARPS) * 32;
 constexpr int F_GROUP = 4;  // chunks (48 MMAs) per TMEM accumulator before a drain
+// TMEM columns: two group accumulators [0, 256) and the running sum [256, 384)
+constexpr int F_SUM_COL = 2 * F_BN, F_TMEM_COLS = 512;
 constexpr int F_RAW_STAGES = 2, F_OP_STAGES = 2;
 constexpr int F_TILE_BYTES = F_BM * F_BK * 4;  // 16 KB: one 128 x 32 fp32 operand tile
 static_assert(F_BM == F_BN, "A and B operand tiles share one size");
@@ -134,19 +140,39 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(su32(bar))
                : "memory");
 }
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+        "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};\n" ::"r"(
+          taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+      "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+      : "memory");
+}
 // float offset of (row r, k) in a K-major SW128 tile of 32-float rows
 __device__ __forceinline__ int swz(int r, int k4) { return r * 32 + (((k4 ^ (r & 7))) << 2); }
 
+// v = hi + lo with hi = v's top 11 significand bits (exactly a TF32) and
+// lo = v - hi exact in fp32; the tensor core truncates lo to TF32, an error
+// below 2^-21 |v|, and the dropped lo*lo term is below 2^-20 |y z|.
+__device__ __forceinline__ float tf32_hi(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
+
 __device__ __forceinline__ void split_store(float* hi_tile, float* lo_tile, int off, float4 v) {
   float4 h, l;
-  h.x = rna_tf32(v.x);
-  h.y = rna_tf32(v.y);
-  h.z = rna_tf32(v.z);
-  h.w = rna_tf32(v.w);
-  l.x = rna_tf32(v.x - h.x);
-  l.y = rna_tf32(v.y - h.y);
-  l.z = rna_tf32(v.z - h.z);
-  l.w = rna_tf32(v.w - h.w);
+  h.x = tf32_hi(v.x);
+  h.y = tf32_hi(v.y);
+  h.z = tf32_hi(v.z);
+  h.w = tf32_hi(v.w);
+  l.x = v.x - h.x;
+  l.y = v.y - h.y;
+  l.z = v.z - h.z;
+  l.w = v.w - h.w;
   *reinterpret_cast<float4*>(hi_tile + off) = h;
   *reinterpret_cast<float4*>(lo_tile + off) = l;
 }
@@ -173,19 +199,19 @@ __global__ void __launch_bounds__(F_THREADS, 1) mttkrp_f32_umma_sm100(const __gr
   if (threadIdx.x == 0) {
     for (int s = 0; s < 2; ++s) {
       bar_init(&raw_full[s], 1);
-      bar_init(&raw_empty[s], 4);
-      bar_init(&op_full[s], 4);
+      bar_init(&raw_empty[s], F_XFORM_WARPS);
+      bar_init(&op_full[s], F_XFORM_WARPS);
       bar_init(&op_empty[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
       bar_init(&acc_full[b], 1);
-      bar_init(&acc_empty[b], 4);
+      bar_init(&acc_empty[b], F_DRAIN_WARPS);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(su32(tslot)),
-                 "r"(2 * F_BN));
+                 "r"(F_TMEM_COLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
@@ -269,9 +295,11 @@ __global__ void __launch_bounds__(F_THREADS, 1) mttkrp_f32_umma_sm100(const __gr
         if (it % F_GROUP == F_GROUP - 1 || it == nst - 1) umma_commit(&acc_full[b]);
       }
     }
-  } else if (warp < 6) {
+  } else if (warp < 2 + F_XFORM_WARPS) {
     // ------------------------------------------------------------ transform
-    const int t = threadIdx.x - 64;  // 0..127: one operand row (m for Y, n for Z)
+    // 256 threads: operand row r = t % 128 (m for Y, n for Z), float4
+    // groups k4 in [4h, 4h + 4) with h = t / 128
+    const int t = threadIdx.x - 64, r = t & (F_BM - 1), k4_0 = (t >> 7) * 4;
     for (int it = 0; it < nst; ++it) {
       const int s = it & 1, o = it & 1;
       bar_wait(&raw_full[s], (it >> 1) & 1);
@@ -286,39 +314,39 @@ __global__ void __launch_bounds__(F_THREADS, 1) mttkrp_f32_umma_sm100(const __gr
       if constexpr (KMAJ) {
         // TMA already wrote Y K-major with the 128-B swizzle: split in place
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int off = (t + 128 * i) * 4;  // float4 chunk index * 4
+        for (int i = 0; i < 4; ++i) {
+          const int off = (t + 256 * i) * 4;  // float4 chunk index * 4
           split_store(a_hi, a_lo, off, *reinterpret_cast<const float4*>(ry + off));
         }
       } else {
         // Y landed M-major [32 k][128 m]: transpose row m = t into K-major
 #pragma unroll
-        for (int k4 = 0; k4 < 8; ++k4) {
+        for (int k4 = k4_0; k4 < k4_0 + 4; ++k4) {
           float4 v;
-          v.x = ry[(4 * k4 + 0) * F_BM + t];
-          v.y = ry[(4 * k4 + 1) * F_BM + t];
-          v.z = ry[(4 * k4 + 2) * F_BM + t];
-          v.w = ry[(4 * k4 + 3) * F_BM + t];
-          split_store(a_hi, a_lo, swz(t, k4), v);
+          v.x = ry[(4 * k4 + 0) * F_BM + r];
+          v.y = ry[(4 * k4 + 1) * F_BM + r];
+          v.z = ry[(4 * k4 + 2) * F_BM + r];
+          v.w = ry[(4 * k4 + 3) * F_BM + r];
+          split_store(a_hi, a_lo, swz(r, k4), v);
         }
       }
-      // Z^T row n = t: Z[k][n] = A_f[f0 + k][n] * prod_o A_o[o][n]
+      // Z^T row n = r: Z[k][n] = A_f[f0 + k][n] * prod_o A_o[o][n]
       const float* rf = reinterpret_cast<const float*>(st + C::RAW_F);
       float pr = 1.0f;
       if constexpr (NO > 0) {
         const float* rp = reinterpret_cast<const float*>(st + C::RAW_P);
-        pr = rp[t];
+        pr = rp[r];
 #pragma unroll
-        for (int i = 1; i < NO; ++i) pr *= rp[i * F_BN + t];
+        for (int i = 1; i < NO; ++i) pr *= rp[i * F_BN + r];
       }
 #pragma unroll
-      for (int k4 = 0; k4 < 8; ++k4) {
+      for (int k4 = k4_0; k4 < k4_0 + 4; ++k4) {
         float4 v;
-        v.x = rf[(4 * k4 + 0) * F_BN + t] * pr;
-        v.y = rf[(4 * k4 + 1) * F_BN + t] * pr;
-        v.z = rf[(4 * k4 + 2) * F_BN + t] * pr;
-        v.w = rf[(4 * k4 + 3) * F_BN + t] * pr;
-        split_store(b_hi, b_lo, swz(t, k4), v);
+        v.x = rf[(4 * k4 + 0) * F_BN + r] * pr;
+        v.y = rf[(4 * k4 + 1) * F_BN + r] * pr;
+        v.z = rf[(4 * k4 + 2) * F_BN + r] * pr;
+        v.w = rf[(4 * k4 + 3) * F_BN + r] * pr;
+        split_store(b_hi, b_lo, swz(r, k4), v);
       }
       asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // generic writes -> UMMA reads
       __syncwarp();
@@ -329,38 +357,48 @@ __global__ void __launch_bounds__(F_THREADS, 1) mttkrp_f32_umma_sm100(const __gr
     }
   } else {
     // ------------------------------------------------------------ drain + epilogue
-    const int quarter = warp & 3;  // TMEM lanes 32q..32q+31 are rows 32q..
-    float acc[F_BN];
-#pragma unroll
-    for (int j = 0; j < F_BN; ++j) acc[j] = 0.0f;
+    // two warps per TMEM lane quarter (rows 32q..32q+31), 64 columns each;
+    // the running sum lives in TMEM too (columns F_SUM_COL..), updated with
+    // round-to-nearest fp32 adds on the CUDA cores
+    constexpr int HALF = F_BN / 2;
+    const int quarter = warp & 3, c_base = ((warp - 2 - F_XFORM_WARPS) >> 2) * HALF;
+    const uint32_t lane_base = tmem + (uint32_t(quarter * 32) << 16);
     const int groups = (nst + F_GROUP - 1) / F_GROUP;
     for (int g = 0; g < groups; ++g) {
       const int b = g & 1;
       bar_wait(&acc_full[b], (g >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
 #pragma unroll
-      for (int c0 = 0; c0 < F_BN; c0 += 16) {
-        uint32_t v[16];
-        const uint32_t ta = tmem + (uint32_t(quarter * 32) << 16) + uint32_t(b * F_BN + c0);
-        asm volatile(
-            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
-            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-              "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
-            : "r"(ta));
+      for (int c0 = 0; c0 < HALF; c0 += 16) {
+        uint32_t v[16], w[16];
+        tmem_ld16(lane_base + uint32_t(b * F_BN + c_base + c0), v);
+        if (g > 0) tmem_ld16(lane_base + uint32_t(F_SUM_COL + c_base + c0), w);
         asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
 #pragma unroll
-        for (int jj = 0; jj < 16; ++jj) acc[c0 + jj] += __uint_as_float(v[jj]);
+        for (int jj = 0; jj < 16; ++jj)
+          w[jj] = g > 0 ? __float_as_uint(__uint_as_float(w[jj]) + __uint_as_float(v[jj])) : v[jj];
+        tmem_st16(lane_base + uint32_t(F_SUM_COL + c_base + c0), w);
       }
+      asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
       asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
       __syncwarp();
       if (lane == 0) bar_arrive(&acc_empty[b]);
     }
     const int n = n0 + quarter * 32 + lane;
-    if (n < p.Ik) {
-      float* dst = p.out + int64_t(blockIdx.z) * p.out_split_stride + int64_t(n) * p.ldo;
+    const int jb = j0 + c_base;
+#pragma unroll 1
+    for (int c0 = 0; c0 < HALF; c0 += 16) {
+      uint32_t w[16];
+      tmem_ld16(lane_base + uint32_t(F_SUM_COL + c_base + c0), w);
+      asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+      if (n < p.Ik) {
+        float* dst = p.out + int64_t(blockIdx.z) * p.out_split_stride + int64_t(n) * p.ldo + jb + c0;
 #pragma unroll
-      for (int j = 0; j < F_BN; ++j)
-        if (j0 + j < p.R) dst[j0 + j] = p.lam ? acc[j] * p.lam[j0 + j] : acc[j];
+        for (int jj = 0; jj < 16; ++jj) {
+          const int j = jb + c0 + jj;
+          if (j < p.R) dst[jj] = p.lam ? __uint_as_float(w[jj]) * p.lam[j] : __uint_as_float(w[jj]);
+        }
+      }
     }
   }
   // teardown: everyone done with TMEM before warp 1 frees it
@@ -368,7 +406,7 @@ __global__ void __launch_bounds__(F_THREADS, 1) mttkrp_f32_umma_sm100(const __gr
   __syncthreads();
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(2 * F_BN));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(F_TMEM_COLS));
   }
 }
 
