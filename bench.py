@@ -301,6 +301,34 @@ def run_b200(args):
             gemm = {"error": f"OOM: {exc}"[:200]}
         torch.cuda.empty_cache()
 
+    # ---- optional float32 path (north star: <= 1e-4): the tcgen05 3xTF32
+    # kernel on the same values rounded to fp32, checked against the FP64
+    # result of those values; not part of `value`
+    f32 = None
+    if args.f32_steps > 0 and world == 1:
+        try:
+            y32 = y.float()
+            f32s = [f.float() for f in fs]
+            y64r = y32.double()
+            f64r = [f.double() for f in f32s]
+            errs, ms = [], [[] for _ in range(3)]
+            for k in range(3):
+                g64, _, _ = mttkrp_device(y64r, local_dims, f64r, k)
+                for it in range(args.f32_steps + 1):
+                    g32, _, t = mttkrp_device(y32, local_dims, f32s, k)
+                    if it > 0:
+                        ms[k].append(t.seconds * 1e3)
+                errs.append(float(torch.linalg.norm(g32.double() - g64) / torch.linalg.norm(g64)))
+                del g64, g32
+            del y64r, f64r, y32
+            fm = [statistics.median(m) for m in ms]
+            f32 = {"impl": "tcgen05.mma kind::tf32, 3xTF32 split, TMEM accumulators (cpk_mttkrp_f32)",
+                   "per_mode_ms": fm, "gflops": algo_flops(local_dims, RANK) * 3 / (sum(fm) * 1e-3) / 1e9,
+                   "rel_frobenius_vs_fp64": errs, "tolerance": 1e-4}
+        except Exception as exc:  # report, do not lose the headline line
+            f32 = {"error": f"{type(exc).__name__}: {exc}"[:300]}
+        torch.cuda.empty_cache()
+
     # ---- e2e through the public API from pinned host buffers (N=1 only: the
     # per-rank host slab at N>1 is the same code path)
     e2e = None
@@ -413,6 +441,7 @@ def run_b200(args):
                          "north_star_frac": roof_t * 3 * args.steps / elapsed},
             "dfma_engine": dfma,
             "gemm_baseline": gemm,
+            "fp32_path": f32,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": 6 * args.steps,
@@ -491,6 +520,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--dfma-steps", type=int, default=2)
     ap.add_argument("--gemm-steps", type=int, default=2)
+    ap.add_argument("--f32-steps", type=int, default=2)
     ap.add_argument("--cpals-iters", type=int, default=10)
     ap.add_argument("--c5-iters", type=int, default=3)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
