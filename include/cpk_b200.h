@@ -87,6 +87,10 @@ typedef struct cpk_plan {
 /* TMA data movement (as CPK_ENGINE_TMA) with the FP64 math on mma.sync
  * m8n8k4 f64 (DMMA) instead of DFMA outer products; rank tiles 64/128/256. */
 #define CPK_ENGINE_DMMA 3
+/* cp.async data movement (any shape / alignment, as CPK_ENGINE_CPASYNC) with
+ * the DMMA consumers; rank tiles 64 (256 rows) and 128 (128 rows).  Picked
+ * where TMA cannot describe the tensor (odd I_0, misaligned factors). */
+#define CPK_ENGINE_CPDMMA 4
 
 /* Last error message of the calling thread (never NULL). */
 const char* cpk_last_error(void);

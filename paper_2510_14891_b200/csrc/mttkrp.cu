@@ -136,7 +136,52 @@ __device__ __forceinline__ void cp_chunk(double* dst, const double* src, int val
     cp_async8(dst, src, v * 8);
 }
 
-template <int BM, int BN, int BK, bool KMAJ, int VEC, int STAGES, int NO>
+// DMMA consumer for the cp.async tiles (256 threads = 8 warps of 32 x 64 warp
+// tiles, as the TMA kernel's, mttkrp_ws.cu): m8n8k4 fragments read from the
+// staged layouts, each 8-deep k block as two k-steps (even k, odd k).  TAIL:
+// the warp's columns straddle R; only its first nf_act 8-column fragments
+// issue DMMAs.
+template <bool KMAJ, bool TAIL, int BM, int BN, int BK, int APITCH>
+__device__ __forceinline__ void cp_dmma_stage(double (&acc)[4][8][2], const double* a_s, const double* b_s, int wm0,
+                                              int wn0, int lane, int nf_act) {
+  const int lr = lane >> 2, lk = lane & 3;
+#pragma unroll 2
+  for (int kk = 0; kk < BK; kk += 8) {
+    double a[4][2], b[8][2];
+#pragma unroll
+    for (int mf = 0; mf < 4; ++mf) {
+      const int m = wm0 + mf * 8 + lr;
+      if constexpr (KMAJ) {
+        const double2 v = *reinterpret_cast<const double2*>(a_s + m * APITCH + kk + 2 * lk);
+        a[mf][0] = v.x;
+        a[mf][1] = v.y;
+      } else {
+        a[mf][0] = a_s[(kk + 2 * lk) * BM + m];
+        a[mf][1] = a_s[(kk + 2 * lk + 1) * BM + m];
+      }
+    }
+    const double* brow = b_s + (kk + 2 * lk) * BN + wn0 + lr;
+#pragma unroll
+    for (int nf = 0; nf < 8; ++nf) {
+      if (TAIL && nf >= nf_act) break;
+      b[nf][0] = brow[nf * 8];
+      b[nf][1] = brow[BN + nf * 8];
+    }
+#pragma unroll
+    for (int ph = 0; ph < 2; ++ph)
+#pragma unroll
+      for (int mf = 0; mf < 4; ++mf)
+#pragma unroll
+        for (int nf = 0; nf < 8; ++nf) {
+          if (TAIL && nf >= nf_act) break;
+          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                       : "+d"(acc[mf][nf][0]), "+d"(acc[mf][nf][1])
+                       : "d"(a[mf][ph]), "d"(b[nf][ph]));
+        }
+  }
+}
+
+template <int BM, int BN, int BK, bool KMAJ, int VEC, int STAGES, int NO, bool DMMA = false>
 __global__ void __launch_bounds__((BM / 8) * (BN / 8), 1)
     mttkrp_f64_sm100(const __grid_constant__ MttkrpParams p) {
   using C = TileCfg<BM, BN, BK, KMAJ, VEC, STAGES, NO>;
@@ -200,11 +245,16 @@ __global__ void __launch_bounds__((BM / 8) * (BN / 8), 1)
     }
   };
 
-  double acc[8][8];
+  double acc[8][8];  // DFMA: 8 x 8 per thread; DMMA: [4 m-frags][8 n-frags][2]
 #pragma unroll
   for (int r = 0; r < 8; ++r)
 #pragma unroll
     for (int c = 0; c < 8; ++c) acc[r][c] = 0.0;
+  double(&dacc)[4][8][2] = *reinterpret_cast<double(*)[4][8][2]>(&acc);
+  static_assert(!DMMA || C::NT == 256, "DMMA tiles run 8 warps");
+  constexpr int DWARPS_N = BN / 64 > 0 ? BN / 64 : 1;
+  const int dwm0 = (warp / DWARPS_N) * 32, dwn0 = (warp % DWARPS_N) * 64;
+  const int dnf_act = int((p.R - j0 - dwn0 + 7) >> 3);
 
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {
@@ -254,6 +304,13 @@ __global__ void __launch_bounds__((BM / 8) * (BN / 8), 1)
 
     const double* a_s = As + buf * C::A_ELEMS;
     const double* b_s = Bs + buf * C::B_ELEMS;
+    if constexpr (DMMA) {
+      if (dnf_act >= 8)
+        cp_dmma_stage<KMAJ, false, BM, BN, BK, C::APITCH>(dacc, a_s, b_s, dwm0, dwn0, lane, 8);
+      else
+        cp_dmma_stage<KMAJ, true, BM, BN, BK, C::APITCH>(dacc, a_s, b_s, dwm0, dwn0, lane, dnf_act);
+      continue;
+    }
 #pragma unroll
     for (int kk = 0; kk < BK; kk += 2) {
       double a[8][2];
@@ -298,6 +355,31 @@ __global__ void __launch_bounds__((BM / 8) * (BN / 8), 1)
   // --- epilogue: partial (or final, lam-folded) tile -> out --------------
   double* out = p.out + int64_t(blockIdx.z + p.z0) * p.out_split_stride;
   const bool fold = p.lam != nullptr;
+  if constexpr (DMMA) {
+    const int lr = lane >> 2, lk = lane & 3;
+#pragma unroll
+    for (int mf = 0; mf < 4; ++mf) {
+      const int64_t n = n0 + dwm0 + mf * 8 + lr;
+      if (n >= p.Ik) continue;
+#pragma unroll
+      for (int nf = 0; nf < 8; ++nf) {
+        const int64_t j = j0 + dwn0 + nf * 8 + 2 * lk;
+        double v0 = dacc[mf][nf][0], v1 = dacc[mf][nf][1];
+        if (fold) {
+          if (j < p.R) v0 *= p.lam[j];
+          if (j + 1 < p.R) v1 *= p.lam[j + 1];
+        }
+        double* dst = out + n * p.ldo + j;
+        if (j + 1 < p.R && ((p.ldo & 1) == 0)) {
+          *reinterpret_cast<double2*>(dst) = make_double2(v0, v1);
+        } else {
+          if (j < p.R) dst[0] = v0;
+          if (j + 1 < p.R) dst[1] = v1;
+        }
+      }
+    }
+    return;
+  }
 #pragma unroll
   for (int r = 0; r < 8; ++r) {
     const int64_t n = n0 + 2 * ty + (r & 1) + 2 * C::TY * (r >> 1);
@@ -405,35 +487,44 @@ struct KernelInfo {
   int stages;
 };
 
-template <int BM, int BN, int BK, bool KMAJ, int VEC, int NO>
+template <int BM, int BN, int BK, bool KMAJ, int VEC, int NO, bool DMMA>
 static KernelInfo info() {
   using P = Pick<BM, BN, BK, KMAJ, VEC, NO>;
-  return {reinterpret_cast<const void*>(&mttkrp_f64_sm100<BM, BN, BK, KMAJ, VEC, P::stages, NO>), P::Cfg::SMEM,
+  return {reinterpret_cast<const void*>(&mttkrp_f64_sm100<BM, BN, BK, KMAJ, VEC, P::stages, NO, DMMA>), P::Cfg::SMEM,
           P::Cfg::NT, P::stages};
 }
 
-template <int BM, int BN, int BK, bool KMAJ, int VEC>
+template <int BM, int BN, int BK, bool KMAJ, int VEC, bool DMMA>
 static KernelInfo pick_no(int no) {
   switch (no) {
-    case 0: return info<BM, BN, BK, KMAJ, VEC, 0>();
-    case 1: return info<BM, BN, BK, KMAJ, VEC, 1>();
-    case 2: return info<BM, BN, BK, KMAJ, VEC, 2>();
-    case 3: return info<BM, BN, BK, KMAJ, VEC, 3>();
+    case 0: return info<BM, BN, BK, KMAJ, VEC, 0, DMMA>();
+    case 1: return info<BM, BN, BK, KMAJ, VEC, 1, DMMA>();
+    case 2: return info<BM, BN, BK, KMAJ, VEC, 2, DMMA>();
+    case 3: return info<BM, BN, BK, KMAJ, VEC, 3, DMMA>();
     default: return {nullptr, 0, 0, 0};
   }
 }
 
-template <int BM, int BN>
+template <int BM, int BN, bool DMMA = false>
 static KernelInfo pick_layout(int bk, bool kmaj, int vec, int no) {
   if (bk == 32) {
     if (vec != 2) return {nullptr, 0, 0, 0};
-    return kmaj ? pick_no<BM, BN, 32, true, 2>(no) : pick_no<BM, BN, 32, false, 2>(no);
+    return kmaj ? pick_no<BM, BN, 32, true, 2, DMMA>(no) : pick_no<BM, BN, 32, false, 2, DMMA>(no);
   }
-  if (kmaj) return vec == 2 ? pick_no<BM, BN, 16, true, 2>(no) : pick_no<BM, BN, 16, true, 1>(no);
-  return vec == 2 ? pick_no<BM, BN, 16, false, 2>(no) : pick_no<BM, BN, 16, false, 1>(no);
+  if (kmaj) return vec == 2 ? pick_no<BM, BN, 16, true, 2, DMMA>(no) : pick_no<BM, BN, 16, true, 1, DMMA>(no);
+  return vec == 2 ? pick_no<BM, BN, 16, false, 2, DMMA>(no) : pick_no<BM, BN, 16, false, 1, DMMA>(no);
 }
 
-static KernelInfo pick_kernel(int rank_tile, int bk, bool kmaj, int vec, int no) {
+// engine CPK_ENGINE_CPASYNC: DFMA tiles; CPK_ENGINE_CPDMMA: 8-warp DMMA tiles
+// (rank tile 64 -> 256 rows, 128 -> 128 rows, as the TMA DMMA kernel's)
+static KernelInfo pick_kernel(int rank_tile, int bk, bool kmaj, int vec, int no, bool dmma = false) {
+  if (dmma) {
+    switch (rank_tile) {
+      case 128: return pick_layout<128, 128, true>(bk, kmaj, vec, no);
+      case 64: return pick_layout<256, 64, true>(bk, kmaj, vec, no);
+      default: return {nullptr, 0, 0, 0};
+    }
+  }
   switch (rank_tile) {
     case 128: return pick_layout<128, 128>(bk, kmaj, vec, no);
     case 64: return pick_layout<128, 64>(bk, kmaj, vec, no);
@@ -442,7 +533,10 @@ static KernelInfo pick_kernel(int rank_tile, int bk, bool kmaj, int vec, int no)
   }
 }
 
-static int block_rows_for(int rank_tile) { return rank_tile == 32 ? 64 : 128; }
+static int block_rows_for(int rank_tile, bool dmma = false) {
+  if (dmma) return rank_tile == 64 ? 256 : 128;
+  return rank_tile == 32 ? 64 : 128;
+}
 
 static int device_sms(int* out) {
   static int cached = 0;
@@ -529,6 +623,7 @@ struct TileChoice {
 static const TileChoice kChoices[] = {
     {CPK_ENGINE_TMA, 256, 0.95}, {CPK_ENGINE_TMA, 128, 1.00}, {CPK_ENGINE_TMA, 64, 0.93},
     {CPK_ENGINE_DMMA, 256, 1.02}, {CPK_ENGINE_DMMA, 128, 1.19}, {CPK_ENGINE_DMMA, 64, 1.26},
+    {CPK_ENGINE_CPDMMA, 128, 0.97}, {CPK_ENGINE_CPDMMA, 64, 0.88},
     {CPK_ENGINE_CPASYNC, 128, 0.92}, {CPK_ENGINE_CPASYNC, 64, 0.78}, {CPK_ENGINE_CPASYNC, 32, 0.55},
 };
 
@@ -541,6 +636,13 @@ static int rows_for(int engine, int rank_tile, int* bm, int* bk_fixed) {
     *bk_fixed = bk;
     return CPK_OK;
   }
+  if (engine == CPK_ENGINE_CPDMMA) {
+    if (rank_tile != 64 && rank_tile != 128)
+      return fail(CPK_ERR_PARAM, "cp.async DMMA engine rank_tile must be 64 or 128 (got %d)", rank_tile);
+    *bm = block_rows_for(rank_tile, true);
+    *bk_fixed = 0;
+    return CPK_OK;
+  }
   if (rank_tile != 32 && rank_tile != 64 && rank_tile != 128)
     return fail(CPK_ERR_PARAM, "cp.async engine rank_tile must be 32, 64 or 128 (got %d)", rank_tile);
   *bm = block_rows_for(rank_tile);
@@ -549,8 +651,8 @@ static int rows_for(int engine, int rank_tile, int* bm, int* bk_fixed) {
 }
 
 static int resolve(const Problem& pr, cpk_plan* plan) {
-  if (plan->engine < CPK_ENGINE_AUTO || plan->engine > CPK_ENGINE_DMMA)
-    return fail(CPK_ERR_PARAM, "engine must be 0 (auto), 1 (cp.async), 2 (TMA) or 3 (TMA + DMMA)");
+  if (plan->engine < CPK_ENGINE_AUTO || plan->engine > CPK_ENGINE_CPDMMA)
+    return fail(CPK_ERR_PARAM, "engine must be 0 (auto), 1 (cp.async), 2 (TMA), 3 (TMA + DMMA) or 4 (cp.async + DMMA)");
   const bool tma_ok = tma_possible(pr);
   if (plan->engine == CPK_ENGINE_AUTO || plan->rank_tile == 0) {
     // (engine, rank tile) minimizing padded rows x padded columns / rate
@@ -627,8 +729,9 @@ static int resolve(const Problem& pr, cpk_plan* plan) {
     } else {
       const int64_t tiles = ceil_div(pr.Ik, bm) * ceil_div(pr.R, plan->rank_tile);
       int per_sm = 1;  // the TMA kernels take one CTA per SM
-      if (plan->engine == CPK_ENGINE_CPASYNC) {
-        KernelInfo ki = pick_kernel(plan->rank_tile, plan->block_k, pr.k != 0, 2, std::min(pr.n_o, 3));
+      if (plan->engine == CPK_ENGINE_CPASYNC || plan->engine == CPK_ENGINE_CPDMMA) {
+        KernelInfo ki = pick_kernel(plan->rank_tile, plan->block_k, pr.k != 0, 2, std::min(pr.n_o, 3),
+                                    plan->engine == CPK_ENGINE_CPDMMA);
         per_sm = ki.fn ? ctas_per_sm(ki) : 1;
       }
       const double ldw = double((pr.R + 1) & ~int64_t(1));
@@ -972,9 +1075,11 @@ static int mttkrp_impl(const double* y, int d, const int64_t* dims, int mode, co
     if (plan_in && is_tma(plan_in->engine))
       return fail(CPK_ERR_PARAM, "TMA engine needs even leading dimensions and 16-byte aligned bases");
     // auto plan, misaligned buffers: same splits (same workspace) on cp.async
-    plan.engine = CPK_ENGINE_CPASYNC;
+    // (the DMMA tiles where the rank tile has one)
+    const bool cpd = plan.engine == CPK_ENGINE_DMMA && (plan.rank_tile == 64 || plan.rank_tile == 128);
+    plan.engine = cpd ? CPK_ENGINE_CPDMMA : CPK_ENGINE_CPASYNC;
     plan.rank_tile = std::min(plan.rank_tile, 128);
-    plan.block_rows = block_rows_for(plan.rank_tile);
+    plan.block_rows = block_rows_for(plan.rank_tile, cpd);
     plan.block_k = 16;
   }
   {
@@ -991,7 +1096,7 @@ static int mttkrp_impl(const double* y, int d, const int64_t* dims, int mode, co
     p.ldo = ldo;
     p.out_split_stride = out_split_stride;
     p.lam = lam_fold;
-    KernelInfo ki = pick_kernel(plan.rank_tile, bk, pr.k != 0, vec2 ? 2 : 1, pr.n_o);
+    KernelInfo ki = pick_kernel(plan.rank_tile, bk, pr.k != 0, vec2 ? 2 : 1, pr.n_o, plan.engine == CPK_ENGINE_CPDMMA);
     if (!ki.fn) return fail(CPK_ERR_PARAM, "no kernel for rank_tile %d", plan.rank_tile);
     if (cudaFuncSetAttribute(ki.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ki.smem)) != cudaSuccess)
       return check_launch("cudaFuncSetAttribute");

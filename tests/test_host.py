@@ -57,7 +57,7 @@ def test_rank_tile_heuristic_mirrors_the_c_planner(rows, rank):
         eng, rt = heuristic_rank_tile(r, dims[0], tma=tma)
         p = _lib.CpkPlan(0, 0, 0, 0, 148, 0, 0)
         _lib.check(_lib.load().cpk_plan_resolve(len(dims), _lib.i64_array(dims), 0, r, p))
-        assert (p.rank_tile, p.engine) == (rt, {"tma": 2, "cpasync": 1, "dmma": 3}[eng]), (dims, r)
+        assert (p.rank_tile, p.engine) == (rt, {"tma": 2, "cpasync": 1, "dmma": 3, "cpdmma": 4}[eng]), (dims, r)
 
 
 def test_plan_for_mode_clamps_tile_volume():

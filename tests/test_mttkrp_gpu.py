@@ -327,3 +327,22 @@ def test_small_modes_merge_with_a_neighbour(dims):
         for lo, hi in zip(cuts[:-1], cuts[1:]):
             mttkrp_device(yd, dims, fd, k, lamd, out=out, landed=(lo, hi))
         assert torch.equal(out, whole), (dims, k)
+
+
+@pytest.mark.parametrize("rank_tile", [64, 128])
+@pytest.mark.parametrize("dims", [(41, 36, 34), (131, 66, 3), (33, 40, 70, 7), (7, 5, 8, 9, 3), (65, 3)])
+def test_cpasync_dmma_engine_parity(dims, rank_tile):
+    """cp.async + DMMA tiles (engine "cpdmma", the path for tensors TMA
+    cannot describe, e.g. odd I_0): ragged shapes, rank tails, splits."""
+    for rank in (2, 67, 300):
+        y = rng_for(sum(dims) * rank + 1).random(int(np.prod(dims)))
+        fs = [rng_for(rank + 11 * j).random((n, rank)) for j, n in enumerate(dims)]
+        lam = rng_for(12).random(rank) + 0.5
+        m = ck.KruskalTensor(lam, fs)
+        t = ck.DenseTensor(dims, y)
+        for k in range(len(dims)):
+            ref = oracle.mttkrp_ref(y, dims, k, fs, lam)
+            for splits in (0, 1, 5):
+                plan = MttkrpPlan(Variant.B200, k, rank_tile=rank_tile, splits=splits, engine="cpdmma")
+                got = ck.run(t, m, plan).matrix
+                assert oracle.rel_err(got, ref) <= TOL, (dims, rank, k, splits)
