@@ -136,7 +136,7 @@ def run_reference(args):
     rank, world, _ = env_rank()
     if rank != 0:
         return
-    budget = max(2.0, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
+    budget = args.ref_seconds or max(2.0, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
     for _ in range(args.warmup):
         cpu_sample(budget / 4)
     vals, secs = [], []
@@ -525,6 +525,7 @@ def main():
     ap.add_argument("--c5-iters", type=int, default=3)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--ref-seconds", type=float, default=0.0, help="reference arm: CPU seconds per step (0 = auto)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "b200":
         print("warning: fewer than 3 warm-up steps", file=sys.stderr)
