@@ -60,7 +60,7 @@ def _is_torch(x) -> bool:
 class DenseTensor:
     """Dense tensor backed by one flat float64 buffer in first-mode-fastest order."""
 
-    __slots__ = ("dims", "data", "_dev")
+    __slots__ = ("dims", "data", "_dev", "_landing")
 
     def __init__(self, dims, data, copy=False):
         self.dims = check_dims(dims)
@@ -82,6 +82,7 @@ class DenseTensor:
             raise ShapeError(f"data has {size} elements, shape {self.dims} needs {n}")
         self.data = arr
         self._dev = arr if (_is_torch(arr) and arr.is_cuda) else None
+        self._landing = None  # (slab bounds, copy events) while a streamed upload is in flight
 
     @classmethod
     def zeros(cls, dims) -> "DenseTensor":
@@ -126,10 +127,16 @@ class DenseTensor:
     def is_device(self) -> bool:
         return _is_torch(self.data) and self.data.is_cuda
 
-    def device_data(self, device=None) -> torch.Tensor:
-        """The flat float64 payload on the CUDA device (cached H2D copy)."""
+    def device_data(self, device=None, wait: bool = True) -> torch.Tensor:
+        """The flat float64 payload on the CUDA device (cached H2D copy).
+
+        While a streamed upload is in flight the current stream is made to
+        wait for it (``wait=False``: the caller orders itself on the slab
+        events)."""
         dev = require_cuda(device)
         if self._dev is not None and self._dev.device == dev:
+            if wait and self.landing is not None:
+                torch.cuda.current_stream(dev).wait_event(self._landing[1][-1])
             return self._dev
         if _is_torch(self.data):
             t = self.data.to(dev, non_blocking=False)
@@ -151,9 +158,19 @@ class DenseTensor:
             return self.data.reshape(-1)
         return torch.from_numpy(np.ascontiguousarray(self.data).reshape(-1))
 
-    def cache_device(self, t: torch.Tensor) -> None:
-        """Adopt `t` (flat float64 CUDA, same contents) as the device copy."""
+    def cache_device(self, t: torch.Tensor, landing=None) -> None:
+        """Adopt `t` (flat float64 CUDA, same contents) as the device copy;
+        `landing` = (slab bounds along the slowest mode, copy events) while
+        the copy is still in flight."""
         self._dev = t
+        self._landing = landing
+
+    @property
+    def landing(self):
+        """(bounds, events) of an upload still in flight, else None."""
+        if self._landing is not None and self._landing[1][-1].query():
+            self._landing = None  # every slab has landed
+        return self._landing
 
     def to_ndarray(self) -> np.ndarray:
         """The data as a numpy array with axis 0 fastest (host copy if on device)."""

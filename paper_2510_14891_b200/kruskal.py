@@ -85,11 +85,13 @@ class KruskalTensor:
         dev = require_cuda(device)
         if self._dev is None or self._dev[0] != dev:
             fs = [_to_device(a, dev) for a in self.factors]
-            self._dev = (dev, fs, _to_device(self.weights, dev))
+            self._dev = [dev, fs, None]  # weights copied on first use only
         return self._dev[1]
 
     def device_weights(self, device=None):
         self.device_factors(device)
+        if self._dev[2] is None:
+            self._dev[2] = _to_device(self.weights, self._dev[0])
         return self._dev[2]
 
     def hadamard_gram(self, skip=None):

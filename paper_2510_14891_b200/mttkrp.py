@@ -171,7 +171,7 @@ def resolve_plan(plan: MttkrpPlan, dims, rank: int) -> dict:
 
 
 def mttkrp_device(y_dev: torch.Tensor, dims, factors, mode: int, weights=None, plan: MttkrpPlan | None = None,
-                  out: torch.Tensor | None = None, landed=None):
+                  out: torch.Tensor | None = None, landed=None, workspace_buf: torch.Tensor | None = None):
     """Low-level device entry: y_dev flat CUDA float64, factors CUDA (I_m, R).
 
     ``landed = (lo, hi)`` runs only the work whose slices along the slowest
@@ -196,7 +196,12 @@ def mttkrp_device(y_dev: torch.Tensor, dims, factors, mode: int, weights=None, p
     nbytes = _lib.C.c_size_t(0)
     lib = _lib.load()
     _lib.check(lib.cpk_mttkrp_workspace_bytes(d, dims_c, mode, rank, req, _lib.C.byref(nbytes)), "workspace")
-    ws = workspace(dev, nbytes.value)
+    if workspace_buf is not None:
+        if workspace_buf.numel() * workspace_buf.element_size() < nbytes.value:
+            raise ParameterError("workspace_buf is smaller than the plan's split-K workspace")
+        ws = workspace_buf if nbytes.value else None
+    else:
+        ws = workspace(dev, nbytes.value)
     if out is None:
         out = torch.empty((dims[mode], rank), dtype=torch.float64, device=dev)
     ptrs = _lib.ptr_array([f.data_ptr() if (m != mode and f is not None) else 0 for m, f in enumerate(factors)])
@@ -266,8 +271,11 @@ def _mttkrp_device_f32(y_dev, dims, factors, mode, weights, plan, out):
 
 
 def _unit_weights(w) -> bool:
+    """True for all-ones weights (then none are passed to the kernel).  A
+    CUDA tensor is never inspected (that would sync the stream): it is
+    folded, which is exact for ones as well."""
     if isinstance(w, torch.Tensor):
-        return bool((w == 1).all().item())
+        return (not w.is_cuda) and bool((w == 1).all().item())
     return bool(np.all(np.asarray(w) == 1.0))
 
 
@@ -283,6 +291,10 @@ def _run_gpu(y: DenseTensor, m: KruskalTensor, plan: MttkrpPlan):
     lam = None if _unit_weights(m.weights) else m.device_weights(dev)
     if y.needs_upload(dev) and y.size * 8 >= STREAM_MIN_BYTES and y.ndim >= 2 and y.dims[-1] >= 2:
         g, p, timer = _mttkrp_streamed(y, fac, plan, lam, dev)
+    elif y.landing is not None:
+        # the upload may still be in flight: run on the slabs as they land
+        # (a side stream, so this call overlaps the earlier ones)
+        g, p, timer = _landed_pieces(y.device_data(dev, wait=False), y.dims, fac, plan, lam, dev, *y.landing)
     else:
         g, p, timer = mttkrp_device(y.device_data(dev), y.dims, fac, plan.mode, lam, plan)
     host = not isinstance(y.data, torch.Tensor)
@@ -290,22 +302,71 @@ def _run_gpu(y: DenseTensor, m: KruskalTensor, plan: MttkrpPlan):
     return matrix, p, timer
 
 
-def _mttkrp_streamed(y: DenseTensor, fac, plan: MttkrpPlan, lam, dev):
-    """First touch of a large host tensor: copy it to the device in slabs
-    along its slowest mode on a side stream while, on the current stream,
-    the MTTKRP work items whose slices have landed run
-    (cpk_mttkrp_f64_landed).  Same plan, work items and split-K merge as a
-    call on the resident tensor, so G is bit-identical to it.  The device
-    copy is cached on `y` for later modes (DenseTensor.device_data)."""
-    dims, mode = y.dims, plan.mode
+_side = {}
+_copy = {}
+
+
+def _modes_stream(dev) -> torch.cuda.Stream:
+    if ("modes", dev.index) not in _copy:
+        _copy[("modes", dev.index)] = torch.cuda.Stream(dev)
+    return _copy[("modes", dev.index)]
+
+
+def _copy_stream(dev) -> torch.cuda.Stream:
+    if dev.index not in _copy:
+        _copy[dev.index] = torch.cuda.Stream(dev)
+    return _copy[dev.index]
+
+
+def _side_stream(dev) -> torch.cuda.Stream:
+    """Round-robin pool of side streams for calls that run on landing slabs."""
+    pool, nxt = _side.setdefault(dev.index, ([torch.cuda.Stream(dev) for _ in range(3)], [0]))
+    s = pool[nxt[0] % len(pool)]
+    nxt[0] += 1
+    return s
+
+
+def _landed_pieces(y_dev, dims, fac, plan, lam, dev, bounds, events):
+    """One MTTKRP as per-slab pieces (cpk_mttkrp_f64_landed), each after its
+    slab's copy event, on a side stream with a private workspace: calls on
+    the same in-flight tensor (the modes of one step) overlap each other and
+    the copy.  Same plan, work items and merge order as one resident call,
+    so G is bit-identical to it."""
+    main = torch.cuda.current_stream(dev)
+    side = _side_stream(dev)
+    side.wait_stream(main)  # inputs (factors, weights) are ordered on `main`
+    mode = plan.mode
+    rank = next(int(f.shape[1]) for f in fac if f is not None)
+    nbytes = _lib.C.c_size_t(0)
+    _lib.check(_lib.load().cpk_mttkrp_workspace_bytes(len(dims), _lib.i64_array(dims), mode, rank,
+                                                       _plan_request(plan), _lib.C.byref(nbytes)), "workspace")
+    with torch.cuda.stream(side):
+        out = torch.empty((dims[mode], rank), dtype=torch.float64, device=dev)
+        ws = torch.empty(max(1, (nbytes.value + 7) // 8), dtype=torch.float64, device=dev)
+        timer = EventTimer(dev)
+        p = None
+        for (lo, hi), ev in zip(bounds, events):
+            side.wait_event(ev)
+            _, p, _ = mttkrp_device(y_dev, dims, fac, mode, lam, plan, out=out, landed=(lo, hi), workspace_buf=ws)
+        timer.stop(dev)
+    main.wait_stream(side)
+    out.record_stream(main)
+    return out, p, timer
+
+
+def _start_upload(y: DenseTensor, dev):
+    """Begin the slab-wise H2D copy of a host tensor on a copy stream; the
+    device copy is cached on `y` with the slab events (DenseTensor.landing)."""
+    dims = y.dims
     per_slice = num_elements(dims[:-1])
     host = y.host_view()
-    y_dev = torch.empty(y.size, dtype=torch.float64, device=dev)
-    rank = next(int(f.shape[1]) for f in fac if f is not None)
-    out = torch.empty((dims[mode], rank), dtype=torch.float64, device=dev)
     compute = torch.cuda.current_stream(dev)
-    copy = torch.cuda.Stream(dev)
-    copy.wait_stream(compute)  # y_dev's allocation is ordered on `compute`
+    copy = _copy_stream(dev)
+    with torch.cuda.stream(copy):
+        # allocated on the copy stream: the copy need not wait for the
+        # compute stream's queue (only its own stream's earlier users)
+        y_dev = torch.empty(y.size, dtype=torch.float64, device=dev)
+    y_dev.record_stream(compute)
     n = min(STREAM_SLABS, dims[-1])
     bounds = [(dims[-1] * i // n, dims[-1] * (i + 1) // n) for i in range(n)]
     landed = []
@@ -315,15 +376,81 @@ def _mttkrp_streamed(y: DenseTensor, fac, plan: MttkrpPlan, lam, dev):
             ev = torch.cuda.Event()
             ev.record(copy)
             landed.append(ev)
-    timer = EventTimer(dev)
-    p = None
-    for (lo, hi), ev in zip(bounds, landed):
-        compute.wait_event(ev)
-        _, p, _ = mttkrp_device(y_dev, dims, fac, mode, lam, plan, out=out, landed=(lo, hi))
-    timer.stop(dev)
     y_dev.record_stream(copy)
-    y.cache_device(y_dev)
-    return out, p, timer
+    y.cache_device(y_dev, landing=(bounds, landed))
+    return y_dev, bounds, landed
+
+
+def mttkrp_modes(tensor, factors, modes=None, weights=None, plan: MttkrpPlan | None = None) -> list:
+    """The MTTKRPs of several modes against the same factors (e.g. every mode
+    of a step), returned as a list of (I_k, R) matrices of the input's kind.
+
+    For a large host tensor this is where streaming pays most: the copy runs
+    in slabs along the slowest mode and, for every landed slab, the work
+    items of *all* requested modes are issued in slab order on one stream
+    (cpk_mttkrp_f64_landed), so the copy hides under the compute of every
+    mode, not just the first.  Each mode keeps its own plan, workspace and
+    merge order: results are bit-identical to one resident call per mode.
+    """
+    if isinstance(factors, KruskalTensor):
+        m = factors
+    else:
+        fs = list(factors)
+        m = KruskalTensor(weights if weights is not None else np.ones(int(fs[0].shape[1])), fs, validate=False)
+    if not isinstance(tensor, DenseTensor):
+        tensor = DenseTensor(m.dims, tensor)
+    y = tensor
+    modes = list(range(y.ndim)) if modes is None else [int(k) for k in modes]
+    for k in modes:
+        _check_inputs(y, m, k)
+    dev = require_cuda()
+    stream_it = y.needs_upload(dev) and y.size * 8 >= STREAM_MIN_BYTES and y.ndim >= 2 and y.dims[-1] >= 2
+    if not stream_it and y.landing is None:
+        return [mttkrp(y, m, k, plan=plan) for k in modes]
+    fac = m.device_factors(dev)
+    lam = None if _unit_weights(m.weights) else m.device_weights(dev)
+    if stream_it:
+        y_dev, bounds, events = _start_upload(y, dev)
+    else:
+        y_dev, (bounds, events) = y.device_data(dev, wait=False), y.landing
+    dims, rank = y.dims, m.rank
+    plans = [replace(plan, mode=k) if plan is not None else MttkrpPlan(Variant.B200, k) for k in modes]
+    # The pieces run on a side stream, never on the legacy default stream:
+    # waits on the copy events issued there resolved only after the whole
+    # copy once the default stream had done any H2D (measured,
+    # tools/dbg_copy2.py), which serialized copy and compute.
+    main = torch.cuda.current_stream(dev)
+    side = _modes_stream(dev)  # one stream: its allocator pool is reused call after call
+    side.wait_stream(main)  # inputs are ordered on `main`
+    outs = []
+    with torch.cuda.stream(side):
+        wss = []
+        for pk in plans:
+            nbytes = _lib.C.c_size_t(0)
+            _lib.check(_lib.load().cpk_mttkrp_workspace_bytes(len(dims), _lib.i64_array(dims), pk.mode, rank,
+                                                               _plan_request(pk), _lib.C.byref(nbytes)), "workspace")
+            outs.append(torch.empty((dims[pk.mode], rank), dtype=torch.float64, device=dev))
+            wss.append(torch.empty(max(1, (nbytes.value + 7) // 8), dtype=torch.float64, device=dev))
+        for (lo, hi), ev in zip(bounds, events):
+            side.wait_event(ev)
+            for pk, out, ws in zip(plans, outs, wss):
+                mttkrp_device(y_dev, dims, fac, pk.mode, lam, pk, out=out, landed=(lo, hi), workspace_buf=ws)
+    main.wait_stream(side)
+    for out in outs:
+        out.record_stream(main)
+    host = not isinstance(y.data, torch.Tensor)
+    return [np.ascontiguousarray(g.cpu().numpy()) for g in outs] if host else outs
+
+
+def _mttkrp_streamed(y: DenseTensor, fac, plan: MttkrpPlan, lam, dev):
+    """First touch of a large host tensor: copy it to the device in slabs
+    along its slowest mode on a copy stream while the MTTKRP work items whose
+    slices have landed run (_landed_pieces).  The device copy is cached on
+    `y` together with the slab events, so the next calls (the other modes of
+    the same step) also start on landed slabs instead of waiting for the
+    whole copy."""
+    y_dev, bounds, landed = _start_upload(y, dev)
+    return _landed_pieces(y_dev, y.dims, fac, plan, lam, dev, bounds, landed)
 
 
 def _stats(variant, y, m, plan, p, timer, *, element_visits, atomic_updates, tile_volume=None, unroll=None,
@@ -440,9 +567,9 @@ def mttkrp(tensor, factors, mode: int, weights=None, plan: MttkrpPlan | None = N
     else:
         fs = list(factors)
         r = int(fs[0].shape[1])
-        w = weights if weights is not None else (
-            torch.ones(r, dtype=torch.float64, device=fs[0].device) if isinstance(fs[0], torch.Tensor)
-            else np.ones(r))
+        # unit weights stay on the host: checking device weights for == 1
+        # would cost a stream sync per call
+        w = weights if weights is not None else np.ones(r)
         m = KruskalTensor(w, fs, validate=False)
     if not isinstance(tensor, DenseTensor):
         tensor = DenseTensor(m.dims, tensor)
