@@ -3,6 +3,11 @@ from pathlib import Path
 import numpy as np, torch
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 import paper_2510_14891_b200 as ck
+import importlib
+_mt = importlib.import_module("paper_2510_14891_b200.mttkrp")
+for a in sys.argv:
+    if a.startswith("--slabs="):
+        _mt.STREAM_SLABS = int(a.split("=")[1])
 from oracle import gen
 dims, R = (1024, 1024, 1024), 2000
 dev = torch.device("cuda", 0)
