@@ -430,7 +430,12 @@ def run_b200(args):
                        "l2": "inputs 8 GiB >> 126 MB L2; no flush needed"},
             "per_mode_ms": per_mode,
             "paper_gflops": int(np.prod(DIMS)) * RANK * 3 * 3 * args.steps / elapsed / 1024 ** 3,
-            "roofline": {"bound": "fp64", "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "TFLOP/s",
+            # bound "tensor": the DMMA kernel is bound by the tensor pipe's
+            # FP64 (DMMA) subpipe (ncu sm__inst_executed_pipe_tensor_subpipe_dmma
+            # ~96 %); its peak is the FP64 one, measured live -- not the bf16
+            # peak of MEASURED_PEAKS.json
+            "roofline": {"bound": "tensor", "pipe": "fp64 (DMMA = DFMA datapath)",
+                         "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "TFLOP/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "peak_source": "cpk_fp64_peak_probe (max of register DFMA and DMMA loops, this run)"
                          if fp64_peak else "nominal 148 SM x 64 FP64 FMA/clk x 2 x 1.965 GHz",
@@ -474,7 +479,11 @@ def bench_cpals(ck, dev, iters):
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
         if graph is None:  # the API default (eager below GRAPH_MIN_ITERS sweeps)
-            res.update({"sec_per_iter": dt / iters,
+            from paper_2510_14891_b200.perfmodel import roofline_seconds
+
+            roof = 4 * roofline_seconds(dims, 256)  # the sweep's 4 MTTKRPs at the north-star roofline
+            res.update({"sec_per_iter": dt / iters, "roofline_sec_per_iter": roof,
+                        "roofline_frac": roof / (dt / iters),
                         "mttkrp_sec_per_iter": statistics.median(sum(s) for s in tr.mttkrp_seconds),
                         "other_sec_per_iter": statistics.median(tr.other_seconds), "fit_last": tr.fits[-1]})
         else:  # forced capture: sweeps 2.. are one CUDA-graph replay each
@@ -508,8 +517,13 @@ def bench_c5(dev, iters):
         sec, mt = (float(v) for v in t.tolist())
     del y
     flops = 3 * 2 * 4096 * 2048 * 2048 * r * 2
+    from paper_2510_14891_b200.perfmodel import roofline_seconds
+
+    # the sweep's 3 MTTKRPs of the whole tensor at the roofline of this many GPUs
+    roof = 3 * roofline_seconds(dims, r) / comm.world
     return {"config": "c5: 3-way 4096x2048x2048 f64, rank 512, mode-0 block partition", "gpus": comm.world,
-            "iters": iters, "sec_per_iter": sec, "mttkrp_sec_per_iter": mt,
+            "iters": iters, "sec_per_iter": sec, "roofline_sec_per_iter": roof, "roofline_frac": roof / sec,
+            "mttkrp_sec_per_iter": mt,
             "mttkrp_gflops": flops / mt / 1e9, "comm_seconds_total": comm.seconds,
             "comm_bytes_total": comm.bytes, "fits": tr.fits}
 
