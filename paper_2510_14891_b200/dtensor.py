@@ -60,7 +60,7 @@ def _is_torch(x) -> bool:
 class DenseTensor:
     """Dense tensor backed by one flat float64 buffer in first-mode-fastest order."""
 
-    __slots__ = ("dims", "data", "_dev", "_landing")
+    __slots__ = ("dims", "data", "_dev", "_landing", "_even")
 
     def __init__(self, dims, data, copy=False):
         self.dims = check_dims(dims)
@@ -83,6 +83,7 @@ class DenseTensor:
         self.data = arr
         self._dev = arr if (_is_torch(arr) and arr.is_cuda) else None
         self._landing = None  # (slab bounds, copy events) while a streamed upload is in flight
+        self._even = None  # zero-padded copy with an even first extent (even_device_data)
 
     @classmethod
     def zeros(cls, dims) -> "DenseTensor":
@@ -171,6 +172,22 @@ class DenseTensor:
         if self._landing is not None and self._landing[1][-1].query():
             self._landing = None  # every slab has landed
         return self._landing
+
+    def even_device_data(self, device=None) -> torch.Tensor:
+        """A device copy with I_0 padded to I_0 + 1 by a zero slice (cached).
+
+        The TMA kernels need 16-byte strides, i.e. an even I_0.  Zero
+        elements contribute nothing to any MTTKRP, so the padded tensor
+        gives the same G for every mode k > 0, and G's first I_0 rows for
+        k = 0, with A_0 extended by any one row."""
+        dev = require_cuda(device)
+        if self._even is None or self._even.device != dev:
+            i0 = self.dims[0]
+            src = self.device_data(dev).view(-1, i0)
+            pad = torch.zeros((src.shape[0], i0 + 1), dtype=torch.float64, device=dev)
+            pad[:, :i0] = src
+            self._even = pad.view(-1)
+        return self._even
 
     def to_ndarray(self) -> np.ndarray:
         """The data as a numpy array with axis 0 fastest (host copy if on device)."""

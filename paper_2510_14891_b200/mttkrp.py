@@ -295,11 +295,41 @@ def _run_gpu(y: DenseTensor, m: KruskalTensor, plan: MttkrpPlan):
         # the upload may still be in flight: run on the slabs as they land
         # (a side stream, so this call overlaps the earlier ones)
         g, p, timer = _landed_pieces(y.device_data(dev, wait=False), y.dims, fac, plan, lam, dev, *y.landing)
+    elif _pad_first_mode(y, plan, dev):
+        g, p, timer = _mttkrp_even(y, fac, plan, lam, dev)
     else:
         g, p, timer = mttkrp_device(y.device_data(dev), y.dims, fac, plan.mode, lam, plan)
     host = not isinstance(y.data, torch.Tensor)
     matrix = np.ascontiguousarray(g.cpu().numpy()) if host else g
     return matrix, p, timer
+
+
+# An odd I_0 rules out TMA (16-byte strides); tensors up to this size are
+# run through a zero-padded copy with an even I_0 instead (DenseTensor.
+# even_device_data): the TMA + DMMA kernel on the copy beats the cp.async
+# kernel on the original by ~40 % (c4-sized, profiles/r01_sweep_odd_cpdmma.agg.csv).
+EVEN_PAD_MAX_BYTES = 16 << 30
+
+
+def _pad_first_mode(y: DenseTensor, plan: MttkrpPlan, dev) -> bool:
+    if y.ndim < 2 or y.dims[0] % 2 == 0 or Variant(plan.variant) not in (Variant.B200, Variant.GEMM,
+                                                                          Variant.FULL_KRP, Variant.ELEM):
+        return False
+    if plan.engine not in ("auto", "dmma") or plan.rank_tile or plan.splits or plan.block_k:
+        return False
+    nbytes = 8 * (y.size // y.dims[0]) * (y.dims[0] + 1)
+    return nbytes <= min(EVEN_PAD_MAX_BYTES, torch.cuda.mem_get_info(dev)[0] // 4)
+
+
+def _mttkrp_even(y: DenseTensor, fac, plan: MttkrpPlan, lam, dev):
+    """MTTKRP through the zero-padded even copy (see _pad_first_mode)."""
+    dims = (y.dims[0] + 1,) + y.dims[1:]
+    fac = list(fac)
+    if plan.mode != 0:
+        a0 = fac[0]
+        fac[0] = torch.cat([a0, torch.zeros((1, a0.shape[1]), dtype=a0.dtype, device=a0.device)])
+    g, p, timer = mttkrp_device(y.even_device_data(dev), dims, fac, plan.mode, lam, plan)
+    return (g[: y.dims[0]] if plan.mode == 0 else g), p, timer
 
 
 _side = {}

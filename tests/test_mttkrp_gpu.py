@@ -392,3 +392,20 @@ def test_mttkrp_modes_streams_all_modes_bit_identically(monkeypatch, dims):
             g = g.cpu().numpy() if torch.is_tensor(g) else g
             assert np.array_equal(g, ref), (dims, k)
             assert oracle.rel_err(g, oracle.mttkrp_ref(y, dims, k, fs, lam)) <= TOL
+
+
+@pytest.mark.parametrize("dims", [(41, 36, 34), (7, 5, 8, 9), (65, 3), (129, 20, 3)])
+def test_odd_first_extent_runs_through_the_even_copy(dims):
+    """Odd I_0 (no 16-byte TMA strides): auto plans run on a zero-padded
+    copy with an even I_0 -- same G for every mode (first I_0 rows for
+    mode 0), weights folded once."""
+    rank = 45
+    y = rng_for(61).random(int(np.prod(dims)))
+    fs = [rng_for(62 + j).random((n, rank)) for j, n in enumerate(dims)]
+    lam = rng_for(60).random(rank) + 0.5
+    m = ck.KruskalTensor(lam, fs)
+    t = ck.DenseTensor(dims, y)
+    for k in range(len(dims)):
+        got = ck.run(t, m, MttkrpPlan(Variant.B200, k)).matrix
+        assert got.shape == (dims[k], rank)
+        assert oracle.rel_err(got, oracle.mttkrp_ref(y, dims, k, fs, lam)) <= TOL, (dims, k)
