@@ -132,7 +132,6 @@ def cp_als(y: DenseTensor, config: AlsConfig, graph: bool | None = None) -> tupl
     if graph is None:
         graph = config.max_iters >= GRAPH_MIN_ITERS
     dev = require_cuda()
-    y_dev = y.device_data(dev)
     norm_y = y.norm()
     if not math.isfinite(norm_y):  # NaN/Inf anywhere make ||y|| non-finite
         raise ParameterError("tensor has non-finite entries")
@@ -144,26 +143,34 @@ def cp_als(y: DenseTensor, config: AlsConfig, graph: bool | None = None) -> tupl
     lib = _lib.load()
 
     t_start = time.perf_counter()
+    # an odd I_0 runs on the zero-padded even copy (mttkrp._pad_first_mode):
+    # A_0 then carries one extra row, which stays exactly zero (its MTTKRP
+    # row is a sum over zeros, and solve / normalize / Gram keep it at zero)
+    pad = mt._pad_first_mode(y, mt.plan_for_mode(config.plan, dims, 0), dev) and d >= 2
+    run_dims = ((dims[0] + 1,) + dims[1:]) if pad else dims
+    y_dev = y.even_device_data(dev) if pad else y.device_data(dev)
     # fixed buffers: every sweep (eager or replayed) reads and writes these
     factors = [torch.from_numpy(a).to(dev) for a in init_factors(dims, r, config.seed)]
+    if pad:
+        factors[0] = torch.cat([factors[0], torch.zeros((1, r), dtype=torch.float64, device=dev)])
     grams = [gram(a) for a in factors]
     lam = torch.ones(r, dtype=torch.float64, device=dev)
-    solver = _Solver(dev, max(dims), r)
+    solver = _Solver(dev, max(run_dims), r)
     gamma = torch.empty((r, r), dtype=torch.float64, device=dev)
     h = torch.empty((r, r), dtype=torch.float64, device=dev)
     normsq = torch.empty(r, dtype=torch.float64, device=dev)
-    g_last = torch.empty((dims[d - 1], r), dtype=torch.float64, device=dev)
+    g_last = torch.empty((run_dims[d - 1], r), dtype=torch.float64, device=dev)
     stats = torch.zeros(2 + d, dtype=torch.float64, device=dev)  # fit terms, Cholesky flags
     info = torch.zeros(d, dtype=torch.int32, device=dev)
     stats_host = torch.zeros(2 + d, dtype=torch.float64, pin_memory=True)
-    plans = [mt.plan_for_mode(config.plan, dims, k) for k in range(d)]
+    plans = [mt.plan_for_mode(config.plan, run_dims, k) for k in range(d)]
     ev = [torch.cuda.Event(enable_timing=True, external=True) for _ in range(d + 2)]
 
     def sweep(spec: bool) -> None:
         sp = stream_ptr(dev)
         ev[0].record()
         for k in range(d):
-            mt.mttkrp_device(y_dev, dims, factors, k, None, plans[k], out=factors[k])
+            mt.mttkrp_device(y_dev, run_dims, factors, k, None, plans[k], out=factors[k])
             ev[k + 1].record()
             if k == d - 1:  # the fit needs the last mode's G itself
                 g_last.copy_(factors[k])
@@ -175,7 +182,7 @@ def cp_als(y: DenseTensor, config: AlsConfig, graph: bool | None = None) -> tupl
                 if x is not factors[k]:  # least-squares last rung
                     factors[k].copy_(x)
             _lib.check(
-                lib.cpk_normalize_columns_f64(factors[k].data_ptr(), dims[k], r, factors[k].stride(0),
+                lib.cpk_normalize_columns_f64(factors[k].data_ptr(), run_dims[k], r, factors[k].stride(0),
                                               lam.data_ptr(), normsq.data_ptr(), sp),
                 "normalize",
             )
@@ -184,7 +191,7 @@ def cp_als(y: DenseTensor, config: AlsConfig, graph: bool | None = None) -> tupl
         # g_last is the unit-weight mode-(d-1) MTTKRP and A_{d-1} was solved from it
         _lib.check(
             lib.cpk_fit_terms_f64(h.data_ptr(), lam.data_ptr(), g_last.data_ptr(), factors[d - 1].data_ptr(),
-                                  dims[d - 1], r, stats.data_ptr(), sp),
+                                  run_dims[d - 1], r, stats.data_ptr(), sp),
             "fit terms",
         )
         stats[2:].copy_(info)
@@ -251,6 +258,8 @@ def cp_als(y: DenseTensor, config: AlsConfig, graph: bool | None = None) -> tupl
 
     torch.cuda.synchronize(dev)
     total = time.perf_counter() - t_start
+    if pad:
+        factors[0] = factors[0][: dims[0]]
     model = KruskalTensor(lam.clone(), factors, validate=False)
     trace = AlsTrace(
         fits=fits,

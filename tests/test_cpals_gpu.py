@@ -131,3 +131,15 @@ def test_graph_rollback_on_singular_gamma():
     _, t_e = ck.cp_als(y, cfg, graph=False)
     assert np.all(np.isfinite(t_g.fits))
     np.testing.assert_array_equal(t_g.fits, t_e.fits)
+
+
+@pytest.mark.parametrize("dims", [(9, 8, 7), (5, 6, 4, 3)])
+def test_odd_first_extent_sweeps_on_the_even_copy(dims):
+    """Odd I_0: the sweep runs on the zero-padded copy with A_0 one row
+    longer (that row stays zero); fits follow the oracle's cp_als and the
+    model has the tensor's shapes."""
+    y = rng_for(sum(dims) + 3).random(int(np.prod(dims)))
+    model, tr = ck.cp_als(ck.DenseTensor(dims, y), ck.AlsConfig(rank=4, tol=0.0, max_iters=6, seed=2))
+    _, _, ref = oracle.cp_als(y, dims, 4, max_iters=6, tol=0.0, seed=2)
+    assert np.max(np.abs(np.asarray(tr.fits) - np.asarray(ref))) <= 1e-8
+    assert [tuple(a.shape) for a in model.factors] == [(n, 4) for n in dims]
