@@ -37,3 +37,60 @@ def test_uniform_slab_matches_cpu_twin():
         assert np.array_equal(got, full[lo:hi])
     t = ck.DenseTensor.uniform(dims, seed=5)
     assert np.array_equal(t.data.cpu().numpy(), full.ravel(order="F"))
+
+
+def _gpu_worker(rank, world, port, dims, rank_r, iters, dten, out_q):
+    import os
+
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    # gloo with CUDA tensors: every rank on cuda:0 (one GPU here); the
+    # kernels, partition, collectives and fit assembly are the real path
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        part = sharded.partition_for(dims, world)
+        if dten:
+            y_local = sharded.dten_slab(dten, part, rank, device="cuda")
+        else:
+            y_local = sharded.uniform_slab(part, rank, seed=7)
+        model, tr = sharded.cp_als_sharded(y_local, part, ck.AlsConfig(rank=rank_r, tol=0.0, max_iters=iters,
+                                                                       seed=3), sharded.Comm())
+        out_q.put((rank, tr.fits, [a.cpu().numpy() for a in model.factors], model.weights.cpu().numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,dims,dten", [(2, (40, 36, 34), False), (3, (30, 20, 8, 6), False),
+                                             (2, (33, 24, 18), True)])
+def test_multi_process_device_path_matches_single_process(tmp_path, world, dims, dten):
+    """world 2-3 processes, each running the sm_100a kernels on its slab
+    (generated on device, or read from a DTEN file), gloo collectives:
+    every rank ends with the single-process trajectory and model."""
+    import socket
+
+    import torch.multiprocessing as mp
+
+    full = gen.splitmix_uniform(int(np.prod(dims)), seed=7)
+    path = None
+    if dten:
+        path = str(tmp_path / "y.dten")
+        ck.write_dten(path, ck.DenseTensor(dims, full))
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_gpu_worker, args=(r, world, port, dims, 6, 4, path, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=300) for _ in procs], key=lambda x: x[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    _, tr_ref = ck.cp_als(ck.DenseTensor(dims, full), ck.AlsConfig(rank=6, tol=0.0, max_iters=4, seed=3))
+    for rank, fits, factors, lam in res:
+        assert np.max(np.abs(np.asarray(fits) - np.asarray(tr_ref.fits))) <= 1e-10, rank
+        assert [a.shape for a in factors] == [(n, 6) for n in dims]
+        assert np.array_equal(factors[1], res[0][2][1]) and np.array_equal(lam, res[0][3])  # replicated
