@@ -51,7 +51,7 @@ constexpr int F_THREADS = (2 + F_XFORM_WARPS + F_DRAIN_WARPS) * 32;
 constexpr int F_GROUP = 4;  // chunks (48 MMAs) per TMEM accumulator before a drain
 // TMEM columns: two group accumulators [0, 256) and the running sum [256, 384)
 constexpr int F_SUM_COL = 2 * F_BN, F_TMEM_COLS = 512;
-constexpr int F_RAW_STAGES = 2, F_OP_STAGES = 2;
+constexpr int F_OP_STAGES = 2;
 constexpr int F_TILE_BYTES = F_BM * F_BK * 4;  // 16 KB: one 128 x 32 fp32 operand tile
 static_assert(F_BM == F_BN, "A and B operand tiles share one size");
 
@@ -67,16 +67,25 @@ struct alignas(64) F32Params {
   const float* lam;  // folded in the epilogue only when writing G directly
 };
 
-template <int NO>
+// KMAJ (mode > 0): TMA lands Y K-major with the 128-B swizzle, which is
+// already the UMMA A layout, and the tensor core's fp32 -> TF32 truncation is
+// exactly tf32_hi(): the UMMAs read Y_hi from the raw stage itself, so only
+// Y_lo is written (the op stage drops A_hi) and the raw stage stays busy
+// until the MMAs have read it -- hence 3 raw stages.  Mode 0 transposes.
+template <int NO, bool KMAJ>
 struct F32Cfg {
+  static constexpr int RAW_STAGES = KMAJ ? 3 : 2;
   static constexpr int RAW_Y = 0;
   static constexpr int RAW_F = RAW_Y + F_TILE_BYTES;        // [32 k][128 n] fp32
   static constexpr int RAW_P = RAW_F + F_BK * F_BN * 4;     // NO x 128 fp32
   static constexpr int RAW_BYTES = ((RAW_P + NO * F_BN * 4 + 1023) / 1024) * 1024;
   static constexpr int TX = F_TILE_BYTES + F_BK * F_BN * 4 + NO * F_BN * 4;
-  // operand stage: A_hi, A_lo, B_hi, B_lo (K-major SW128, 1024-B aligned)
-  static constexpr int OP_BYTES = 4 * F_TILE_BYTES;
-  static constexpr int OP_BASE = F_RAW_STAGES * RAW_BYTES;
+  // operand stage: [A_hi (mode 0 only)], A_lo, B_hi, B_lo (K-major SW128)
+  static constexpr int A_HI = 0;
+  static constexpr int A_LO = KMAJ ? 0 : F_TILE_BYTES;
+  static constexpr int B_HI = A_LO + F_TILE_BYTES, B_LO = B_HI + F_TILE_BYTES;
+  static constexpr int OP_BYTES = B_LO + F_TILE_BYTES;
+  static constexpr int OP_BASE = RAW_STAGES * RAW_BYTES;
   static constexpr int BAR_BASE = OP_BASE + F_OP_STAGES * OP_BYTES;
   static constexpr size_t SMEM = size_t(BAR_BASE) + 256;
 };
@@ -180,16 +189,17 @@ __device__ __forceinline__ void split_store(float* hi_tile, float* lo_tile, int 
 // ---------------------------------------------------------------- kernel
 template <bool KMAJ, int NO>
 __global__ void __launch_bounds__(F_THREADS, 1) mttkrp_f32_umma_sm100(const __grid_constant__ F32Params p) {
-  using C = F32Cfg<NO>;
+  using C = F32Cfg<NO, KMAJ>;
+  constexpr int RS = C::RAW_STAGES;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::BAR_BASE);
-  uint64_t* raw_full = bars;                          // [2] TMA landed
-  uint64_t* raw_empty = bars + 2;                     // [2] transform done with the raw stage
-  uint64_t* op_full = bars + 4;                       // [2] operands written
-  uint64_t* op_empty = bars + 6;                      // [2] UMMAs done reading
-  uint64_t* acc_full = bars + 8;                      // [2] accumulator group done
-  uint64_t* acc_empty = bars + 10;                    // [2] accumulator drained
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 12);
+  uint64_t* raw_full = bars;                          // [RS] TMA landed
+  uint64_t* raw_empty = bars + 3;                     // [RS] raw stage consumed (transform, + MMA if KMAJ)
+  uint64_t* op_full = bars + 6;                       // [2] operands written
+  uint64_t* op_empty = bars + 8;                      // [2] UMMAs done reading
+  uint64_t* acc_full = bars + 10;                     // [2] accumulator group done
+  uint64_t* acc_empty = bars + 12;                    // [2] accumulator drained
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 14);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t q0 = int64_t(blockIdx.z) * p.chunks_per_split;
@@ -197,9 +207,11 @@ __global__ void __launch_bounds__(F_THREADS, 1) mttkrp_f32_umma_sm100(const __gr
   const int j0 = blockIdx.x * F_BN, n0 = blockIdx.y * F_BM;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < RS; ++s) {
       bar_init(&raw_full[s], 1);
-      bar_init(&raw_empty[s], F_XFORM_WARPS);
+      bar_init(&raw_empty[s], F_XFORM_WARPS + (KMAJ ? 1 : 0));
+    }
+    for (int s = 0; s < 2; ++s) {
       bar_init(&op_full[s], F_XFORM_WARPS);
       bar_init(&op_empty[s], 1);
     }
@@ -233,8 +245,8 @@ __global__ void __launch_bounds__(F_THREADS, 1) mttkrp_f32_umma_sm100(const __gr
       }
       constexpr int D = NO + 2;
       for (int it = 0; it < nst; ++it) {
-        const int s = it & 1;
-        if (it >= 2) bar_wait(&raw_empty[s], ((it >> 1) - 1) & 1);
+        const int s = it % RS;
+        if (it >= RS) bar_wait(&raw_empty[s], ((it / RS) - 1) & 1);
         uint8_t* st = smem + s * C::RAW_BYTES;
         bar_expect_tx(&raw_full[s], C::TX);
         const int if0 = qf * F_BK;
@@ -281,8 +293,10 @@ __global__ void __launch_bounds__(F_THREADS, 1) mttkrp_f32_umma_sm100(const __gr
         bar_wait(&op_full[o], (it >> 1) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
         const uint32_t base = su32(smem + C::OP_BASE + o * C::OP_BYTES);
-        const uint64_t a_hi = sw128_desc(base), a_lo = sw128_desc(base + F_TILE_BYTES);
-        const uint64_t b_hi = sw128_desc(base + 2 * F_TILE_BYTES), b_lo = sw128_desc(base + 3 * F_TILE_BYTES);
+        const int s = it % RS;
+        const uint64_t a_hi = KMAJ ? sw128_desc(su32(smem + s * C::RAW_BYTES + C::RAW_Y)) : sw128_desc(base + C::A_HI);
+        const uint64_t a_lo = sw128_desc(base + C::A_LO);
+        const uint64_t b_hi = sw128_desc(base + C::B_HI), b_lo = sw128_desc(base + C::B_LO);
         const uint32_t acc_t = tmem + uint32_t(b * F_BN);
 #pragma unroll
         for (int ks = 0; ks < F_BK / 8; ++ks) {  // UMMA_K = 8 tf32 = 32 B: +2 in the 16-B address units
@@ -292,6 +306,7 @@ __global__ void __launch_bounds__(F_THREADS, 1) mttkrp_f32_umma_sm100(const __gr
           umma_tf32(acc_t, a_lo + adv, b_hi + adv, 1u);
         }
         umma_commit(&op_empty[o]);  // operand stage free once these MMAs have read it
+        if constexpr (KMAJ) umma_commit(&raw_empty[s]);  // and the raw stage (Y_hi)
         if (it % F_GROUP == F_GROUP - 1 || it == nst - 1) umma_commit(&acc_full[b]);
       }
     }
@@ -301,22 +316,29 @@ __global__ void __launch_bounds__(F_THREADS, 1) mttkrp_f32_umma_sm100(const __gr
     // groups k4 in [4h, 4h + 4) with h = t / 128
     const int t = threadIdx.x - 64, r = t & (F_BM - 1), k4_0 = (t >> 7) * 4;
     for (int it = 0; it < nst; ++it) {
-      const int s = it & 1, o = it & 1;
-      bar_wait(&raw_full[s], (it >> 1) & 1);
+      const int s = it % RS, o = it & 1;
+      bar_wait(&raw_full[s], (it / RS) & 1);
       if (it >= 2) bar_wait(&op_empty[o], ((it >> 1) - 1) & 1);
       const uint8_t* st = smem + s * C::RAW_BYTES;
-      float* op = reinterpret_cast<float*>(smem + C::OP_BASE + o * C::OP_BYTES);
-      float* a_hi = op;
-      float* a_lo = op + F_BM * F_BK;
-      float* b_hi = op + 2 * F_BM * F_BK;
-      float* b_lo = op + 3 * F_BM * F_BK;
+      uint8_t* op = smem + C::OP_BASE + o * C::OP_BYTES;
+      float* a_hi = reinterpret_cast<float*>(op + C::A_HI);
+      float* a_lo = reinterpret_cast<float*>(op + C::A_LO);
+      float* b_hi = reinterpret_cast<float*>(op + C::B_HI);
+      float* b_lo = reinterpret_cast<float*>(op + C::B_LO);
       const float* ry = reinterpret_cast<const float*>(st + C::RAW_Y);
       if constexpr (KMAJ) {
-        // TMA already wrote Y K-major with the 128-B swizzle: split in place
+        // Y_hi is the raw tile itself (see F32Cfg): write Y_lo only, at the
+        // same swizzled offsets
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           const int off = (t + 256 * i) * 4;  // float4 chunk index * 4
-          split_store(a_hi, a_lo, off, *reinterpret_cast<const float4*>(ry + off));
+          const float4 v = *reinterpret_cast<const float4*>(ry + off);
+          float4 l;
+          l.x = v.x - tf32_hi(v.x);
+          l.y = v.y - tf32_hi(v.y);
+          l.z = v.z - tf32_hi(v.z);
+          l.w = v.w - tf32_hi(v.w);
+          *reinterpret_cast<float4*>(a_lo + off) = l;
         }
       } else {
         // Y landed M-major [32 k][128 m]: transpose row m = t into K-major
@@ -453,8 +475,9 @@ int encode32(CUtensorMap* map, const void* base, int rank, const cuuint64_t* dim
 
 template <bool KMAJ, int NO>
 void f32_kernel(const void** fn, size_t* smem) {
+  static_assert(F32Cfg<NO, KMAJ>::SMEM <= 227 * 1024, "shared memory budget");
   *fn = reinterpret_cast<const void*>(&mttkrp_f32_umma_sm100<KMAJ, NO>);
-  *smem = F32Cfg<NO>::SMEM;
+  *smem = F32Cfg<NO, KMAJ>::SMEM;
 }
 
 struct F32Problem {
