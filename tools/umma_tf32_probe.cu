@@ -2,6 +2,10 @@
 // the float32 MTTKRP: K-major SWIZZLE_128B smem operands written by threads,
 // UMMA smem descriptors, the instruction descriptor, TMEM alloc / ld, and
 // commit-to-mbarrier.  D[128 x N] = A[128 x K] * B[N x K]^T, K = 32 per stage.
+// Modes: 0 = A K-major (works; the fp32 kernel's layout); 1/2 = A in the
+// MN-major SWIZZLE_128B canonical layout with the transpose-A bit set (and
+// LBO/SBO swapped): both return all zeros on this B200/driver, which is why
+// the fp32 kernel transposes mode-0 tiles itself.
 // nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/umma_tf32_probe tools/umma_tf32_probe.cu
 #include <cstdio>
 #include <cstdlib>
@@ -31,13 +35,22 @@ __device__ __forceinline__ uint64_t sdesc(const void* p) {
   return d;
 }
 
-__host__ __device__ constexpr uint32_t idesc_tf32(int m, int n) {
+__host__ __device__ constexpr uint32_t idesc_tf32(int m, int n, int a_mn = 0) {
   return (1u << 4)            // D = F32
          | (2u << 7)          // A = TF32
          | (2u << 10)         // B = TF32
-         | (0u << 15)         // A K-major
+         | (uint32_t(a_mn) << 15)  // A K-major (0) / MN-major (1)
          | (0u << 16)         // B K-major
          | (uint32_t(n >> 3) << 17) | (uint32_t(m >> 4) << 24);
+}
+// MN-major SW128: 32-m groups of 32 k-rows x 128 B (4096 B), 8-row atoms
+__device__ __forceinline__ int mn_off(int m, int k) {
+  return (m / 32) * 1024 + k * 32 + ((((m % 32) >> 2) ^ (k & 7)) << 2) + (m & 3);
+}
+__device__ __forceinline__ uint64_t sdesc_mn(const void* p, int swap) {
+  const uint64_t a = smem_u32(p);
+  const uint64_t lbo = swap ? 1024 : 4096, sbo = swap ? 4096 : 1024;
+  return ((a >> 4) & 0x3FFF) | ((lbo >> 4) << 16) | ((sbo >> 4) << 32) | (uint64_t(1) << 46) | (uint64_t(2) << 61);
 }
 
 __global__ void __launch_bounds__(128, 1) probe(const float* A, const float* B, float* D, int reps, int mode) {
@@ -47,7 +60,7 @@ __global__ void __launch_bounds__(128, 1) probe(const float* A, const float* B, 
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 32768);
   uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + 32768 + 64);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  for (int i = tid; i < M * K; i += 128) As[swz_off(i / K, i % K)] = A[i];
+  for (int i = tid; i < M * K; i += 128) As[mode ? mn_off(i / K, i % K) : swz_off(i / K, i % K)] = A[i];
   for (int i = tid; i < N * K; i += 128) Bs[swz_off(i / K, i % K)] = B[i];
   asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
   if (tid == 0) {
@@ -62,12 +75,12 @@ __global__ void __launch_bounds__(128, 1) probe(const float* A, const float* B, 
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
   const uint32_t tmem = *tslot;
-  constexpr uint32_t id = idesc_tf32(M, N);
+  const uint32_t id = idesc_tf32(M, N, mode ? 1 : 0);
   if (tid == 0) {
     for (int r = 0; r < reps; ++r) {
 #pragma unroll
       for (int k = 0; k < K / 8; ++k) {  // UMMA_K = 8 tf32 = 32 bytes: advance the start address
-        const uint64_t da = sdesc(As) + uint64_t((k * 32) >> 4);
+        const uint64_t da = mode ? sdesc_mn(As, mode == 2) + uint64_t(k * 64) : sdesc(As) + uint64_t((k * 32) >> 4);
         const uint64_t db = sdesc(Bs) + uint64_t((k * 32) >> 4);
         const uint32_t acc = (r > 0 || k > 0) ? 1u : 0u;
         asm volatile(
@@ -117,9 +130,10 @@ int main() {
   cudaMemcpy(dB, B.data(), B.size() * 4, cudaMemcpyHostToDevice);
   const int smem = 32768 + 1024;
   cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  probe<<<1, 128, smem>>>(dA, dB, dD, 1, 0);
+  for (int mode = 0; mode < 3; ++mode) {
+  probe<<<1, 128, smem>>>(dA, dB, dD, 1, mode);
   cudaError_t e = cudaDeviceSynchronize();
-  printf("launch: %s\n", cudaGetErrorString(e));
+  printf("mode %d (0 K-major, 1 MN-major, 2 MN swapped) launch: %s\n", mode, cudaGetErrorString(e));
   std::vector<float> D(M * N);
   cudaMemcpy(D.data(), dD, D.size() * 4, cudaMemcpyDeviceToHost);
   double maxrel = 0, maxabs = 0;
@@ -131,6 +145,7 @@ int main() {
       maxrel = std::max(maxrel, std::fabs(ref - D[m * N + n]) / std::fabs(ref));
     }
   printf("D[0][0]=%f  max rel err vs fp64 = %.3e (tf32 expected ~1e-3), max abs %.3e\n", D[0], maxrel, maxabs);
+  }
   // rate: reps MMAs of 128x128x32 per CTA, 148 CTAs
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
