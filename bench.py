@@ -274,6 +274,34 @@ def run_b200(args):
     total_flops = algo_flops(DIMS, RANK) * 3 * args.steps
     value = total_flops / elapsed / 1e9
 
+    # ---- GFLOP/s and roofline fraction vs rank R (BASELINE.json's metric
+    # name) on the config-2 shape, every mode, auto plans; not part of `value`
+    rank_sweep = None
+    if args.rank_sweep and world == 1:
+        from paper_2510_14891_b200.perfmodel import roofline_seconds
+
+        d2 = (512, 512, 512)
+        y2 = torch.empty(int(np.prod(d2)), dtype=torch.float64, device=dev)
+        _lib.check(lib.cpk_fill_uniform_f64(y2.data_ptr(), y2.numel(), SEED, 0,
+                                            torch.cuda.current_stream().cuda_stream), "fill")
+        rank_sweep = {"shape": list(d2), "roofline": "max(8N/HBM, 2NR(d-1)/FP64 nominal)", "points": []}
+        for r in (16, 32, 64, 128, 256, 512, 1000, 2000):
+            rng = np.random.Generator(np.random.Philox(1))
+            f2 = [torch.from_numpy(rng.random((n, r))).to(dev) for n in d2]
+            ms = []
+            for k in range(3):
+                ts = []
+                for _ in range(3):
+                    _, _, t = mttkrp_device(y2, d2, f2, k, None, MttkrpPlan(Variant.B200, k))
+                    ts.append(t.seconds)
+                ms.append(min(ts[1:]) * 1e3)
+            roof = roofline_seconds(d2, r) * 1e3  # nominal FP64 peak (37.2 TF/s at 1965 MHz)
+            rank_sweep["points"].append({"rank": r, "ms_per_mode": ms,
+                                         "gflops": algo_flops(d2, r) * 3 / (sum(ms) * 1e-3) / 1e9,
+                                         "roofline_frac": 3 * roof / sum(ms)})
+        del y2, f2
+        torch.cuda.empty_cache()
+
     # ---- the library baseline on the same GPU: partial KRPs + cuBLAS DGEMM
     # (the reference's mttkrp_gemm, mttkrp.py:230-276); not part of `value`
     gemm = None
@@ -448,6 +476,7 @@ def run_b200(args):
                          "north_star_roofline_ms_per_mode": roof_t * 1e3,
                          "north_star_frac": roof_t * 3 * args.steps / elapsed},
             "dfma_engine": dfma,
+            "rank_sweep": rank_sweep,
             "gemm_baseline": gemm,
             "fp32_path": f32,
             "cpu_baseline": cpu,
@@ -537,6 +566,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--dfma-steps", type=int, default=2)
     ap.add_argument("--gemm-steps", type=int, default=2)
+    ap.add_argument("--rank-sweep", type=int, default=1, help="1: add the GFLOP/s-vs-rank leg (c2 shape)")
     ap.add_argument("--f32-steps", type=int, default=2)
     ap.add_argument("--cpals-iters", type=int, default=10)
     ap.add_argument("--c5-iters", type=int, default=3)
