@@ -34,7 +34,7 @@ import torch
 from . import _lib
 from ._device import EventTimer, require_cuda, stream_ptr, workspace
 from .dtensor import DenseTensor, check_dims, num_elements
-from .errors import IndexRangeError, ParameterError, ShapeError
+from .errors import DeviceError, IndexRangeError, ParameterError, ShapeError
 from .kruskal import KruskalTensor
 
 
@@ -183,9 +183,26 @@ def mttkrp_device(y_dev: torch.Tensor, dims, factors, mode: int, weights=None, p
     d = len(dims)
     mode = int(mode)
     dev = y_dev.device
+    if not y_dev.is_cuda:
+        raise DeviceError("mttkrp_device needs a CUDA tensor (there is no CPU path)")
+    if y_dev.dim() != 1 or not y_dev.is_contiguous() or y_dev.numel() != num_elements(dims):
+        raise ShapeError(f"y must be a flat contiguous tensor of {num_elements(dims)} elements")
+    if len(factors) != d:
+        raise ShapeError(f"{len(factors)} factors for a {d}-way tensor")
     rank = next(int(f.shape[1]) for f in factors if f is not None)
     if plan is None:
         plan = MttkrpPlan(Variant.B200, mode)
+    # the kernels read row-major factors with unit column stride, in y's dtype
+    want = y_dev.dtype if y_dev.dtype == torch.float32 else torch.float64
+    # (mode k's own factor is not read: passed through untouched)
+    factors = [f if (m == mode or (f.dtype == want and f.device == dev and f.stride(1) == 1)) else
+               f.to(device=dev, dtype=want).contiguous()
+               for m, f in enumerate(factors)]
+    for m, f in enumerate(factors):
+        if m != mode and (f.dim() != 2 or f.shape[0] != dims[m] or f.shape[1] != rank):
+            raise ShapeError(f"factor {m} has shape {tuple(f.shape)}, expected ({dims[m]}, {rank})")
+    if weights is not None and (weights.dtype != want or weights.device != dev or not weights.is_contiguous()):
+        weights = weights.to(device=dev, dtype=want).contiguous()
     if y_dev.dtype == torch.float32:
         if landed is not None:
             raise ParameterError("the float32 path has no streamed (landed) form")

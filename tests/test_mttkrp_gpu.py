@@ -409,3 +409,31 @@ def test_odd_first_extent_runs_through_the_even_copy(dims):
         got = ck.run(t, m, MttkrpPlan(Variant.B200, k)).matrix
         assert got.shape == (dims[k], rank)
         assert oracle.rel_err(got, oracle.mttkrp_ref(y, dims, k, fs, lam)) <= TOL, (dims, k)
+
+
+def test_device_entry_normalizes_factor_layouts_and_checks_shapes():
+    """mttkrp_device with column-major (transposed-view) or float32 factors
+    and a float64 tensor: the factors are re-laid out, not misread; wrong
+    shapes and CPU tensors raise the reference's classes."""
+    from paper_2510_14891_b200.mttkrp import mttkrp_device
+
+    dims, rank = (20, 18, 16), 24
+    y = rng_for(71).random(int(np.prod(dims)))
+    fs = [rng_for(72 + j).random((n, rank)) for j, n in enumerate(dims)]
+    yd = torch.from_numpy(y).cuda()
+    for k in range(3):
+        ref = oracle.mttkrp_ref(y, dims, k, fs)
+        col_major = [torch.from_numpy(np.asfortranarray(a)).cuda() for a in fs]  # stride(1) != 1
+        assert col_major[0].stride(1) != 1
+        g, _, _ = mttkrp_device(yd, dims, col_major, k)
+        assert oracle.rel_err(g.cpu().numpy(), ref) <= TOL
+        g32f, _, _ = mttkrp_device(yd, dims, [torch.from_numpy(a.astype(np.float32)).cuda() for a in fs], k)
+        assert g32f.dtype == torch.float64
+        ref32f = oracle.mttkrp_ref(y, dims, k, [a.astype(np.float32).astype(np.float64) for a in fs])
+        assert oracle.rel_err(g32f.cpu().numpy(), ref32f) <= TOL
+    with pytest.raises(ck.ShapeError):
+        mttkrp_device(yd, dims, [torch.from_numpy(a).cuda() for a in fs[:2]], 0)
+    with pytest.raises(ck.ShapeError):
+        mttkrp_device(yd, (20, 18, 15), [torch.from_numpy(a).cuda() for a in fs], 0)
+    with pytest.raises(ck.DeviceError):
+        mttkrp_device(torch.from_numpy(y), dims, [torch.from_numpy(a) for a in fs], 0)
