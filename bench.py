@@ -186,8 +186,8 @@ def run_b200(args):
 
     import paper_2510_14891_b200 as ck
     from paper_2510_14891_b200 import _lib
+    from paper_2510_14891_b200 import harness
     from paper_2510_14891_b200.mttkrp import MttkrpPlan, Variant, mttkrp_device, resolve_plan
-    from oracle import gen
 
     # ---- inputs resident in HBM: this rank's mode-0 slab of config 4
     lo, hi = shard_rows(DIMS[0], world, rank)
@@ -203,7 +203,8 @@ def run_b200(args):
     else:
         y = full.view(DIMS[2] * DIMS[1], DIMS[0])[:, lo:hi].contiguous().view(-1)
         del full
-    fs_host = gen.bench_factors(DIMS, RANK, SEED)
+    # the reference CLI's factor recipe (cli.py:137-141): Philox(seed + 1)
+    fs_host = [np.asarray(a) for a in harness.bench_factors(DIMS, RANK, SEED).factors]
     fs_host[0] = np.ascontiguousarray(fs_host[0][lo:hi])
     fs = [torch.from_numpy(a).to(dev) for a in fs_host]
     torch.cuda.synchronize()

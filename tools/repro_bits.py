@@ -13,7 +13,7 @@ import torch
 ROOT = Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT))
 import paper_2510_14891_b200 as ck  # noqa: E402
-from oracle import gen  # noqa: E402
+from paper_2510_14891_b200 import harness  # noqa: E402
 from paper_2510_14891_b200.mttkrp import MttkrpPlan, Variant, mttkrp_device, resolve_plan  # noqa: E402
 
 ap = argparse.ArgumentParser()
@@ -22,8 +22,8 @@ ap.add_argument("--small", action="store_true")
 a = ap.parse_args()
 dims, rank = ((40, 36, 34), 130) if a.small else ((512, 512, 512), 64)
 dev = torch.device("cuda", 0)
-y = torch.from_numpy(gen.philox_tensor(dims, 0)).to(dev)
-fs = [torch.from_numpy(f).to(dev) for f in gen.bench_factors(dims, rank, 0)]
+y = torch.from_numpy(np.random.Generator(np.random.Philox(0)).random(int(np.prod(dims)))).to(dev)
+fs = [torch.from_numpy(np.asarray(f)).to(dev) for f in harness.bench_factors(dims, rank, 0).factors]
 for engine, rt, bk in (("tma", 128, 32), ("tma", 64, 0), ("cpasync", 128, 32), ("dmma", 128, 32), ("dmma", 64, 0)):
     for k in range(3):
         plan = MttkrpPlan(Variant.B200, k, rank_tile=rt, block_k=bk, engine=engine)
