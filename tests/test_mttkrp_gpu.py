@@ -437,3 +437,35 @@ def test_device_entry_normalizes_factor_layouts_and_checks_shapes():
         mttkrp_device(yd, (20, 18, 15), [torch.from_numpy(a).cuda() for a in fs], 0)
     with pytest.raises(ck.DeviceError):
         mttkrp_device(torch.from_numpy(y), dims, [torch.from_numpy(a) for a in fs], 0)
+
+
+def test_c5_full_size_row_sampled_parity():
+    """BASELINE config 5 at full size on one GPU (4096 x 2048 x 2048 float64,
+    137 GB, R = 512; int64 indexing well past 2^31 elements): rows of every
+    mode's G against the oracle's TILE restatement on single-slice
+    sub-tensors."""
+    dims, rank, seed = (4096, 2048, 2048), 512, 0
+    free = torch.cuda.mem_get_info()[0]
+    if free < 8 * int(np.prod(dims)) + (8 << 30):
+        pytest.skip(f"needs ~146 GB of free device memory, has {free / 1e9:.0f} GB")
+    t = ck.DenseTensor.uniform(dims, seed=seed)
+    fs = gen.bench_factors(dims, rank, 0)
+    m = ck.KruskalTensor(np.ones(rank), fs, validate=False)
+    inner = []
+    try:
+        for k in range(3):
+            got = ck.run(t, m, MttkrpPlan(Variant.B200, k)).matrix.cpu().numpy()
+            # size-independent identity: sum_n G_k[n, :] * A_k[n, :] = <Y, a_0j o a_1j o a_2j>
+            # is the same vector for every mode k
+            inner.append((got * fs[k]).sum(axis=0))
+            for n in (0, dims[k] - 1):
+                ys = gen.splitmix_slice(dims, k, n, seed)
+                sub_dims = tuple(1 if j == k else e for j, e in enumerate(dims))
+                sub_f = [a[n:n + 1] if j == k else a for j, a in enumerate(fs)]
+                ref = oracle.mttkrp_tile(ys, sub_dims, k, sub_f, f_cols=16, n_t=65536)[0][0]
+                assert oracle.rel_err(got[n], ref) <= TOL, (k, n)
+        for k in (1, 2):
+            assert oracle.rel_err(inner[k], inner[0]) <= 1e-12, k
+    finally:
+        del t
+        torch.cuda.empty_cache()
