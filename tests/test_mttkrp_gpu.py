@@ -181,8 +181,10 @@ def test_c4_row_sampled_parity():
     t = ck.DenseTensor.uniform(dims, seed=seed)
     fs = gen.bench_factors(dims, rank, 0)
     m = ck.KruskalTensor(np.ones(rank), fs, validate=False)
+    inner = []
     for k in range(3):
         got = ck.run(t, m, MttkrpPlan(Variant.B200, k)).matrix.cpu().numpy()
+        inner.append((got * fs[k]).sum(axis=0))  # the same vector for every mode
         for n in (0, 517, 1023):
             ys = gen.splitmix_slice(dims, k, n, seed)
             sub_dims = tuple(1 if j == k else e for j, e in enumerate(dims))
@@ -190,6 +192,7 @@ def test_c4_row_sampled_parity():
             # the TILE restatement on the single-slice sub-tensor, all host cores
             ref = oracle.mttkrp_tile(ys, sub_dims, k, sub_f, f_cols=16, n_t=16384)[0][0]
             assert oracle.rel_err(got[n], ref) <= TOL, (k, n)
+    assert oracle.rel_err(inner[1], inner[0]) <= 1e-12 and oracle.rel_err(inner[2], inner[0]) <= 1e-12
 
 
 @pytest.mark.parametrize("engine", ["tma", "dmma"])
