@@ -418,13 +418,29 @@ __global__ void __launch_bounds__(WS_THREADS, 1) mttkrp_f64_ws_sm100(const __gri
           pr.x *= v.x;
           pr.y *= v.y;
         }
-#pragma unroll 4
-        for (int k = row0; k < BK; k += ROW_STEP) {
-          double2* rp = reinterpret_cast<double2*>(b_s + k * BN + 2 * pair);
-          double2 v = *rp;
-          v.x *= pr.x;
-          v.y *= pr.y;
-          *rp = v;
+        // loads of a batch of rows first, then the DMULs, then the stores:
+        // one round trip of shared-memory latency per batch instead of one
+        // per row (c3: 4.26 -> 4.11 ms per mode); batches of 8 rows keep the
+        // producer inside its setmaxnreg budget
+        constexpr int NR = (BK + ROW_STEP - 1) / ROW_STEP, NB = NR < 8 ? NR : 8;
+#pragma unroll
+        for (int b0 = 0; b0 < NR; b0 += NB) {
+          double2 v[NB];
+#pragma unroll
+          for (int i = 0; i < NB; ++i) {
+            const int k = row0 + (b0 + i) * ROW_STEP;
+            if (b0 + i < NR && k < BK) v[i] = *reinterpret_cast<const double2*>(b_s + k * BN + 2 * pair);
+          }
+#pragma unroll
+          for (int i = 0; i < NB; ++i) {
+            v[i].x *= pr.x;
+            v[i].y *= pr.y;
+          }
+#pragma unroll
+          for (int i = 0; i < NB; ++i) {
+            const int k = row0 + (b0 + i) * ROW_STEP;
+            if (b0 + i < NR && k < BK) *reinterpret_cast<double2*>(b_s + k * BN + 2 * pair) = v[i];
+          }
         }
         // generic-proxy writes must be ordered before the next TMA into this buffer
         fence_proxy_async();

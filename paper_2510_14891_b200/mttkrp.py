@@ -662,7 +662,7 @@ def heuristic_tile_volume(dims, machine) -> int:
 # csrc/mttkrp.cu; rates from the B200 sweeps (profiles/r01_sweep_*.agg.csv)
 _TILE_CHOICES = (  # same order as kChoices (ties go to the earlier entry)
     ("tma", 256, 96, 0.95), ("tma", 128, 128, 1.00), ("tma", 64, 256, 0.93),
-    ("dmma", 256, 64, 1.02), ("dmma", 128, 128, 1.19), ("dmma", 64, 256, 1.26),
+    ("dmma", 256, 64, 1.02), ("dmma", 128, 128, 1.23), ("dmma", 64, 256, 1.26),
     ("cpdmma", 128, 128, 0.97), ("cpdmma", 64, 256, 0.88),
     ("cpasync", 128, 128, 0.92), ("cpasync", 64, 128, 0.78), ("cpasync", 32, 64, 0.55),
 )
