@@ -592,14 +592,27 @@ def run(y: DenseTensor, m: KruskalTensor, plan: MttkrpPlan, **kwargs) -> MttkrpO
     return mttkrp_b200(y, m, plan)
 
 
+def _split_weights(factors, weights):
+    """Accept a ``(weights, [A_0, ..., A_{d-1}])`` pair where a factor list is
+    expected (the (lambda, factors) form of a Kruskal model)."""
+    if (isinstance(factors, tuple) and len(factors) == 2 and isinstance(factors[1], (list, tuple))
+            and getattr(factors[0], "ndim", 2) == 1):
+        if weights is not None:
+            raise ParameterError("weights given twice")
+        return list(factors[1]), factors[0]
+    return factors, weights
+
+
 def mttkrp(tensor, factors, mode: int, weights=None, plan: MttkrpPlan | None = None):
     """North-star convenience: G = MTTKRP(tensor, factors, mode).
 
     ``tensor`` is a DenseTensor or a flat/first-mode-fastest CUDA tensor
     (then ``factors`` must be CUDA too); ``factors`` is a list of (I_m, R)
-    matrices or a KruskalTensor (its weights are folded once).  Returns an
-    (I_k, R) matrix of the input's kind (numpy for host, torch for CUDA).
+    matrices, a ``(weights, factors)`` pair, or a KruskalTensor (weights are
+    folded once).  Returns an (I_k, R) matrix of the input's kind (numpy for
+    host, torch for CUDA).
     """
+    factors, weights = _split_weights(factors, weights)
     if isinstance(tensor, torch.Tensor) and tensor.is_cuda and tensor.dtype == torch.float32:
         # optional float32 path: device in, device out (float32)
         fs = list(factors.factors if isinstance(factors, KruskalTensor) else factors)

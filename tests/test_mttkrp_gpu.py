@@ -472,3 +472,17 @@ def test_c5_full_size_row_sampled_parity():
     finally:
         del t
         torch.cuda.empty_cache()
+
+
+def test_mttkrp_accepts_weights_factors_pair():
+    """ck.mttkrp(tensor, (weights, factors), mode) == the KruskalTensor form."""
+    dims, rank = (12, 10, 8), 9
+    y = rng_for(81).random(int(np.prod(dims)))
+    fs = [rng_for(82 + j).random((n, rank)) for j, n in enumerate(dims)]
+    lam = rng_for(80).random(rank) + 0.5
+    t = ck.DenseTensor(dims, y)
+    for k in range(3):
+        a = ck.mttkrp(t, (lam, fs), k)
+        b = ck.mttkrp(t, ck.KruskalTensor(lam, fs), k)
+        assert np.array_equal(a, b)
+        assert oracle.rel_err(a, oracle.mttkrp_ref(y, dims, k, fs, lam)) <= TOL
