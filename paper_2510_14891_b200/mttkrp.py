@@ -300,6 +300,7 @@ def _unit_weights(w) -> bool:
 # slabs, each slab's MTTKRP overlapping the copy of the next.
 STREAM_MIN_BYTES = 256 << 20
 STREAM_SLABS = 16  # 8 -> 16: e2e 394 -> 387 ms at c4 (first slab lands sooner); 32 is slower
+STREAM_GEOMETRIC = 8  # slabs 1/128, 1/128, 1/64, ... 1/2 of the extent (0: equal slabs)
 
 
 def _run_gpu(y: DenseTensor, m: KruskalTensor, plan: MttkrpPlan):
@@ -401,6 +402,21 @@ def _landed_pieces(y_dev, dims, fac, plan, lam, dev, bounds, events):
     return out, p, timer
 
 
+def _slab_bounds(extent: int) -> list:
+    """Slabs of the slowest mode for a streamed upload.  STREAM_GEOMETRIC:
+    sizes grow geometrically from 1/2^(n-1) of the extent (first slab lands
+    after ~1 % of the copy, so compute starts almost at once; the copy then
+    stays ahead of the compute, which consumes the tensor ~2x slower than
+    PCIe delivers it); else STREAM_SLABS equal slabs."""
+    if STREAM_GEOMETRIC and extent >= 2 ** (STREAM_GEOMETRIC - 1):
+        n = STREAM_GEOMETRIC
+        cuts = [0] + [extent >> (n - 1 - i) for i in range(n)]
+        cuts[-1] = extent
+        return [(a, b) for a, b in zip(cuts[:-1], cuts[1:]) if b > a]
+    n = min(STREAM_SLABS, extent)
+    return [(extent * i // n, extent * (i + 1) // n) for i in range(n)]
+
+
 def _start_upload(y: DenseTensor, dev):
     """Begin the slab-wise H2D copy of a host tensor on a copy stream; the
     device copy is cached on `y` with the slab events (DenseTensor.landing)."""
@@ -414,8 +430,7 @@ def _start_upload(y: DenseTensor, dev):
         # compute stream's queue (only its own stream's earlier users)
         y_dev = torch.empty(y.size, dtype=torch.float64, device=dev)
     y_dev.record_stream(compute)
-    n = min(STREAM_SLABS, dims[-1])
-    bounds = [(dims[-1] * i // n, dims[-1] * (i + 1) // n) for i in range(n)]
+    bounds = _slab_bounds(dims[-1])
     landed = []
     with torch.cuda.stream(copy):
         for lo, hi in bounds:
