@@ -254,7 +254,7 @@ def run_b200(args):
     # ---- the same step with the DFMA (CUDA-core FMA) consumers, for the
     # north star's literal math choice; not part of `value`
     dfma = None
-    if args.dfma_steps > 0:
+    if args.dfma_steps > 0 and world == 1:
         ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(3)]
         ms = [[] for _ in range(3)]
         for it in range(args.dfma_steps + 1):
