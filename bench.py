@@ -178,8 +178,15 @@ def run_b200(args):
     if world > 1:
         import torch.distributed as dist
 
+        # one process per GPU over NCCL; BENCH_DIST_BACKEND=gloo lets the
+        # tests run this multi-rank path with several ranks on one GPU
+        backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
+        local = local % torch.cuda.device_count()
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     else:
         torch.cuda.set_device(0)
     dev = torch.device("cuda", torch.cuda.current_device())

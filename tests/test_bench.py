@@ -42,3 +42,24 @@ def test_b200_arm_line():
     e = d["e2e"]
     assert e["h2d_bytes_per_step"] > 8 * 1024 ** 3 and e["d2h_bytes_per_step"] > 0 and 0 < e["value"] < d["value"]
     assert d["gpu_launches"] > 0 and {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
+
+
+@pytest.mark.gpu
+def test_b200_arm_multi_rank_path():
+    """The N > 1 path of bench.py (torchrun, mode-0 slabs, allreduce of the
+    other modes, max-over-ranks timing, e2e per rank) with 2 ranks on the one
+    GPU over gloo: one JSON line from rank 0, n_gpus = 2, the global
+    workload's flops."""
+    import os
+
+    env = dict(os.environ, BENCH_DIST_BACKEND="gloo")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", "--master-port=29517", str(ROOT / "bench.py"), "--gpus", "2", "--steps",
+           "1", "--warmup", "3", "--e2e-steps", "1", "--c5-iters", "0", "--cpu-seconds", "0.5"]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=1200, cwd=ROOT, env=env)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["e2e"]["value"] > 0
+    assert d["config"]["parallelism"] == "mode-0 block partition x2"
