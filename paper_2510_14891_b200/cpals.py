@@ -11,15 +11,15 @@ floating-point reassociation.
 Everything between two MTTKRPs stays on the device (Gram, Hadamard,
 Cholesky via cuSOLVER, normalization, fit terms), in fixed buffers: the
 MTTKRP of mode k is written straight into A_k's buffer (mode k's own factor
-is not read by its MTTKRP) and solved in place.  The first sweep runs
-eagerly with the full regularization ladder (cpals.py:78-88; one host sync
-per mode for the Cholesky flag).  Every later sweep is one CUDA-graph
-replay: a snapshot of (factors, Grams, lam), the d modes with a
-*speculative* rung-0 solve whose Cholesky flags stay on the device, and the
-fit terms; the only host sync per sweep is one 2 + d scalar readback (fit
-terms + flags) for the stopping rule (cpals.py:157).  If a flag shows a
-failed Cholesky, the snapshot is restored and that sweep reruns eagerly
-through the ladder, so the trajectory is the eager one either way.
+is not read by its MTTKRP) and solved in place.  Every sweep is
+speculative: a snapshot of (factors, Grams, lam), the d modes with a rung-0
+solve whose Cholesky flags stay on the device, and the fit terms; the only
+host sync per sweep is one 2 + d scalar readback (fit terms + flags) for
+the stopping rule (cpals.py:157).  If a flag shows a failed Cholesky, the
+snapshot is restored and that sweep reruns through the full regularization
+ladder (cpals.py:78-88; a host sync per mode), so the trajectory is the
+ladder's either way.  With ``graph`` sweeps 2.. are one CUDA-graph replay
+each (no per-launch host work at all).
 """
 
 from __future__ import annotations
@@ -198,7 +198,7 @@ def cp_als(y: DenseTensor, config: AlsConfig, graph: bool | None = None) -> tupl
         stats_host.copy_(stats, non_blocking=True)
         ev[d + 1].record()  # after the readback: waiting on it makes stats_host valid
 
-    saved = None
+    saved = [torch.empty_like(t) for t in factors + grams + [lam]]
     captured = None
 
     def snapshot():
@@ -213,13 +213,13 @@ def cp_als(y: DenseTensor, config: AlsConfig, graph: bool | None = None) -> tupl
     converged = False
     for it in range(config.max_iters):
         if it == 0 or not graph:
+            # eager: the same speculative sweep, one host sync per sweep
+            snapshot()
             info.zero_()
-            sweep(spec=False)
+            sweep(spec=True)
         else:
             if captured is None:
-                saved = [torch.empty_like(t) for t in factors + grams + [lam]]
                 keep = list(_device_workspaces(dev))  # captured pointers stay alive
-                info.zero_()
                 captured = torch.cuda.CUDAGraph()
                 side = torch.cuda.Stream(dev)
                 side.wait_stream(torch.cuda.current_stream(dev))
@@ -237,9 +237,9 @@ def cp_als(y: DenseTensor, config: AlsConfig, graph: bool | None = None) -> tupl
                 captured.keep = keep
             captured.replay()
         ev[d + 1].synchronize()
-        if it > 0 and graph and bool((stats_host[2:] != 0).any()):
+        if bool((stats_host[2:] != 0).any()):
             # a speculative Cholesky failed: roll the sweep back, rerun it
-            # through the ladder
+            # through the ladder (cpals.py:78-88)
             restore()
             info.zero_()
             sweep(spec=False)
