@@ -8,6 +8,8 @@
 #include <cusolverDn.h>
 
 #include <algorithm>
+#include <cstdlib>
+#include <cstring>
 #include <vector>
 
 namespace cpk {
@@ -134,18 +136,21 @@ __device__ double block_sum(double v, double* sh) {
   return r;
 }
 
-// out[0] = lam^T H lam  ((lam @ H) @ lam as cpals.py:146), out[1] = sum((G*lam)*A)
+// out[0] = lam^T H lam  (cpals.py:146 forms (lam @ H) @ lam), out[1] = sum((G*lam)*A)
 __global__ void __launch_bounds__(1024) fit_terms_kernel(const double* __restrict__ H,
                                                          const double* __restrict__ lam,
                                                          const double* __restrict__ G,
                                                          const double* __restrict__ A, int64_t rows,
                                                          int64_t R, double* __restrict__ out) {
   __shared__ double sh[1024];
+  // lam^T (H lam): warp a-rows, lanes stride the (coalesced) columns, so the
+  // loads are independent of the accumulation chain (H is symmetric)
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double s0 = 0.0;
-  for (int64_t b = threadIdx.x; b < R; b += 1024) {
+  for (int64_t a = warp; a < R; a += 32) {
     double v = 0.0;
-    for (int64_t a = 0; a < R; ++a) v = fma(lam[a], H[a * R + b], v);
-    s0 = fma(v, lam[b], s0);
+    for (int64_t b = lane; b < R; b += 32) v = fma(H[a * R + b], lam[b], v);
+    s0 = fma(lam[a], v, s0);
   }
   double s1 = 0.0;
   if (G && A)
@@ -195,6 +200,376 @@ __global__ void copy_regularize_kernel(const double* __restrict__ gamma, int64_t
     if (eps != 0.0 && idx / R == idx % R) v += shift;
     out[idx] = v;
   }
+}
+
+// ---------------------------------------------------------------- small-R Cholesky
+// For R <= CHOL_SMALL_MAX the normal-equation solve runs as two of our own
+// launches instead of cuSOLVER potrf + potrs (~20 latency-bound launches,
+// ~0.4 ms per mode at R = 256).  Same algorithm as cho_factor / cho_solve
+// (cpals.py:79-85): Gamma = L L^T, then X L L^T = G row by row; only the
+// blocking and the summation order differ.
+//
+// chol_small_kernel: one CTA, right-looking over 32-column blocks.  Warp 0
+// factors the diagonal block in registers (lane = row, shuffles carry the
+// pivot column), the CTA solves the panel below it against that block (one
+// thread per row), and 64-thread groups apply the symmetric rank-32 update
+// to the trailing lower triangle in 32 x 32 tiles (4 x 4 per thread).  The
+// matrix lives in the caller's workspace (L2-resident); the panel is staged
+// in shared memory for the update.  On exit the lower triangle holds L (the
+// upper triangle is not written).  info = 0, or the 1-based column whose
+// pivot was not positive (LAPACK's potrf convention).
+constexpr int CB = 32, CHOL_THREADS = 512;
+constexpr int CHOL_SMALL_MAX = 512;
+
+static size_t chol_smem(int64_t R) {
+  const int64_t np = std::max<int64_t>(0, R - CB);
+  return size_t(CB * 33 + ((np + CB - 1) / CB) * CB * 33) * sizeof(double);
+}
+
+__global__ void __launch_bounds__(CHOL_THREADS, 1) chol_small_kernel(const double* __restrict__ gamma, int R,
+                                                                     double eps, double* __restrict__ L,
+                                                                     int* __restrict__ info) {
+  extern __shared__ double csm[];
+  double* dg = csm;             // [32][33] the factored diagonal block
+  double* pan = csm + CB * 33;  // [round32(R - 32)][33] the solved panel
+  __shared__ double red[CHOL_THREADS / 32], rdg[CB];
+  __shared__ __align__(16) double colk[CB];
+  __shared__ int fail;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  double shift = 0.0;
+  if (eps != 0.0) {  // Gamma + (eps tr(Gamma) / R) I  (cpals.py:84)
+    double t = 0.0;
+    for (int i = tid; i < R; i += CHOL_THREADS) t += gamma[int64_t(i) * R + i];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) t += __shfl_down_sync(~0u, t, o);
+    if (lane == 0) red[warp] = t;
+    __syncthreads();
+    double tr = 0.0;
+    for (int w = 0; w < CHOL_THREADS / 32; ++w) tr += red[w];
+    shift = eps * tr / double(R);
+  }
+  // lower triangle of Gamma (+ shift) -> L; a warp per row, 8 loads in
+  // flight per thread (a plain copy loop would wait out the L2 latency on
+  // every element: this CTA is the whole grid)
+  for (int r = warp; r < R; r += CHOL_THREADS / 32) {
+    const double* src = gamma + int64_t(r) * R;
+    double* dst = L + int64_t(r) * R;
+    for (int c0 = 0; c0 <= r; c0 += 8 * 32) {
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int c = c0 + u * 32 + lane;
+        v[u] = c <= r ? src[c] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int c = c0 + u * 32 + lane;
+        if (c <= r) dst[c] = c == r ? v[u] + shift : v[u];
+      }
+    }
+  }
+  if (tid == 0) fail = 0;
+  __syncthreads();
+
+  const int nblk = (R + CB - 1) / CB;
+#pragma unroll 1
+  for (int j = 0; j < nblk; ++j) {
+    const int j0 = j * CB, bw = min(CB, R - j0);
+    if (warp == 0) {
+      // unblocked Cholesky of the diagonal block in registers: lane = row,
+      // a[c] = A[lane][c]; every loop is unrolled, so a[] never leaves the
+      // register file, and shuffles carry the pivot column
+      double a[CB];
+      const bool in = lane < bw;
+#pragma unroll
+      for (int c = 0; c < CB; ++c) a[c] = (in && c <= lane) ? L[int64_t(j0 + lane) * R + j0 + c] : 0.0;
+      int bad = 0;
+#pragma unroll
+      for (int k = 0; k < CB; ++k) {
+        if (k < bw && bad == 0) {  // warp-uniform
+          const double dkk = __shfl_sync(~0u, a[k], k);
+          if (!(dkk > 0.0)) {  // also catches NaN
+            bad = k + 1;
+          } else {
+            // potf2 scales the column by 1 / sqrt(pivot); rsqrt is one MUFU
+            // + Newton steps, shorter than sqrt then a reciprocal
+            const double rl = rsqrt(dkk);
+            a[k] = lane == k ? dkk * rl : (lane > k ? a[k] * rl : 0.0);
+            colk[lane] = a[k];  // column k, read back as broadcasts
+            __syncwarp();
+            // unpredicated: lanes < c only touch their (unused) upper entries
+#pragma unroll
+            for (int c = 1; c < CB; ++c) {  // constant trip count: unrolls fully
+              if (c <= k) continue;
+              a[c] = fma(-a[k], colk[c], a[c]);
+            }
+            __syncwarp();
+          }
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < CB; ++c) dg[lane * 33 + c] = a[c];
+      __syncwarp();
+      if (bad) {
+        if (lane == 0) fail = j0 + bad;
+      } else {
+#pragma unroll
+        for (int c = 0; c < CB; ++c)
+          if (in && c <= lane) L[int64_t(j0 + lane) * R + j0 + c] = a[c];
+        rdg[lane] = lane < bw ? 1.0 / dg[lane * 33 + lane] : 0.0;
+      }
+    }
+    __syncthreads();
+    if (fail) {
+      if (tid == 0) *info = fail;
+      return;
+    }
+    // panel rows p0..: X L_jj^T = A, solved in place in shared memory
+    const int p0 = j0 + CB, np = R - p0, npr = ((np + CB - 1) / CB) * CB;
+    for (int t0 = warp; t0 < npr; t0 += 8 * (CHOL_THREADS / 32)) {  // 8 rows in flight per warp
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int t = t0 + u * (CHOL_THREADS / 32);
+        v[u] = t < np ? L[int64_t(p0 + t) * R + j0 + lane] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int t = t0 + u * (CHOL_THREADS / 32);
+        if (t < npr) pan[t * 33 + lane] = v[u];
+      }
+    }
+    __syncthreads();
+    static_assert(CHOL_SMALL_MAX - CB <= CHOL_THREADS, "one panel row per thread");
+    if (tid < np) {  // not a loop: the dg reads would be hoisted and spill
+      const int t = tid;
+      double x[CB];  // fully unrolled: stays in registers
+#pragma unroll
+      for (int c = 0; c < CB; ++c) x[c] = pan[t * 33 + c];
+#pragma unroll
+      for (int c = 0; c < CB; ++c) {
+        double v = x[c];
+#pragma unroll
+        for (int u = 0; u < c; ++u) v = fma(-x[u], dg[c * 33 + u], v);
+        x[c] = v * rdg[c];
+      }
+#pragma unroll
+      for (int c = 0; c < CB; ++c) pan[t * 33 + c] = x[c];
+    }
+    __syncthreads();
+    for (int idx = tid; idx < np * CB; idx += CHOL_THREADS) {
+      const int t = idx >> 5, c = idx & 31;
+      L[int64_t(p0 + t) * R + j0 + c] = pan[t * 33 + c];
+    }
+    // trailing lower triangle -= P P^T, 32 x 32 tiles
+    const int nb2 = npr / CB, ntiles = nb2 * (nb2 + 1) / 2;
+    const int grp = tid >> 6, gl = tid & 63, ty = gl >> 3, tx = gl & 7;
+    for (int tile = grp; tile < ntiles; tile += CHOL_THREADS / 64) {
+      int bi = 0, bl = tile;
+      while (bl > bi) {
+        bl -= bi + 1;
+        ++bi;
+      }
+      const int r0 = bi * CB + ty * 4, c0 = bl * CB + tx * 4;
+      double acc[4][4] = {};
+#pragma unroll 8
+      for (int u = 0; u < CB; ++u) {
+        double pr[4], pc[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          pr[i] = pan[(r0 + i) * 33 + u];
+          pc[i] = pan[(c0 + i) * 33 + u];
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int jj = 0; jj < 4; ++jj) acc[i][jj] = fma(pr[i], pc[jj], acc[i][jj]);
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) {
+          const int rr = r0 + i, cc = c0 + jj;
+          if (rr < np && cc <= rr) L[int64_t(p0 + rr) * R + p0 + cc] -= acc[i][jj];
+        }
+    }
+    __syncthreads();
+  }
+  if (tid == 0) *info = 0;
+}
+
+// X L L^T = G for every row of G (rows x R, row-major, ld R), skipped when
+// *info != 0.  RW rows per warp, ROWS_WARPS warps per CTA; the rows live in
+// shared memory interleaved (z[c][q]), lane j owns column tb * 32 + j of the
+// current 32-column block.  Per block the CTA stages the 32-column strip of
+// L^T / L it needs (coalesced, all loads in flight at once), then each warp
+// runs the dot-product part from shared memory (RW independent chains per
+// strip element) and the sequential in-block substitution (shuffles).
+// Forward Z L^T = G needs L[t][u] (u < t), backward X L = Z needs L[c][t]
+// (c > t): both from the lower triangle.
+constexpr int ROWS_WARPS = 4, ROWS_RW = 4;
+
+static size_t rows_smem(int64_t R) {
+  const int64_t rp = (R + 31) / 32 * 32;
+  return size_t(rp * 33 + int64_t(ROWS_WARPS) * ROWS_RW * rp + 32) * sizeof(double);
+}
+
+__global__ void __launch_bounds__(ROWS_WARPS * 32) chol_rows_kernel(const double* __restrict__ LU, int R,
+                                                                    double* __restrict__ G, int64_t rows,
+                                                                    const int* __restrict__ info) {
+  if (*info != 0) return;
+  constexpr int RW = ROWS_RW;
+  extern __shared__ __align__(16) double rsm[];
+  const int rp = (R + 31) / 32 * 32;
+  double* strip = rsm;                                   // [rp][33]: the strip of block tb
+  double* zall = rsm + rp * 33;                          // [warp][rp][RW]
+  double* rdiag = zall + ROWS_WARPS * RW * rp;           // [32]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t q0 = (int64_t(blockIdx.x) * ROWS_WARPS + warp) * RW;
+  const bool active = q0 < rows;  // inactive warps still help stage strips
+  double* z = zall + int64_t(warp) * rp * RW;
+  for (int c = lane; c < rp; c += 32)
+#pragma unroll
+    for (int q = 0; q < RW; ++q) z[c * RW + q] = (active && q0 + q < rows && c < R) ? G[(q0 + q) * R + c] : 0.0;
+  const int nblk = rp / 32;
+  // Stage the strip of block tb: forward strip[u][t] = L[b0 + t][u]
+  // (u < b0 + 32), backward strip[c][t] = L[c][b0 + t] (c >= b0); lower
+  // triangle only (the upper is not written by chol_small), 8 loads in
+  // flight per thread, rows padded to 33 so both patterns are conflict-free.
+  auto stage = [&](int tb, bool fwd) {
+    __syncthreads();  // everyone is done with the previous strip
+    const int b0 = tb * 32;
+    if (fwd) {
+      const int nu = b0 + 32;
+      for (int e0 = 0; e0 < 32 * nu; e0 += 8 * ROWS_WARPS * 32) {
+        double v[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int e = e0 + i * ROWS_WARPS * 32 + threadIdx.x, t = e / nu, u = e - t * nu;
+          v[i] = (e < 32 * nu && b0 + t < R && u <= b0 + t) ? LU[int64_t(b0 + t) * R + u] : 0.0;
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int e = e0 + i * ROWS_WARPS * 32 + threadIdx.x, t = e / nu, u = e - t * nu;
+          if (e < 32 * nu) strip[u * 33 + t] = v[i];
+        }
+      }
+    } else {
+      const int nc = rp - b0;
+      for (int e0 = 0; e0 < 32 * nc; e0 += 8 * ROWS_WARPS * 32) {
+        double v[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int e = e0 + i * ROWS_WARPS * 32 + threadIdx.x, c = b0 + (e >> 5), t = e & 31;
+          v[i] = (e < 32 * nc && c < R && b0 + t < R && c >= b0 + t) ? LU[int64_t(c) * R + b0 + t] : 0.0;
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int e = e0 + i * ROWS_WARPS * 32 + threadIdx.x, c = b0 + (e >> 5), t = e & 31;
+          if (e < 32 * nc) strip[c * 33 + t] = v[i];
+        }
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      const int k = b0 + threadIdx.x;
+      rdiag[threadIdx.x] = k < R ? 1.0 / strip[k * 33 + threadIdx.x] : 0.0;
+    }
+    __syncthreads();
+  };
+  // forward: z_t = (g_t - sum_{u<t} z_u L[t][u]) / L[t][t]
+  for (int tb = 0; tb < nblk; ++tb) {
+    stage(tb, true);
+    if (!active) continue;
+    const int b0 = tb * 32, t = b0 + lane;
+    double acc[RW];
+#pragma unroll
+    for (int q = 0; q < RW; ++q) acc[q] = z[t * RW + q];
+#pragma unroll 8
+    for (int u = 0; u < b0; ++u) {
+      const double w = strip[u * 33 + lane];
+      const double4 zu = *reinterpret_cast<const double4*>(z + u * RW);
+      acc[0] = fma(-zu.x, w, acc[0]);
+      acc[1] = fma(-zu.y, w, acc[1]);
+      acc[2] = fma(-zu.z, w, acc[2]);
+      acc[3] = fma(-zu.w, w, acc[3]);
+    }
+    const int kmax = min(32, R - b0);
+    for (int k = 0; k < kmax; ++k) {
+      const double rd = rdiag[k];
+      const double w = lane > k ? strip[(b0 + k) * 33 + lane] : 0.0;  // L[t][k]
+#pragma unroll
+      for (int q = 0; q < RW; ++q) {
+        const double zk = __shfl_sync(~0u, acc[q], k) * rd;
+        acc[q] = lane == k ? zk : (lane > k ? fma(-zk, w, acc[q]) : acc[q]);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < RW; ++q) z[t * RW + q] = acc[q];
+    __syncwarp();
+  }
+  // backward: x_t = (z_t - sum_{c>t} x_c L[c][t]) / L[t][t]
+  for (int tb = nblk - 1; tb >= 0; --tb) {
+    stage(tb, false);
+    if (!active) continue;
+    const int b0 = tb * 32, t = b0 + lane;
+    double acc[RW];
+#pragma unroll
+    for (int q = 0; q < RW; ++q) acc[q] = z[t * RW + q];
+#pragma unroll 8
+    for (int c = b0 + 32; c < R; ++c) {
+      const double w = strip[c * 33 + lane];
+      const double4 zc = *reinterpret_cast<const double4*>(z + c * RW);
+      acc[0] = fma(-zc.x, w, acc[0]);
+      acc[1] = fma(-zc.y, w, acc[1]);
+      acc[2] = fma(-zc.z, w, acc[2]);
+      acc[3] = fma(-zc.w, w, acc[3]);
+    }
+    const int kmax = min(32, R - b0);
+    for (int k = kmax - 1; k >= 0; --k) {
+      const double rd = rdiag[k];
+      const double w = lane < k ? strip[(b0 + k) * 33 + lane] : 0.0;  // L[k][t], t < k
+#pragma unroll
+      for (int q = 0; q < RW; ++q) {
+        const double xk = __shfl_sync(~0u, acc[q], k) * rd;
+        acc[q] = lane == k ? xk : (lane < k ? fma(-xk, w, acc[q]) : acc[q]);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < RW; ++q) z[t * RW + q] = acc[q];
+    __syncwarp();
+  }
+  if (!active) return;
+  for (int c = lane; c < R; c += 32)
+#pragma unroll
+    for (int q = 0; q < RW; ++q)
+      if (q0 + q < rows) G[(q0 + q) * R + c] = z[c * RW + q];
+}
+
+// CPK_SOLVE=cusolver forces the library path (A/B comparisons and tests)
+static bool use_small_chol(int64_t R) {
+  if (R > CHOL_SMALL_MAX) return false;
+  const char* e = getenv("CPK_SOLVE");
+  return !(e && strcmp(e, "cusolver") == 0);
+}
+
+static int chol_small(const double* gamma, int64_t R, double eps, double* L, int* info, cudaStream_t st) {
+  const cudaError_t attr = cudaFuncSetAttribute(chol_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                int(chol_smem(CHOL_SMALL_MAX)));
+  if (attr != cudaSuccess) return fail(CPK_ERR_CUDA, "chol smem attribute: %s", cudaGetErrorString(attr));
+  chol_small_kernel<<<1, CHOL_THREADS, chol_smem(R), st>>>(gamma, int(R), eps, L, info);
+  return check_launch("chol_small");
+}
+
+static int chol_rows(const double* LU, int64_t R, double* G, int64_t rows, const int* info, cudaStream_t st) {
+  if (rows <= 0) return CPK_OK;
+  const size_t smem = rows_smem(R);
+  if (cudaFuncSetAttribute(chol_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           int(rows_smem(CHOL_SMALL_MAX))) != cudaSuccess)
+    return check_launch("chol_rows smem attribute");
+  const unsigned grid = unsigned((rows + ROWS_WARPS * ROWS_RW - 1) / (ROWS_WARPS * ROWS_RW));
+  chol_rows_kernel<<<grid, ROWS_WARPS * 32, smem, st>>>(LU, int(R), G, rows, info);
+  return check_launch("chol_rows");
 }
 
 struct SolverCtx {
@@ -336,7 +711,19 @@ extern "C" int cpk_solve_normal_f64(const double* gamma, double* G, int64_t rows
   const unsigned cblocks = unsigned(std::min<int64_t>((rank * rank + 255) / 256, 148 * 4));
   // Rung 0 is the plain Cholesky; rungs 1..5 add eps tr/R I, eps = 1e-12 * 1e3^i
   double eps = 0.0;
+  const bool small = use_small_chol(rank);
   for (int rung = 0; rung <= 5; ++rung) {
+    if (small) {
+      rc = chol_small(gamma, rank, eps, L, info_d, st);
+      if (rc) return rc;
+      int info = 0;
+      if (cudaMemcpyAsync(&info, info_d, sizeof(int), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+          cudaStreamSynchronize(st) != cudaSuccess)
+        return fail(CPK_ERR_CUDA, "chol info readback failed");
+      if (info == 0) return chol_rows(L, rank, G, rows, info_d, st);
+      eps = rung == 0 ? 1e-12 : eps * 1e3;
+      continue;
+    }
     copy_regularize_kernel<<<std::max(cblocks, 1u), 256, 0, st>>>(gamma, rank, eps, L);
     rc = check_launch("copy_regularize");
     if (rc) return rc;
@@ -379,6 +766,11 @@ extern "C" int cpk_solve_normal_spec_f64(const double* gamma, double* G, int64_t
   double* L = reinterpret_cast<double*>(base);
   double* w = reinterpret_cast<double*>(base + off_w);
   int* info_d = reinterpret_cast<int*>(base + off_info);
+  if (use_small_chol(rank)) {
+    rc = chol_small(gamma, rank, 0.0, L, info_out, st);
+    if (rc) return rc;
+    return chol_rows(L, rank, G, rows, info_out, st);
+  }
   const unsigned cblocks = unsigned(std::min<int64_t>((rank * rank + 255) / 256, 148 * 4));
   copy_regularize_kernel<<<std::max(cblocks, 1u), 256, 0, st>>>(gamma, rank, 0.0, L);
   rc = check_launch("copy_regularize");

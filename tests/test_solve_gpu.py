@@ -1,0 +1,125 @@
+"""The CP-ALS normal-equation solve X Gamma = G (cpals._solve_normal,
+cpals.py:75-89) on the device: the small-rank Cholesky kernels (R <= 512,
+csrc/als.cu chol_small_kernel / chol_rows_kernel) and the cuSOLVER path
+(CPK_SOLVE=cusolver) against the oracle's scipy cho_factor / cho_solve.
+
+Bar: relative Frobenius error <= 1e-10 on well-conditioned Gamma (observed
+~1e-14); the non-positive-definite pivot flag matches LAPACK's column.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import oracle
+from paper_2510_14891_b200 import cpals
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-10
+
+
+def spd(r, rng, cond_shift=0.5):
+    a = rng.standard_normal((max(2 * r, 4), r))
+    return a.T @ a + cond_shift * np.eye(r)
+
+
+def run_spec(gamma, g):
+    dev = torch.device("cuda", 0)
+    gam = torch.from_numpy(gamma).to(dev)
+    gt = torch.from_numpy(np.ascontiguousarray(g)).to(dev)
+    info = torch.zeros(1, dtype=torch.int32, device=dev)
+    solver = cpals._Solver(dev, max(g.shape[0], 1), gamma.shape[0])
+    cpals._solve_spec(solver, gam, gt, info)
+    torch.cuda.synchronize()
+    return gt.cpu().numpy(), int(info.item())
+
+
+def run_ladder(gamma, g):
+    dev = torch.device("cuda", 0)
+    gam = torch.from_numpy(gamma).to(dev)
+    gt = torch.from_numpy(np.ascontiguousarray(g)).to(dev)
+    solver = cpals._Solver(dev, max(g.shape[0], 1), gamma.shape[0])
+    x = solver(gam, gt)
+    torch.cuda.synchronize()
+    return x.cpu().numpy()
+
+
+@pytest.mark.parametrize("path", ["kernel", "cusolver"])
+@pytest.mark.parametrize("r", [1, 5, 31, 32, 33, 64, 100, 256, 300, 512])
+def test_spd_solve_matches_cho_solve(monkeypatch, path, r):
+    if path == "cusolver":
+        monkeypatch.setenv("CPK_SOLVE", "cusolver")
+    else:
+        monkeypatch.delenv("CPK_SOLVE", raising=False)
+    rng = np.random.Generator(np.random.Philox(r))
+    gamma = spd(r, rng)
+    for rows in (1, 7, 33, 128, 1000):
+        g = rng.standard_normal((rows, r))
+        want = oracle._solve_normal(gamma, g)
+        got, info = run_spec(gamma, g)
+        assert info == 0
+        err = np.linalg.norm(got - want) / np.linalg.norm(want)
+        assert err <= TOL, (path, r, rows, err)
+        got2 = run_ladder(gamma, g)
+        err2 = np.linalg.norm(got2 - want) / np.linalg.norm(want)
+        assert err2 <= TOL, (path, r, rows, err2)
+
+
+def test_kernel_and_cusolver_agree_on_a_cp_als_gamma(monkeypatch):
+    # a Hadamard product of Grams, as the sweep builds it (cond ~1e4)
+    rng = np.random.Generator(np.random.Philox(7))
+    r = 256
+    grams = [(lambda a: a.T @ a)(rng.random((128, r))) for _ in range(3)]
+    gamma = grams[0] * grams[1] * grams[2]
+    g = rng.random((128, r))
+    monkeypatch.delenv("CPK_SOLVE", raising=False)
+    x_kernel, info = run_spec(gamma, g)
+    assert info == 0
+    monkeypatch.setenv("CPK_SOLVE", "cusolver")
+    x_lib, info = run_spec(gamma, g)
+    assert info == 0
+    want = oracle._solve_normal(gamma, g)
+    scale = np.linalg.norm(want)
+    assert np.linalg.norm(x_kernel - want) / scale <= TOL
+    assert np.linalg.norm(x_kernel - x_lib) / scale <= TOL
+
+
+@pytest.mark.parametrize("r,bad", [(1, 0), (40, 17), (256, 100), (256, 255)])
+def test_not_positive_definite_flags_the_lapack_column(monkeypatch, r, bad):
+    monkeypatch.delenv("CPK_SOLVE", raising=False)
+    gamma = np.eye(r) * 2.0
+    gamma[bad, bad] = -1.0
+    g = np.ones((5, r))
+    _, info = run_spec(gamma, g)
+    assert info == bad + 1  # potrf's 1-based column of the failed pivot
+    # the ladder cannot fix a negative eigenvalue either: last rung = lstsq
+    x = run_ladder(gamma, g)
+    want = oracle._solve_normal(gamma, g)
+    assert np.allclose(x, want, rtol=1e-12, atol=1e-12)
+
+
+def test_nan_gamma_is_flagged(monkeypatch):
+    monkeypatch.delenv("CPK_SOLVE", raising=False)
+    gamma = np.eye(8)
+    gamma[3, 3] = np.nan
+    _, info = run_spec(gamma, np.ones((2, 8)))
+    assert info == 4
+
+
+def test_singular_gamma_takes_a_regularized_rung(monkeypatch):
+    # PSD Gamma with an exactly zero block (zero factor columns): rung 0 hits
+    # a zero pivot, rung 1 (eps = 1e-12) succeeds; the blocks decouple, so
+    # each is compared on its own scale
+    monkeypatch.delenv("CPK_SOLVE", raising=False)
+    rng = np.random.Generator(np.random.Philox(3))
+    a = rng.standard_normal((100, 64))
+    a[:, 20:] = 0.0
+    gamma = a.T @ a
+    g = rng.standard_normal((9, 64))
+    _, info = run_spec(gamma, g)
+    assert info == 21
+    x = run_ladder(gamma, g)
+    want = oracle._solve_normal(gamma, g)
+    for blk in (slice(0, 20), slice(20, 64)):
+        err = np.linalg.norm(x[:, blk] - want[:, blk]) / np.linalg.norm(want[:, blk])
+        assert err <= TOL, (blk, err)
