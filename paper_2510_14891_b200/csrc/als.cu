@@ -204,8 +204,7 @@ __global__ void copy_regularize_kernel(const double* __restrict__ gamma, int64_t
 
 // ---------------------------------------------------------------- small-R Cholesky
 // For R <= CHOL_SMALL_MAX the normal-equation solve runs as two of our own
-// launches instead of cuSOLVER potrf + potrs (~20 latency-bound launches,
-// ~0.4 ms per mode at R = 256).  Same algorithm as cho_factor / cho_solve
+// launches instead of cuSOLVER potrf + potrs (~20 latency-bound launches).  Same algorithm as cho_factor / cho_solve
 // (cpals.py:79-85): Gamma = L L^T, then X L L^T = G row by row; only the
 // blocking and the summation order differ.
 //
@@ -215,11 +214,17 @@ __global__ void copy_regularize_kernel(const double* __restrict__ gamma, int64_t
 // thread per row), and 64-thread groups apply the symmetric rank-32 update
 // to the trailing lower triangle in 32 x 32 tiles (4 x 4 per thread).  The
 // matrix lives in the caller's workspace (L2-resident); the panel is staged
-// in shared memory for the update.  On exit the lower triangle holds L (the
-// upper triangle is not written).  info = 0, or the 1-based column whose
-// pivot was not positive (LAPACK's potrf convention).
+// in shared memory for the update.  On exit the lower triangle holds L and
+// the upper triangle of each 32 x 32 diagonal block the transposed strictly
+// lower part of that block's inverse (for chol_rows); the rest of the upper
+// triangle is not written.  info = 0, or the 1-based column whose pivot was
+// not positive (LAPACK's potrf convention).
 constexpr int CB = 32, CHOL_THREADS = 512;
-constexpr int CHOL_SMALL_MAX = 512;
+// The kernels handle R <= CHOL_KERNEL_CAP; by default they replace cuSOLVER
+// up to CHOL_SMALL_MAX, where they stop winning (single CTA: the trailing
+// updates grow as R^3).  tools/solve_bench.py, B200: R = 32 19 vs 40 us,
+// 64 35 vs 79, 128 84 vs 172, 256 271 vs 362, 384 633 vs 554.
+constexpr int CHOL_KERNEL_CAP = 512, CHOL_SMALL_MAX = 256;
 
 static size_t chol_smem(int64_t R) {
   const int64_t np = std::max<int64_t>(0, R - CB);
@@ -340,7 +345,24 @@ __global__ void __launch_bounds__(CHOL_THREADS, 1) chol_small_kernel(const doubl
       }
     }
     __syncthreads();
-    static_assert(CHOL_SMALL_MAX - CB <= CHOL_THREADS, "one panel row per thread");
+    static_assert(CHOL_KERNEL_CAP - CB <= CHOL_THREADS - 32, "one panel row per thread, last warp free");
+    if (warp == CHOL_THREADS / 32 - 1) {
+      // meanwhile the last warp inverts the diagonal block for the row
+      // solve: lane j = column j of L_bb^-1 (forward substitution on e_j);
+      // its strictly-lower part goes, transposed, into the unused upper
+      // triangle of the block: L[j0 + j][j0 + i] = (L_bb^-1)[i][j], i > j
+      double x[CB];
+#pragma unroll
+      for (int i = 0; i < CB; ++i) {
+        double v = i == lane ? 1.0 : 0.0;
+#pragma unroll
+        for (int u = 0; u < i; ++u) v = fma(-dg[i * 33 + u], x[u], v);  // x[u] = 0 for u < lane
+        x[i] = i >= lane ? v * rdg[i] : 0.0;
+      }
+#pragma unroll
+      for (int i = 0; i < CB; ++i)
+        if (i > lane && i < bw) L[int64_t(j0 + lane) * R + j0 + i] = x[i];
+    }
     if (tid < np) {  // not a loop: the dg reads would be hoisted and spill
       const int t = tid;
       double x[CB];  // fully unrolled: stays in registers
@@ -402,16 +424,17 @@ __global__ void __launch_bounds__(CHOL_THREADS, 1) chol_small_kernel(const doubl
 // *info != 0.  RW rows per warp, ROWS_WARPS warps per CTA; the rows live in
 // shared memory interleaved (z[c][q]), lane j owns column tb * 32 + j of the
 // current 32-column block.  Per block the CTA stages the 32-column strip of
-// L^T / L it needs (coalesced, all loads in flight at once), then each warp
-// runs the dot-product part from shared memory (RW independent chains per
-// strip element) and the sequential in-block substitution (shuffles).
+// L it needs (coalesced, 8 loads in flight per thread) and the block's
+// inverse (chol_small leaves it in the upper triangle), then each warp runs
+// the dot-product part from shared memory (RW independent chains per strip
+// element) and the in-block solve as a 32 x 32 GEMV with the inverse.
 // Forward Z L^T = G needs L[t][u] (u < t), backward X L = Z needs L[c][t]
 // (c > t): both from the lower triangle.
 constexpr int ROWS_WARPS = 4, ROWS_RW = 4;
 
 static size_t rows_smem(int64_t R) {
   const int64_t rp = (R + 31) / 32 * 32;
-  return size_t(rp * 33 + int64_t(ROWS_WARPS) * ROWS_RW * rp + 32) * sizeof(double);
+  return size_t(rp * 33 + int64_t(ROWS_WARPS) * ROWS_RW * rp + 32 + 32 * 33) * sizeof(double);
 }
 
 __global__ void __launch_bounds__(ROWS_WARPS * 32) chol_rows_kernel(const double* __restrict__ LU, int R,
@@ -424,6 +447,7 @@ __global__ void __launch_bounds__(ROWS_WARPS * 32) chol_rows_kernel(const double
   double* strip = rsm;                                   // [rp][33]: the strip of block tb
   double* zall = rsm + rp * 33;                          // [warp][rp][RW]
   double* rdiag = zall + ROWS_WARPS * RW * rp;           // [32]
+  double* dblk = rdiag + 32;                             // [32][33]: dblk[a][b] = (L_bb^-1)[b][a], a < b
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t q0 = (int64_t(blockIdx.x) * ROWS_WARPS + warp) * RW;
   const bool active = q0 < rows;  // inactive warps still help stage strips
@@ -446,12 +470,15 @@ __global__ void __launch_bounds__(ROWS_WARPS * 32) chol_rows_kernel(const double
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
           const int e = e0 + i * ROWS_WARPS * 32 + threadIdx.x, t = e / nu, u = e - t * nu;
-          v[i] = (e < 32 * nu && b0 + t < R && u <= b0 + t) ? LU[int64_t(b0 + t) * R + u] : 0.0;
+          v[i] = (e < 32 * nu && b0 + t < R && u < R) ? LU[int64_t(b0 + t) * R + u] : 0.0;
         }
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
           const int e = e0 + i * ROWS_WARPS * 32 + threadIdx.x, t = e / nu, u = e - t * nu;
-          if (e < 32 * nu) strip[u * 33 + t] = v[i];
+          if (e < 32 * nu) {
+            strip[u * 33 + t] = u <= b0 + t ? v[i] : 0.0;
+            if (u > b0 + t) dblk[t * 33 + (u - b0)] = v[i];  // (L_bb^-1)[u][t]
+          }
         }
       }
     } else {
@@ -461,12 +488,15 @@ __global__ void __launch_bounds__(ROWS_WARPS * 32) chol_rows_kernel(const double
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
           const int e = e0 + i * ROWS_WARPS * 32 + threadIdx.x, c = b0 + (e >> 5), t = e & 31;
-          v[i] = (e < 32 * nc && c < R && b0 + t < R && c >= b0 + t) ? LU[int64_t(c) * R + b0 + t] : 0.0;
+          v[i] = (e < 32 * nc && c < R && b0 + t < R) ? LU[int64_t(c) * R + b0 + t] : 0.0;
         }
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
           const int e = e0 + i * ROWS_WARPS * 32 + threadIdx.x, c = b0 + (e >> 5), t = e & 31;
-          if (e < 32 * nc) strip[c * 33 + t] = v[i];
+          if (e < 32 * nc) {
+            strip[c * 33 + t] = c >= b0 + t ? v[i] : 0.0;
+            if (c < b0 + t) dblk[(c - b0) * 33 + t] = v[i];  // (L_bb^-1)[t][c - b0]
+          }
         }
       }
     }
@@ -494,16 +524,23 @@ __global__ void __launch_bounds__(ROWS_WARPS * 32) chol_rows_kernel(const double
       acc[2] = fma(-zu.z, w, acc[2]);
       acc[3] = fma(-zu.w, w, acc[3]);
     }
-    const int kmax = min(32, R - b0);
-    for (int k = 0; k < kmax; ++k) {
-      const double rd = rdiag[k];
-      const double w = lane > k ? strip[(b0 + k) * 33 + lane] : 0.0;  // L[t][k]
+    // in-block: z_b = L_bb^-1 rhs_b (a 32 x 32 GEMV, no sequential chain)
 #pragma unroll
-      for (int q = 0; q < RW; ++q) {
-        const double zk = __shfl_sync(~0u, acc[q], k) * rd;
-        acc[q] = lane == k ? zk : (lane > k ? fma(-zk, w, acc[q]) : acc[q]);
-      }
+    for (int q = 0; q < RW; ++q) z[t * RW + q] = acc[q];
+    __syncwarp();
+    const double rd = rdiag[lane];
+#pragma unroll
+    for (int q = 0; q < RW; ++q) acc[q] *= rd;
+#pragma unroll
+    for (int u = 0; u < 31; ++u) {
+      const double w = u < lane ? dblk[u * 33 + lane] : 0.0;  // (L_bb^-1)[t][u]
+      const double4 zu = *reinterpret_cast<const double4*>(z + (b0 + u) * RW);
+      acc[0] = fma(w, zu.x, acc[0]);
+      acc[1] = fma(w, zu.y, acc[1]);
+      acc[2] = fma(w, zu.z, acc[2]);
+      acc[3] = fma(w, zu.w, acc[3]);
     }
+    __syncwarp();
 #pragma unroll
     for (int q = 0; q < RW; ++q) z[t * RW + q] = acc[q];
     __syncwarp();
@@ -525,16 +562,23 @@ __global__ void __launch_bounds__(ROWS_WARPS * 32) chol_rows_kernel(const double
       acc[2] = fma(-zc.z, w, acc[2]);
       acc[3] = fma(-zc.w, w, acc[3]);
     }
-    const int kmax = min(32, R - b0);
-    for (int k = kmax - 1; k >= 0; --k) {
-      const double rd = rdiag[k];
-      const double w = lane < k ? strip[(b0 + k) * 33 + lane] : 0.0;  // L[k][t], t < k
+    // in-block: x_b = rhs_b L_bb^-1, x_t = sum_{u >= t} rhs_u (L_bb^-1)[u][t]
 #pragma unroll
-      for (int q = 0; q < RW; ++q) {
-        const double xk = __shfl_sync(~0u, acc[q], k) * rd;
-        acc[q] = lane == k ? xk : (lane < k ? fma(-xk, w, acc[q]) : acc[q]);
-      }
+    for (int q = 0; q < RW; ++q) z[t * RW + q] = acc[q];
+    __syncwarp();
+    const double rd = rdiag[lane];
+#pragma unroll
+    for (int q = 0; q < RW; ++q) acc[q] *= rd;
+#pragma unroll
+    for (int u = 1; u < 32; ++u) {
+      const double w = u > lane ? dblk[lane * 33 + u] : 0.0;  // (L_bb^-1)[u][t]
+      const double4 zu = *reinterpret_cast<const double4*>(z + (b0 + u) * RW);
+      acc[0] = fma(w, zu.x, acc[0]);
+      acc[1] = fma(w, zu.y, acc[1]);
+      acc[2] = fma(w, zu.z, acc[2]);
+      acc[3] = fma(w, zu.w, acc[3]);
     }
+    __syncwarp();
 #pragma unroll
     for (int q = 0; q < RW; ++q) z[t * RW + q] = acc[q];
     __syncwarp();
@@ -546,16 +590,18 @@ __global__ void __launch_bounds__(ROWS_WARPS * 32) chol_rows_kernel(const double
       if (q0 + q < rows) G[(q0 + q) * R + c] = z[c * RW + q];
 }
 
-// CPK_SOLVE=cusolver forces the library path (A/B comparisons and tests)
+// CPK_SOLVE=cusolver / =kernel force one path (A/B comparisons and tests)
 static bool use_small_chol(int64_t R) {
-  if (R > CHOL_SMALL_MAX) return false;
+  if (R > CHOL_KERNEL_CAP) return false;
   const char* e = getenv("CPK_SOLVE");
-  return !(e && strcmp(e, "cusolver") == 0);
+  if (e && strcmp(e, "cusolver") == 0) return false;
+  if (e && strcmp(e, "kernel") == 0) return true;
+  return R <= CHOL_SMALL_MAX;
 }
 
 static int chol_small(const double* gamma, int64_t R, double eps, double* L, int* info, cudaStream_t st) {
   const cudaError_t attr = cudaFuncSetAttribute(chol_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                int(chol_smem(CHOL_SMALL_MAX)));
+                                                int(chol_smem(CHOL_KERNEL_CAP)));
   if (attr != cudaSuccess) return fail(CPK_ERR_CUDA, "chol smem attribute: %s", cudaGetErrorString(attr));
   chol_small_kernel<<<1, CHOL_THREADS, chol_smem(R), st>>>(gamma, int(R), eps, L, info);
   return check_launch("chol_small");
@@ -565,7 +611,7 @@ static int chol_rows(const double* LU, int64_t R, double* G, int64_t rows, const
   if (rows <= 0) return CPK_OK;
   const size_t smem = rows_smem(R);
   if (cudaFuncSetAttribute(chol_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           int(rows_smem(CHOL_SMALL_MAX))) != cudaSuccess)
+                           int(rows_smem(CHOL_KERNEL_CAP))) != cudaSuccess)
     return check_launch("chol_rows smem attribute");
   const unsigned grid = unsigned((rows + ROWS_WARPS * ROWS_RW - 1) / (ROWS_WARPS * ROWS_RW));
   chol_rows_kernel<<<grid, ROWS_WARPS * 32, smem, st>>>(LU, int(R), G, rows, info);

@@ -1,7 +1,8 @@
 """The CP-ALS normal-equation solve X Gamma = G (cpals._solve_normal,
 cpals.py:75-89) on the device: the small-rank Cholesky kernels (R <= 512,
 csrc/als.cu chol_small_kernel / chol_rows_kernel) and the cuSOLVER path
-(CPK_SOLVE=cusolver) against the oracle's scipy cho_factor / cho_solve.
+(CPK_SOLVE=cusolver; CPK_SOLVE=kernel forces the kernels up to R = 512)
+against the oracle's scipy cho_factor / cho_solve.
 
 Bar: relative Frobenius error <= 1e-10 on well-conditioned Gamma (observed
 ~1e-14); the non-positive-definite pivot flag matches LAPACK's column.
@@ -47,10 +48,7 @@ def run_ladder(gamma, g):
 @pytest.mark.parametrize("path", ["kernel", "cusolver"])
 @pytest.mark.parametrize("r", [1, 5, 31, 32, 33, 64, 100, 256, 300, 512])
 def test_spd_solve_matches_cho_solve(monkeypatch, path, r):
-    if path == "cusolver":
-        monkeypatch.setenv("CPK_SOLVE", "cusolver")
-    else:
-        monkeypatch.delenv("CPK_SOLVE", raising=False)
+    monkeypatch.setenv("CPK_SOLVE", path)  # force the path (default: kernel for R <= 256)
     rng = np.random.Generator(np.random.Philox(r))
     gamma = spd(r, rng)
     for rows in (1, 7, 33, 128, 1000):
@@ -65,14 +63,14 @@ def test_spd_solve_matches_cho_solve(monkeypatch, path, r):
         assert err2 <= TOL, (path, r, rows, err2)
 
 
-def test_kernel_and_cusolver_agree_on_a_cp_als_gamma(monkeypatch):
+@pytest.mark.parametrize("r", [256, 512])
+def test_kernel_and_cusolver_agree_on_a_cp_als_gamma(monkeypatch, r):
     # a Hadamard product of Grams, as the sweep builds it (cond ~1e4)
     rng = np.random.Generator(np.random.Philox(7))
-    r = 256
     grams = [(lambda a: a.T @ a)(rng.random((128, r))) for _ in range(3)]
     gamma = grams[0] * grams[1] * grams[2]
     g = rng.random((128, r))
-    monkeypatch.delenv("CPK_SOLVE", raising=False)
+    monkeypatch.setenv("CPK_SOLVE", "kernel")
     x_kernel, info = run_spec(gamma, g)
     assert info == 0
     monkeypatch.setenv("CPK_SOLVE", "cusolver")
@@ -84,9 +82,9 @@ def test_kernel_and_cusolver_agree_on_a_cp_als_gamma(monkeypatch):
     assert np.linalg.norm(x_kernel - x_lib) / scale <= TOL
 
 
-@pytest.mark.parametrize("r,bad", [(1, 0), (40, 17), (256, 100), (256, 255)])
+@pytest.mark.parametrize("r,bad", [(1, 0), (40, 17), (256, 100), (256, 255), (500, 480)])
 def test_not_positive_definite_flags_the_lapack_column(monkeypatch, r, bad):
-    monkeypatch.delenv("CPK_SOLVE", raising=False)
+    monkeypatch.setenv("CPK_SOLVE", "kernel")
     gamma = np.eye(r) * 2.0
     gamma[bad, bad] = -1.0
     g = np.ones((5, r))

@@ -29,10 +29,7 @@ for r in a.ranks:
         g0 = torch.from_numpy(rng.random((rows, r))).to(dev)
         out = {"rank": r, "rows": rows}
         for path in ("kernel", "cusolver"):
-            if path == "cusolver":
-                os.environ["CPK_SOLVE"] = "cusolver"
-            else:
-                os.environ.pop("CPK_SOLVE", None)
+            os.environ["CPK_SOLVE"] = path
             solver = cpals._Solver(dev, rows, r)
             info = torch.zeros(1, dtype=torch.int32, device=dev)
             g = g0.clone()
