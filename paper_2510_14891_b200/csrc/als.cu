@@ -253,26 +253,8 @@ __global__ void __launch_bounds__(CHOL_THREADS, 1) chol_small_kernel(const doubl
     for (int w = 0; w < CHOL_THREADS / 32; ++w) tr += red[w];
     shift = eps * tr / double(R);
   }
-  // lower triangle of Gamma (+ shift) -> L; a warp per row, 8 loads in
-  // flight per thread (a plain copy loop would wait out the L2 latency on
-  // every element: this CTA is the whole grid)
-  for (int r = warp; r < R; r += CHOL_THREADS / 32) {
-    const double* src = gamma + int64_t(r) * R;
-    double* dst = L + int64_t(r) * R;
-    for (int c0 = 0; c0 <= r; c0 += 8 * 32) {
-      double v[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int c = c0 + u * 32 + lane;
-        v[u] = c <= r ? src[c] : 0.0;
-      }
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int c = c0 + u * 32 + lane;
-        if (c <= r) dst[c] = c == r ? v[u] + shift : v[u];
-      }
-    }
-  }
+  // no copy of Gamma: step 0 reads Gamma (+ shift on the diagonal) wherever
+  // later steps read L, and every lower element is written by step 0
   if (tid == 0) fail = 0;
   __syncthreads();
 
@@ -280,6 +262,8 @@ __global__ void __launch_bounds__(CHOL_THREADS, 1) chol_small_kernel(const doubl
 #pragma unroll 1
   for (int j = 0; j < nblk; ++j) {
     const int j0 = j * CB, bw = min(CB, R - j0);
+    const double* src = j == 0 ? gamma : L;
+    const double dshift = j == 0 ? shift : 0.0;
     if (warp == 0) {
       // unblocked Cholesky of the diagonal block in registers: lane = row,
       // a[c] = A[lane][c]; every loop is unrolled, so a[] never leaves the
@@ -287,7 +271,8 @@ __global__ void __launch_bounds__(CHOL_THREADS, 1) chol_small_kernel(const doubl
       double a[CB];
       const bool in = lane < bw;
 #pragma unroll
-      for (int c = 0; c < CB; ++c) a[c] = (in && c <= lane) ? L[int64_t(j0 + lane) * R + j0 + c] : 0.0;
+      for (int c = 0; c < CB; ++c)
+        a[c] = (in && c <= lane) ? src[int64_t(j0 + lane) * R + j0 + c] + (c == lane ? dshift : 0.0) : 0.0;
       int bad = 0;
 #pragma unroll
       for (int k = 0; k < CB; ++k) {
@@ -336,7 +321,7 @@ __global__ void __launch_bounds__(CHOL_THREADS, 1) chol_small_kernel(const doubl
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
         const int t = t0 + u * (CHOL_THREADS / 32);
-        v[u] = t < np ? L[int64_t(p0 + t) * R + j0 + lane] : 0.0;
+        v[u] = t < np ? src[int64_t(p0 + t) * R + j0 + lane] : 0.0;
       }
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
@@ -393,7 +378,14 @@ __global__ void __launch_bounds__(CHOL_THREADS, 1) chol_small_kernel(const doubl
         ++bi;
       }
       const int r0 = bi * CB + ty * 4, c0 = bl * CB + tx * 4;
-      double acc[4][4] = {};
+      double acc[4][4];  // starts as the old values, loaded before the products
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) {
+          const int rr = r0 + i, cc = c0 + jj;
+          acc[i][jj] = (rr < np && cc <= rr) ? src[int64_t(p0 + rr) * R + p0 + cc] + (rr == cc ? dshift : 0.0) : 0.0;
+        }
 #pragma unroll 8
       for (int u = 0; u < CB; ++u) {
         double pr[4], pc[4];
@@ -405,14 +397,14 @@ __global__ void __launch_bounds__(CHOL_THREADS, 1) chol_small_kernel(const doubl
 #pragma unroll
         for (int i = 0; i < 4; ++i)
 #pragma unroll
-          for (int jj = 0; jj < 4; ++jj) acc[i][jj] = fma(pr[i], pc[jj], acc[i][jj]);
+          for (int jj = 0; jj < 4; ++jj) acc[i][jj] = fma(-pr[i], pc[jj], acc[i][jj]);
       }
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
         for (int jj = 0; jj < 4; ++jj) {
           const int rr = r0 + i, cc = c0 + jj;
-          if (rr < np && cc <= rr) L[int64_t(p0 + rr) * R + p0 + cc] -= acc[i][jj];
+          if (rr < np && cc <= rr) L[int64_t(p0 + rr) * R + p0 + cc] = acc[i][jj];
         }
     }
     __syncthreads();
@@ -463,40 +455,36 @@ __global__ void __launch_bounds__(ROWS_WARPS * 32) chol_rows_kernel(const double
   auto stage = [&](int tb, bool fwd) {
     __syncthreads();  // everyone is done with the previous strip
     const int b0 = tb * 32;
-    if (fwd) {
-      const int nu = b0 + 32;
-      for (int e0 = 0; e0 < 32 * nu; e0 += 8 * ROWS_WARPS * 32) {
-        double v[8];
+    constexpr int RPW = 32 / ROWS_WARPS;  // strip rows per warp and 32-row slab
+    if (fwd) {  // rows b0 + t of L, columns u < b0 + 32 (lanes along u)
+      for (int u0 = 0; u0 < b0 + 32; u0 += 32) {
+        const int u = u0 + lane;
+        double v[RPW];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int e = e0 + i * ROWS_WARPS * 32 + threadIdx.x, t = e / nu, u = e - t * nu;
-          v[i] = (e < 32 * nu && b0 + t < R && u < R) ? LU[int64_t(b0 + t) * R + u] : 0.0;
+        for (int i = 0; i < RPW; ++i) {
+          const int t = warp + ROWS_WARPS * i;
+          v[i] = (b0 + t < R && u < R) ? LU[int64_t(b0 + t) * R + u] : 0.0;
         }
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int e = e0 + i * ROWS_WARPS * 32 + threadIdx.x, t = e / nu, u = e - t * nu;
-          if (e < 32 * nu) {
-            strip[u * 33 + t] = u <= b0 + t ? v[i] : 0.0;
-            if (u > b0 + t) dblk[t * 33 + (u - b0)] = v[i];  // (L_bb^-1)[u][t]
-          }
+        for (int i = 0; i < RPW; ++i) {
+          const int t = warp + ROWS_WARPS * i;
+          strip[u * 33 + t] = u <= b0 + t ? v[i] : 0.0;
+          if (u > b0 + t) dblk[t * 33 + (u - b0)] = v[i];  // (L_bb^-1)[u][t]
         }
       }
-    } else {
-      const int nc = rp - b0;
-      for (int e0 = 0; e0 < 32 * nc; e0 += 8 * ROWS_WARPS * 32) {
-        double v[8];
+    } else {  // rows c >= b0 of L, columns b0 + t (lanes along t)
+      for (int c0 = b0; c0 < rp; c0 += 32) {
+        double v[RPW];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int e = e0 + i * ROWS_WARPS * 32 + threadIdx.x, c = b0 + (e >> 5), t = e & 31;
-          v[i] = (e < 32 * nc && c < R && b0 + t < R) ? LU[int64_t(c) * R + b0 + t] : 0.0;
+        for (int i = 0; i < RPW; ++i) {
+          const int c = c0 + warp + ROWS_WARPS * i;
+          v[i] = (c < R && b0 + lane < R) ? LU[int64_t(c) * R + b0 + lane] : 0.0;
         }
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int e = e0 + i * ROWS_WARPS * 32 + threadIdx.x, c = b0 + (e >> 5), t = e & 31;
-          if (e < 32 * nc) {
-            strip[c * 33 + t] = c >= b0 + t ? v[i] : 0.0;
-            if (c < b0 + t) dblk[(c - b0) * 33 + t] = v[i];  // (L_bb^-1)[t][c - b0]
-          }
+        for (int i = 0; i < RPW; ++i) {
+          const int c = c0 + warp + ROWS_WARPS * i;
+          strip[c * 33 + lane] = c >= b0 + lane ? v[i] : 0.0;
+          if (c < b0 + lane) dblk[(c - b0) * 33 + lane] = v[i];  // (L_bb^-1)[t][c - b0]
         }
       }
     }
