@@ -223,7 +223,7 @@ constexpr int CB = 32, CHOL_THREADS = 512;
 // The kernels handle R <= CHOL_KERNEL_CAP; by default they replace cuSOLVER
 // up to CHOL_SMALL_MAX, where they stop winning (single CTA: the trailing
 // updates grow as R^3).  tools/solve_bench.py, B200: R = 32 19 vs 40 us,
-// 64 35 vs 79, 128 84 vs 172, 256 271 vs 362, 384 633 vs 554.
+// 64 34 vs 81, 128 81 vs 172, 256 258 vs 363, 384 597 vs 558 (rows = 128).
 constexpr int CHOL_KERNEL_CAP = 512, CHOL_SMALL_MAX = 256;
 
 static size_t chol_smem(int64_t R) {

@@ -2,6 +2,7 @@
 
     python tools/ncu_summary.py gpurun_out/prof_c4_mode0_r01.ncu-rep [...] --tag r01
     python tools/ncu_summary.py --launches gpurun_out/launches_r01.csv --tag r01
+    python tools/ncu_summary.py gpurun_out/prof_c3_mode1.ncu-rep --tag r01 --aux   # not the c4 kernel
 
 Writes profiles/<tag>_<report-stem>.txt (key metrics, stall reasons, shared-
 memory wavefronts per LDS, SASS opcode mix) and updates
@@ -130,12 +131,14 @@ if __name__ == "__main__":
     ap.add_argument("reports", nargs="*")
     ap.add_argument("--tag", default="r01")
     ap.add_argument("--launches")
+    ap.add_argument("--aux", action="store_true",
+                    help="not the bench's dominant kernel: write the .txt summaries only, leave ncu_summary.json")
     a = ap.parse_args()
     PROF.mkdir(exist_ok=True)
     if a.launches:
         summarize_launches(Path(a.launches), a.tag)
     res = [summarize_report(Path(p), a.tag) for p in a.reports]
-    if res:
+    if res and not a.aux:
         summ = {"tag": a.tag, "reports": res,
                 "dram_bytes_per_launch": sum(r["dram_bytes_per_launch"] for r in res) / len(res)}
         (PROF / "ncu_summary.json").write_text(json.dumps(summ, indent=1) + "\n")
