@@ -198,6 +198,16 @@ int cpk_solve_normal_spec_f64(const double* gamma, double* G, int64_t rows,
                               int64_t rank, void* work, size_t work_bytes,
                               int* info_out, void* stream);
 
+/* The same speculative solve in its two halves, so the factorization (which
+ * needs only Gamma) can run on a side stream while the mode's MTTKRP
+ * produces G: _factor writes the Cholesky factor into `work` and the flag
+ * into *info_out; _apply (same work / rank, stream-ordered after _factor)
+ * solves G in place, and skips when *info_out != 0. */
+int cpk_solve_factor_spec_f64(const double* gamma, int64_t rank, void* work,
+                              size_t work_bytes, int* info_out, void* stream);
+int cpk_solve_apply_spec_f64(double* G, int64_t rows, int64_t rank, void* work,
+                             size_t work_bytes, const int* info_out, void* stream);
+
 /* Column 2-norms of A (rows x rank), A[:, nz] /= nrm, lam = where(nz, nrm, 0)
  * -- cpals.py:134-137.  Split in two so the sharded driver can allreduce the
  * squared norms of a row-partitioned factor in between:

@@ -782,9 +782,38 @@ extern "C" int cpk_solve_normal_f64(const double* gamma, double* G, int64_t rows
   return fail(CPK_ERR_NOT_PD, "Gamma is not positive definite after 5 regularization rungs");
 }
 
-extern "C" int cpk_solve_normal_spec_f64(const double* gamma, double* G, int64_t rows, int64_t rank, void* work,
-                                         size_t work_bytes, int* info_out, void* stream) {
-  if (!gamma || !G || !work || !info_out || rank < 1 || rows < 0) return fail(CPK_ERR_PARAM, "bad solve arguments");
+extern "C" int cpk_solve_factor_spec_f64(const double* gamma, int64_t rank, void* work, size_t work_bytes,
+                                         int* info_out, void* stream) {
+  if (!gamma || !work || !info_out || rank < 1) return fail(CPK_ERR_PARAM, "bad solve arguments");
+  cudaStream_t st = as_stream(stream);
+  cusolverDnHandle_t h;
+  int rc = solver_for(st, &h);
+  if (rc) return rc;
+  int lwork = 0;
+  if (cusolverDnDpotrf_bufferSize(h, CUBLAS_FILL_MODE_UPPER, int(rank), nullptr, int(rank), &lwork) !=
+      CUSOLVER_STATUS_SUCCESS)
+    return fail(CPK_ERR_LIB, "potrf_bufferSize failed");
+  size_t total, off_w, off_info;
+  solve_layout(0, rank, lwork, &total, &off_w, &off_info);
+  if (work_bytes < total) return fail(CPK_ERR_RESOURCE, "solve workspace needs %zu bytes, got %zu", total, work_bytes);
+  char* base = static_cast<char*>(work);
+  double* L = reinterpret_cast<double*>(base);
+  double* w = reinterpret_cast<double*>(base + off_w);
+  if (use_small_chol(rank)) return chol_small(gamma, rank, 0.0, L, info_out, st);
+  const unsigned cblocks = unsigned(std::min<int64_t>((rank * rank + 255) / 256, 148 * 4));
+  copy_regularize_kernel<<<std::max(cblocks, 1u), 256, 0, st>>>(gamma, rank, 0.0, L);
+  rc = check_launch("copy_regularize");
+  if (rc) return rc;
+  // rung 0 only, and no readback: the caller checks *info_out later
+  if (cusolverDnDpotrf(h, CUBLAS_FILL_MODE_UPPER, int(rank), L, int(rank), w, lwork, info_out) !=
+      CUSOLVER_STATUS_SUCCESS)
+    return fail(CPK_ERR_LIB, "potrf failed");
+  return check_launch("potrf");
+}
+
+extern "C" int cpk_solve_apply_spec_f64(double* G, int64_t rows, int64_t rank, void* work, size_t work_bytes,
+                                        const int* info_out, void* stream) {
+  if (!G || !work || !info_out || rank < 1 || rows < 0) return fail(CPK_ERR_PARAM, "bad solve arguments");
   cudaStream_t st = as_stream(stream);
   cusolverDnHandle_t h;
   int rc = solver_for(st, &h);
@@ -798,23 +827,19 @@ extern "C" int cpk_solve_normal_spec_f64(const double* gamma, double* G, int64_t
   if (work_bytes < total) return fail(CPK_ERR_RESOURCE, "solve workspace needs %zu bytes, got %zu", total, work_bytes);
   char* base = static_cast<char*>(work);
   double* L = reinterpret_cast<double*>(base);
-  double* w = reinterpret_cast<double*>(base + off_w);
   int* info_d = reinterpret_cast<int*>(base + off_info);
-  if (use_small_chol(rank)) {
-    rc = chol_small(gamma, rank, 0.0, L, info_out, st);
-    if (rc) return rc;
-    return chol_rows(L, rank, G, rows, info_out, st);
-  }
-  const unsigned cblocks = unsigned(std::min<int64_t>((rank * rank + 255) / 256, 148 * 4));
-  copy_regularize_kernel<<<std::max(cblocks, 1u), 256, 0, st>>>(gamma, rank, 0.0, L);
-  rc = check_launch("copy_regularize");
-  if (rc) return rc;
-  // rung 0 only, and no readback: the caller checks *info_out later
-  if (cusolverDnDpotrf(h, CUBLAS_FILL_MODE_UPPER, int(rank), L, int(rank), w, lwork, info_out) !=
-      CUSOLVER_STATUS_SUCCESS)
-    return fail(CPK_ERR_LIB, "potrf failed");
+  if (use_small_chol(rank)) return chol_rows(L, rank, G, rows, info_out, st);
+  // potrs on a failed factor just produces garbage, which the caller discards
   if (rows > 0 && cusolverDnDpotrs(h, CUBLAS_FILL_MODE_UPPER, int(rank), int(rows), L, int(rank), G, int(rank),
                                    info_d) != CUSOLVER_STATUS_SUCCESS)
     return fail(CPK_ERR_LIB, "potrs failed");
   return check_launch("potrs");
+}
+
+extern "C" int cpk_solve_normal_spec_f64(const double* gamma, double* G, int64_t rows, int64_t rank, void* work,
+                                         size_t work_bytes, int* info_out, void* stream) {
+  if (!gamma || !G || !work || !info_out || rank < 1 || rows < 0) return fail(CPK_ERR_PARAM, "bad solve arguments");
+  const int rc = cpk_solve_factor_spec_f64(gamma, rank, work, work_bytes, info_out, stream);
+  if (rc) return rc;
+  return cpk_solve_apply_spec_f64(G, rows, rank, work, work_bytes, info_out, stream);
 }

@@ -61,8 +61,11 @@ class MttkrpPlan:
     ``rank_tile`` (0 = auto, else 32/64/128/256), ``splits`` (0 = auto) and
     ``block_k`` (chunk depth, 0 = auto, else 16/32) are the B200
     realization of the rank tiling and of N_T; ``engine`` picks the data
-    movement ("auto", "tma" = warp-specialized TMA kernel, "cpasync").  ``workers`` is
-    accepted for compatibility and ignored (one GPU per process).
+    movement ("auto", "tma" = warp-specialized TMA kernel, "cpasync").
+    ``sm_count`` (0 = the device's) is how many SMs the automatic split
+    count fills in whole waves -- cp_als leaves one free for the Cholesky it
+    runs beside the MTTKRP.  ``workers`` is accepted for compatibility and
+    ignored (one GPU per process).
     """
 
     variant: Variant
@@ -76,6 +79,7 @@ class MttkrpPlan:
     splits: int = 0
     block_k: int = 0
     engine: str = "auto"
+    sm_count: int = 0
 
     def validate(self, dims, rank) -> None:
         d = len(dims)
@@ -95,6 +99,8 @@ class MttkrpPlan:
             raise ParameterError(f"engine must be one of {sorted(_ENGINES)}, got {self.engine!r}")
         if self.block_k not in (0, 16, 32):
             raise ParameterError(f"block_k must be 0, 16 or 32, got {self.block_k}")
+        if self.sm_count < 0:
+            raise ParameterError(f"sm_count must be >= 0, got {self.sm_count}")
         if self.variant == Variant.TILE:
             n_s = num_elements(dims) // dims[self.mode]
             if self.tile_volume is None:
@@ -143,7 +149,7 @@ def _check_inputs(y: DenseTensor, m: KruskalTensor, mode: int) -> None:
 def _plan_request(plan: MttkrpPlan) -> _lib.CpkPlan:
     """The CpkPlan the C side resolves itself: zero fields mean "choose"
     (a fully automatic request may also merge a small mode with a neighbour)."""
-    p = _lib.CpkPlan(plan.rank_tile, 0, 0, plan.splits, 0, plan.block_k, _ENGINES[plan.engine])
+    p = _lib.CpkPlan(plan.rank_tile, 0, 0, plan.splits, plan.sm_count, plan.block_k, _ENGINES[plan.engine])
     v = Variant(plan.variant)
     if plan.splits == 0:
         if v == Variant.TILE:
