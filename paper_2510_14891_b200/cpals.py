@@ -258,11 +258,11 @@ def cp_als(y: DenseTensor, config: AlsConfig, graph: bool | None = None) -> tupl
             if captured is None:
                 keep = list(_device_workspaces(dev))  # captured pointers stay alive
                 captured = torch.cuda.CUDAGraph()
-                side = torch.cuda.Stream(dev)
-                side.wait_stream(torch.cuda.current_stream(dev))
+                cap = torch.cuda.Stream(dev)  # not `side`: sweep() forks onto that one
+                cap.wait_stream(torch.cuda.current_stream(dev))
                 # capture_begin/end directly: torch.cuda.graph() would also
                 # gc.collect() and empty the allocator cache on entry
-                with torch.cuda.stream(side):
+                with torch.cuda.stream(cap):
                     captured.capture_begin()
                     try:
                         snapshot()
@@ -270,7 +270,7 @@ def cp_als(y: DenseTensor, config: AlsConfig, graph: bool | None = None) -> tupl
                         sweep(spec=True)
                     finally:
                         captured.capture_end()
-                torch.cuda.current_stream(dev).wait_stream(side)
+                torch.cuda.current_stream(dev).wait_stream(cap)
                 captured.keep = keep
             captured.replay()
         ev[d + 1].synchronize()
