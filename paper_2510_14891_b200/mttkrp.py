@@ -360,10 +360,12 @@ _side = {}
 _copy = {}
 
 
-def _modes_stream(dev) -> torch.cuda.Stream:
-    if ("modes", dev.index) not in _copy:
-        _copy[("modes", dev.index)] = torch.cuda.Stream(dev)
-    return _copy[("modes", dev.index)]
+def _modes_stream(dev, i: int = 0) -> torch.cuda.Stream:
+    """Dedicated stream i of mttkrp_modes (one per mode; cached, so each
+    stream's allocator pool is reused call after call)."""
+    if ("modes", dev.index, i) not in _copy:
+        _copy[("modes", dev.index, i)] = torch.cuda.Stream(dev)
+    return _copy[("modes", dev.index, i)]
 
 
 def _copy_stream(dev) -> torch.cuda.Stream:
@@ -455,10 +457,13 @@ def mttkrp_modes(tensor, factors, modes=None, weights=None, plan: MttkrpPlan | N
 
     For a large host tensor this is where streaming pays most: the copy runs
     in slabs along the slowest mode and, for every landed slab, the work
-    items of *all* requested modes are issued in slab order on one stream
-    (cpk_mttkrp_f64_landed), so the copy hides under the compute of every
-    mode, not just the first.  Each mode keeps its own plan, workspace and
-    merge order: results are bit-identical to one resident call per mode.
+    items of *all* requested modes are issued (cpk_mttkrp_f64_landed), so
+    the copy hides under the compute of every mode, not just the first.
+    Each mode has its own stream: a piece's last partial wave of CTAs is
+    filled by the other modes' pieces instead of idling SMs (c4: ~24 piece
+    launches, ~0.5 ms of tail each on one stream).  Each mode keeps its own
+    plan, workspace and merge order: results are bit-identical to one
+    resident call per mode.
     """
     if isinstance(factors, KruskalTensor):
         m = factors
@@ -488,23 +493,23 @@ def mttkrp_modes(tensor, factors, modes=None, weights=None, plan: MttkrpPlan | N
     # copy once the default stream had done any H2D (measured,
     # tools/dbg_copy2.py), which serialized copy and compute.
     main = torch.cuda.current_stream(dev)
-    side = _modes_stream(dev)  # one stream: its allocator pool is reused call after call
-    side.wait_stream(main)  # inputs are ordered on `main`
-    outs = []
-    with torch.cuda.stream(side):
-        wss = []
-        for pk in plans:
+    sides = [_modes_stream(dev, i) for i in range(len(plans))]
+    outs, wss = [], []
+    for pk, st in zip(plans, sides):
+        st.wait_stream(main)  # inputs are ordered on `main`
+        with torch.cuda.stream(st):
             nbytes = _lib.C.c_size_t(0)
             _lib.check(_lib.load().cpk_mttkrp_workspace_bytes(len(dims), _lib.i64_array(dims), pk.mode, rank,
                                                                _plan_request(pk), _lib.C.byref(nbytes)), "workspace")
             outs.append(torch.empty((dims[pk.mode], rank), dtype=torch.float64, device=dev))
             wss.append(torch.empty(max(1, (nbytes.value + 7) // 8), dtype=torch.float64, device=dev))
-        for (lo, hi), ev in zip(bounds, events):
-            side.wait_event(ev)
-            for pk, out, ws in zip(plans, outs, wss):
+    for (lo, hi), ev in zip(bounds, events):  # slab-major, so every stream has work early
+        for pk, out, ws, st in zip(plans, outs, wss, sides):
+            st.wait_event(ev)
+            with torch.cuda.stream(st):
                 mttkrp_device(y_dev, dims, fac, pk.mode, lam, pk, out=out, landed=(lo, hi), workspace_buf=ws)
-    main.wait_stream(side)
-    for out in outs:
+    for out, st in zip(outs, sides):
+        main.wait_stream(st)
         out.record_stream(main)
     host = not isinstance(y.data, torch.Tensor)
     return [np.ascontiguousarray(g.cpu().numpy()) for g in outs] if host else outs
