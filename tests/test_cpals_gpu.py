@@ -143,3 +143,21 @@ def test_odd_first_extent_sweeps_on_the_even_copy(dims):
     _, _, ref = oracle.cp_als(y, dims, 4, max_iters=6, tol=0.0, seed=2)
     assert np.max(np.abs(np.asarray(tr.fits) - np.asarray(ref))) <= 1e-8
     assert [tuple(a.shape) for a in model.factors] == [(n, 4) for n in dims]
+
+
+@pytest.mark.parametrize("solve", ["kernel", "cusolver"])
+@pytest.mark.parametrize("rank", [40, 264])
+def test_side_stream_factorization_paths_follow_the_oracle(monkeypatch, solve, rank):
+    """Gamma is factored on a side stream while the MTTKRP runs (the split
+    speculative solve); both factorization paths -- our kernels (forced up
+    to R = 512) and cuSOLVER (the default above R = 256) -- follow the
+    oracle's cho_solve trajectory, graph-replayed and eager alike."""
+    monkeypatch.setenv("CPK_SOLVE", solve)
+    dims = (40, 36, 34)
+    y = rng_for(rank).random(int(np.prod(dims)))
+    cfg = ck.AlsConfig(rank=rank, tol=0.0, max_iters=5, seed=4)
+    _, t_e = ck.cp_als(ck.DenseTensor(dims, y), cfg, graph=False)
+    _, t_g = ck.cp_als(ck.DenseTensor(dims, y), cfg, graph=True)
+    _, _, ref = oracle.cp_als(y, dims, rank, max_iters=5, tol=0.0, seed=4)
+    assert np.max(np.abs(np.asarray(t_e.fits) - np.asarray(ref))) <= 1e-8
+    assert t_g.fits == t_e.fits
