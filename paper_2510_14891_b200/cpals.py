@@ -136,10 +136,11 @@ def _solve_spec(solver: "_Solver", gamma: torch.Tensor, g: torch.Tensor, info: t
     )
 
 
-# Capturing a sweep costs ~15-20 ms once and saves ~1 ms of launch overhead
-# per sweep (c3, profiles/r01_bench.jsonl), so the auto mode captures only
-# runs that may go this long.
-GRAPH_MIN_ITERS = 24
+# Capturing a sweep costs ~6 ms once and saves ~0.5 ms of host gaps per
+# sweep (c3: 17.5 ms eager vs 17.0 replayed; 10 sweeps break even,
+# profiles/r01_bench.jsonl), so the auto mode captures runs that may go
+# longer than that.
+GRAPH_MIN_ITERS = 12
 
 
 def cp_als(y: DenseTensor, config: AlsConfig, graph: bool | None = None) -> tuple:
@@ -238,13 +239,11 @@ def cp_als(y: DenseTensor, config: AlsConfig, graph: bool | None = None) -> tupl
     saved = [torch.empty_like(t) for t in factors + grams + [lam]]
     captured = None
 
-    def snapshot():
-        for dst, src in zip(saved, factors + grams + [lam]):
-            dst.copy_(src)
+    def snapshot():  # one multi-tensor copy launch, not 2d + 1
+        torch._foreach_copy_(saved, factors + grams + [lam])
 
     def restore():
-        for dst, src in zip(factors + grams + [lam], saved):
-            dst.copy_(src)
+        torch._foreach_copy_(factors + grams + [lam], saved)
 
     fits, mttkrp_seconds, other_seconds = [], [], []
     converged = False
