@@ -133,6 +133,85 @@ def _ints(s: str, what: str) -> list:
         raise ParameterError(f"bad {what} list {s!r}") from exc
 
 
+# Named shapes of the reference CLI (cli.py:42-47): the paper's tearing and
+# island tensors and their small twins.
+PRESETS = {
+    "tearing": (401, 201, 12, 501),
+    "island": (129, 129, 129, 12, 39),
+    "tearing-small": (51, 26, 12, 51),
+    "island-small": (17, 17, 17, 12, 9),
+}
+
+
+def model_report(dims, ranks, modes=None, machine: pm.MachineSpec | None = None) -> dict:
+    """The reference's `cpkern model` document (cli.py:470-545): work, traffic
+    models and predicted times per rank, per variant (ELEM N_T = 1, SLICE
+    N_T = N_S, TILE the Eq. 6 heuristic) and mode, the dense-GEMM footprint
+    and capacity-only device counts -- no kernels run.  Same keys and values
+    (tests/golden/model_cli.json); a "b200" entry adds the north-star
+    roofline per mode (max(8 N / HBM, 2 N R (d-1) / FP64)) on the measured
+    B200 denominators."""
+    machine = machine or pm.bundled_machine("nvidia-b200")
+    dims = tuple(int(x) for x in dims)
+    d, n = len(dims), num_elements(dims)
+    modes = list(range(d)) if modes is None else [int(k) for k in modes]
+    width = mt.heuristic_tile_width(dims, machine) if d >= 2 else 1
+    rows = []
+    for rank in ranks:
+        f = pm.flops(dims, rank)
+        m_inf = pm.mem_infty(dims, rank, machine.s_f_bytes)
+        inten = pm.intensity(f, m_inf)
+        worst, worst_k = pm.mem_gemm_worst(dims, rank, machine.s_f_bytes)
+        variants = {}
+        for name, n_t in (("elem", lambda k: 1), ("slice", lambda k: n // dims[k]),
+                          ("tile", lambda k: max(1, min(width ** (d - 1), n // dims[k])))):
+            per = []
+            for k in modes:
+                m0 = pm.mem_zero(dims, rank, k, n_t(k), machine.s_f_bytes)
+                m0lm = pm.mem_zero_lm(dims, rank, k, n_t(k), machine.l, machine.s_f_bytes)
+                per.append({"mode": k + 1, "N_T": n_t(k), "m_zero": m0, "m_zero_lm": m0lm,
+                            "T0": pm.predict_seconds(f, m0, machine), "T0LM": pm.predict_seconds(f, m0lm, machine)})
+            variants[name] = {"T0_mean": statistics.fmean(r["T0"] for r in per),
+                              "T0LM_mean": statistics.fmean(r["T0LM"] for r in per), "per_mode": per}
+        rows.append({
+            "rank": rank, "f": f, "matrix_free_bytes": m_inf, "matrix_free_gib": m_inf / pm.GIB,
+            "intensity": inten, "compute_bound": pm.is_compute_bound(inten, machine),
+            "TInf": pm.predict_seconds(f, m_inf, machine),
+            "gemm_per_mode_bytes": [pm.mem_gemm(dims, rank, k, machine.s_f_bytes) for k in range(d)],
+            "gemm_worst_bytes": worst, "gemm_worst_gib": worst / pm.GIB, "gemm_worst_mode": worst_k + 1,
+            "matrix_free_pct_of_gemm": 100.0 * m_inf / worst,
+            "devices_matrix_free": pm.device_count(m_inf, machine), "devices_gemm": pm.device_count(worst, machine),
+            "variants": variants,
+            "b200": {"roofline_seconds_per_mode": pm.roofline_seconds(dims, rank),
+                     "algorithmic_flops_per_mode": pm.algorithmic_flops(dims, rank)},
+        })
+    return {"machine": machine.to_dict(), "dims": list(dims), "n_elements": n,
+            "tensor_bytes": machine.s_f_bytes * n, "heuristic_tile_width": width,
+            "heuristic_tile_volume": width ** (d - 1) if d >= 2 else 1, "modes": [k + 1 for k in modes],
+            "ranks": rows}
+
+
+def _print_model(doc: dict) -> None:
+    m = doc["machine"]
+    print(f"shape {tuple(doc['dims'])}  N={doc['n_elements']}  tensor "
+          f"{doc['tensor_bytes'] / pm.GIB:.3f} GiB  machine {m['name']}")
+    print(f"heuristic tile width {doc['heuristic_tile_width']} (N_T={doc['heuristic_tile_volume']})")
+    for r in doc["ranks"]:
+        print(f"\nrank {r['rank']}:")
+        print(f"  f = {r['f']} flops   intensity {r['intensity']:.3f} flop/B"
+              f"   {'compute' if r['compute_bound'] else 'memory'}-bound")
+        print(f"  matrix-free footprint {r['matrix_free_bytes']} B = {r['matrix_free_gib']:.2f} GiB"
+              f"  ({r['matrix_free_pct_of_gemm']:.2f}% of dense baseline)")
+        print(f"  dense baseline worst mode {r['gemm_worst_mode']}: {r['gemm_worst_bytes']} B"
+              f" = {r['gemm_worst_gib']:.2f} GiB")
+        print(f"  devices needed (capacity lower bound): {r['devices_matrix_free']} matrix-free,"
+              f" {r['devices_gemm']} dense")
+        print(f"  T_inf {r['TInf']:.6f} s")
+        for name, v in r["variants"].items():
+            print(f"  {name:6s} T0 {v['T0_mean']:.6f} s   T0,LM {v['T0LM_mean']:.6f} s  (mean over modes)")
+        print(f"  B200 north-star roofline {r['b200']['roofline_seconds_per_mode']:.6f} s per mode")
+
+
 def main(argv=None) -> int:
     import argparse
 
@@ -151,7 +230,40 @@ def main(argv=None) -> int:
     sp.add_argument("--seed", type=int, default=0)
     sp.add_argument("--out", default="sweep.csv")
     sp.add_argument("--agg-out", default=None)
+    mp = sub.add_parser("model", help="analytic work/traffic/time numbers, no kernels (cpkern model, cli.py:470-545)")
+    mp.add_argument("--tensor", help="read the shape from a DTEN header")
+    mp.add_argument("--shape", help="comma-separated extents")
+    mp.add_argument("--preset", choices=sorted(PRESETS), help="named shape (cli.py:42-47)")
+    mp.add_argument("--ranks", default="32")
+    mp.add_argument("--modes", default="all", help="'all' or 1-based, comma-separated")
+    mp.add_argument("--machine", default="nvidia-b200", help="bundled spec name or JSON path")
+    mp.add_argument("--json", action="store_true", help="machine-readable output")
     a = ap.parse_args(argv)
+    if a.cmd == "model":
+        if a.tensor:
+            from .dtensor import read_dten_header
+
+            dims = read_dten_header(a.tensor)
+        elif a.preset:
+            dims = PRESETS[a.preset]
+        elif a.shape:
+            dims = tuple(_ints(a.shape, "shape"))
+        else:
+            raise ParameterError("give --shape, --preset or --tensor")
+        machine = (pm.bundled_machine(a.machine) if a.machine in pm.bundled_machine_names()
+                   else pm.load_machine(a.machine))
+        if a.modes.strip().lower() == "all":
+            modes = None
+        else:
+            modes = [m - 1 for m in _ints(a.modes, "modes")]
+            if any(not 0 <= k < len(dims) for k in modes):
+                raise ParameterError(f"modes must lie in [1, {len(dims)}]")
+        doc = model_report(dims, _ints(a.ranks, "ranks"), modes, machine)
+        if a.json:
+            print(json.dumps(doc, indent=2))
+        else:
+            _print_model(doc)
+        return 0
     if a.tensor:
         from .dtensor import read_dten
 

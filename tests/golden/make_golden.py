@@ -21,6 +21,8 @@ Fixtures (numpy .npz, float64):
                 Philox tensor and a 1-way one) and the reference's verdict
                 (shape, or the FormatError message) on malformed variants
   model.json -- cpkern.perfmodel traffic models / predicted times (sweep columns)
+  model_cli.json -- `cpkern model --json` documents (cli.py:470-545) for
+                presets / shapes / machines / ranks / modes
   als.npz    -- cp_als fit trajectories: the planted suites of test_cpals.py
                 (REFERENCE and GEMM plans), and config 3 for 10 sweeps (GEMM)
 Inputs for c1-c3 follow the reference CLI recipe (cli.py:133-141):
@@ -185,6 +187,33 @@ def make_model():
     (OUT / "model.json").write_text(json.dumps(cases, indent=1) + "\n")
 
 
+MODEL_CLI_CASES = [
+    ["--preset", "tearing", "--ranks", "16,32", "--machine", "nvidia-h100"],
+    ["--preset", "island", "--ranks", "32", "--modes", "1,3,5", "--machine", "intel-8480p"],
+    ["--shape", "1024,1024,1024", "--ranks", "2000", "--machine", "nvidia-h100"],
+    ["--shape", "4096,2048,2048", "--ranks", "512", "--machine", "intel-8480p"],
+    ["--shape", "64,64,64", "--ranks", "1,16", "--machine", "nvidia-h100"],
+    ["--shape", "7", "--ranks", "3", "--machine", "intel-8480p"],
+]
+
+
+def make_model_cli():
+    """`cpkern model --json` (the reference CLI itself) on MODEL_CLI_CASES."""
+    import contextlib
+    import io
+    import json
+
+    from cpkern import cli
+
+    docs = []
+    for args in MODEL_CLI_CASES:
+        buf = io.StringIO()
+        with contextlib.redirect_stdout(buf):
+            assert cli.main(["model", *args, "--json"]) == 0
+        docs.append({"args": args, "doc": json.loads(buf.getvalue())})
+    (OUT / "model_cli.json").write_text(json.dumps(docs, indent=1) + "\n")
+
+
 def make_dten():
     import json
 
@@ -222,9 +251,11 @@ def make_dten():
 
 
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["small", "c1", "c2", "c3", "als", "dten", "model"]
+    which = sys.argv[1:] or ["small", "c1", "c2", "c3", "als", "dten", "model", "model_cli"]
     if "model" in which:
         make_model()
+    if "model_cli" in which:
+        make_model_cli()
     if "dten" in which:
         make_dten()
     if "small" in which:

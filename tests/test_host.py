@@ -181,3 +181,50 @@ def test_traffic_models_match_reference():
         assert pm.predict_seconds(f, c["mem_zero_lm"], ms) == c["T0LM"]
         assert pm.predict_seconds(f, c["mem_infty"], ms) == c["TInf"]
         assert pm.gbytes_per_s(c["mem_zero"], 0.37) == c["gbps"]
+
+
+def _same(ours, ref, path="doc"):
+    """ref's keys/values reproduced in ours (extra keys in ours allowed)."""
+    if isinstance(ref, dict):
+        assert isinstance(ours, dict), path
+        for k, v in ref.items():
+            assert k in ours, f"{path}.{k} missing"
+            _same(ours[k], v, f"{path}.{k}")
+    elif isinstance(ref, list):
+        assert isinstance(ours, list) and len(ours) == len(ref), path
+        for i, (a, b) in enumerate(zip(ours, ref)):
+            _same(a, b, f"{path}[{i}]")
+    elif isinstance(ref, float):
+        assert abs(ours - ref) <= 1e-12 * max(1.0, abs(ref)), (path, ours, ref)
+    else:
+        assert ours == ref, (path, ours, ref)
+
+
+def test_model_command_matches_reference_cli(capsys):
+    """`python -m paper_2510_14891_b200 model --json` reproduces the
+    reference's `cpkern model --json` document (cli.py:470-545; fixtures
+    from the reference CLI itself, tests/golden/model_cli.json) for presets,
+    shapes, machines, ranks and mode subsets; the B200 roofline is extra."""
+    import json
+    from pathlib import Path
+
+    from paper_2510_14891_b200 import harness
+
+    cases = json.loads((Path(__file__).resolve().parent / "golden" / "model_cli.json").read_text())
+    for c in cases:
+        assert harness.main(["model", *c["args"], "--json"]) == 0
+        ours = json.loads(capsys.readouterr().out)
+        _same(ours, c["doc"])
+        assert all("b200" in r for r in ours["ranks"])
+
+
+def test_model_command_text_and_errors(capsys):
+    from paper_2510_14891_b200 import harness
+
+    assert harness.main(["model", "--preset", "tearing-small", "--ranks", "8"]) == 0
+    out = capsys.readouterr().out
+    assert "heuristic tile width" in out and "B200 north-star roofline" in out
+    with pytest.raises(ck.ParameterError):
+        harness.main(["model", "--shape", "4,4", "--modes", "3"])
+    with pytest.raises(ck.ParameterError):
+        harness.main(["model"])
