@@ -223,7 +223,7 @@ def main(argv=None) -> int:
     sp.add_argument("--ranks", default="32")
     sp.add_argument("--variants", default="tile")
     sp.add_argument("--tile-widths", default="")
-    sp.add_argument("--modes", default="", help="1-based, comma-separated (default all)")
+    sp.add_argument("--modes", default="all", help="'all' or 1-based, comma-separated")
     sp.add_argument("--reps", type=int, default=3)
     sp.add_argument("--warmup", type=int, default=1)
     sp.add_argument("--machine", default="nvidia-b200", help="bundled spec name or JSON path")
@@ -274,7 +274,7 @@ def main(argv=None) -> int:
         dims = tuple(_ints(a.shape, "shape"))
         y = DenseTensor(dims, np.random.Generator(np.random.Philox(a.seed)).random(num_elements(dims)))
     machine = pm.bundled_machine(a.machine) if a.machine in pm.bundled_machine_names() else pm.load_machine(a.machine)
-    modes = [m - 1 for m in _ints(a.modes, "modes")] or None
+    modes = None if a.modes.strip().lower() in ("", "all") else [m - 1 for m in _ints(a.modes, "modes")]
     res = sweep(y, _ints(a.ranks, "ranks"), a.variants.split(","), _ints(a.tile_widths, "tile widths") or None,
                 modes, a.reps, a.warmup, machine, a.seed, a.out, a.agg_out)
     print(json.dumps(res))
