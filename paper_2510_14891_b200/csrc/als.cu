@@ -415,13 +415,15 @@ __global__ void __launch_bounds__(CHOL_THREADS, 1) chol_small_kernel(const doubl
 // X L L^T = G for every row of G (rows x R, row-major, ld R), skipped when
 // *info != 0.  RW rows per warp, ROWS_WARPS warps per CTA; the rows live in
 // shared memory interleaved (z[c][q]), lane j owns column tb * 32 + j of the
-// current 32-column block.  Per block the CTA stages the 32-column strip of
-// L it needs (coalesced, 8 loads in flight per thread) and the block's
-// inverse (chol_small leaves it in the upper triangle), then each warp runs
-// the dot-product part from shared memory (RW independent chains per strip
-// element) and the in-block solve as a 32 x 32 GEMV with the inverse.
-// Forward Z L^T = G needs L[t][u] (u < t), backward X L = Z needs L[c][t]
-// (c > t): both from the lower triangle.
+// current 32-column block.  The 2 nblk steps (forward blocks 0.., backward
+// blocks ..0) each need a strip of L and the raw diagonal block (its lower
+// triangle L_bb, its upper the transposed inverse chol_small parks there);
+// they are staged with cp.async into two buffers, the next step's while the
+// current one computes (DB; one buffer when two do not fit, R > 256).  Each
+// warp then runs the dot-product part from shared memory (RW independent
+// chains per strip element) and the in-block solve as a 32 x 32 GEMV with
+// the inverse.  Forward Z L^T = G needs L[t][u] (u < t), backward X L = Z
+// needs L[c][t] (c > t): both from the lower triangle.
 constexpr int ROWS_WARPS = 4;
 
 template <int RW>
@@ -437,22 +439,23 @@ __device__ __forceinline__ void zrow(const double* z, double (&v)[RW]) {  // one
   }
 }
 
-static size_t rows_smem(int64_t R, int rw) {
+static size_t rows_smem(int64_t R, int rw, bool db) {
   const int64_t rp = (R + 31) / 32 * 32;
-  return size_t(rp * 33 + int64_t(ROWS_WARPS) * rw * rp + 32 + 32 * 33) * sizeof(double);
+  const int64_t nb = db ? 2 : 1;
+  return size_t(nb * (rp * 33 + 32 * 33) + int64_t(ROWS_WARPS) * rw * rp + 32) * sizeof(double);
 }
 
-template <int RW>
+template <int RW, bool DB>
 __global__ void __launch_bounds__(ROWS_WARPS * 32) chol_rows_kernel(const double* __restrict__ LU, int R,
                                                                     double* __restrict__ G, int64_t rows,
                                                                     const int* __restrict__ info) {
   if (*info != 0) return;
   extern __shared__ __align__(16) double rsm[];
   const int rp = (R + 31) / 32 * 32;
-  double* strip = rsm;                                   // [rp][33]: the strip of block tb
-  double* zall = rsm + rp * 33;                          // [warp][rp][RW]
+  double* zall = rsm;                                    // [warp][rp][RW]
   double* rdiag = zall + ROWS_WARPS * RW * rp;           // [32]
-  double* dblk = rdiag + 32;                             // [32][33]: dblk[a][b] = (L_bb^-1)[b][a], a < b
+  double* bufs = rdiag + 32;                             // DB ? 2 : 1 x {strip [rp][33], dblk [32][33]}
+  const int buf_elems = rp * 33 + 32 * 33;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t q0 = (int64_t(blockIdx.x) * ROWS_WARPS + warp) * RW;
   const bool active = q0 < rows;  // inactive warps still help stage strips
@@ -460,125 +463,109 @@ __global__ void __launch_bounds__(ROWS_WARPS * 32) chol_rows_kernel(const double
   for (int c = lane; c < rp; c += 32)
 #pragma unroll
     for (int q = 0; q < RW; ++q) z[c * RW + q] = (active && q0 + q < rows && c < R) ? G[(q0 + q) * R + c] : 0.0;
-  const int nblk = rp / 32;
-  // Stage the strip of block tb: forward strip[u][t] = L[b0 + t][u]
-  // (u < b0 + 32), backward strip[c][t] = L[c][b0 + t] (c >= b0); lower
-  // triangle only (the upper is not written by chol_small), 8 loads in
-  // flight per thread, rows padded to 33 so both patterns are conflict-free.
-  auto stage = [&](int tb, bool fwd) {
-    __syncthreads();  // everyone is done with the previous strip
-    const int b0 = tb * 32;
-    constexpr int RPW = 32 / ROWS_WARPS;  // strip rows per warp and 32-row slab
-    if (fwd) {  // rows b0 + t of L, columns u < b0 + 32 (lanes along u)
-      for (int u0 = 0; u0 < b0 + 32; u0 += 32) {
-        const int u = u0 + lane;
-        double v[RPW];
-#pragma unroll
-        for (int i = 0; i < RPW; ++i) {
-          const int t = warp + ROWS_WARPS * i;
-          v[i] = (b0 + t < R && u < R) ? LU[int64_t(b0 + t) * R + u] : 0.0;
+  const int nblk = rp / 32, nsteps = 2 * nblk;
+  // step s: forward block s, then backward blocks nblk-1 .. 0
+  auto block_of = [&](int s) { return s < nblk ? s : 2 * nblk - 1 - s; };
+  auto issue = [&](int s, int b) {
+    const int b0 = block_of(s) * 32;
+    double* strip = bufs + b * buf_elems;
+    double* dblk = strip + rp * 33;
+    for (int e = threadIdx.x; e < 32 * 32; e += ROWS_WARPS * 32) {  // raw diagonal block
+      const int r = e >> 5, c = e & 31;
+      const bool ok = b0 + r < R && b0 + c < R;
+      cp_async8(dblk + r * 33 + c, ok ? LU + int64_t(b0 + r) * R + b0 + c : LU, ok ? 8 : 0);
+    }
+    if (s < nblk) {  // forward: strip[u][t] = L[b0 + t][u], u < b0 (lanes along u)
+      for (int t = warp; t < 32; t += ROWS_WARPS)
+        for (int u = lane; u < b0; u += 32) {
+          const bool ok = b0 + t < R;
+          cp_async8(strip + u * 33 + t, ok ? LU + int64_t(b0 + t) * R + u : LU, ok ? 8 : 0);
         }
-#pragma unroll
-        for (int i = 0; i < RPW; ++i) {
-          const int t = warp + ROWS_WARPS * i;
-          strip[u * 33 + t] = u <= b0 + t ? v[i] : 0.0;
-          if (u > b0 + t) dblk[t * 33 + (u - b0)] = v[i];  // (L_bb^-1)[u][t]
-        }
-      }
-    } else {  // rows c >= b0 of L, columns b0 + t (lanes along t)
-      for (int c0 = b0; c0 < rp; c0 += 32) {
-        double v[RPW];
-#pragma unroll
-        for (int i = 0; i < RPW; ++i) {
-          const int c = c0 + warp + ROWS_WARPS * i;
-          v[i] = (c < R && b0 + lane < R) ? LU[int64_t(c) * R + b0 + lane] : 0.0;
-        }
-#pragma unroll
-        for (int i = 0; i < RPW; ++i) {
-          const int c = c0 + warp + ROWS_WARPS * i;
-          strip[c * 33 + lane] = c >= b0 + lane ? v[i] : 0.0;
-          if (c < b0 + lane) dblk[(c - b0) * 33 + lane] = v[i];  // (L_bb^-1)[t][c - b0]
-        }
+    } else {  // backward: strip[c][t] = L[c][b0 + t], c >= b0 + 32 (lanes along t)
+      for (int c = b0 + 32 + warp; c < rp; c += ROWS_WARPS) {
+        const bool ok = c < R && b0 + lane < R;
+        cp_async8(strip + c * 33 + lane, ok ? LU + int64_t(c) * R + b0 + lane : LU, ok ? 8 : 0);
       }
     }
-    __syncthreads();
-    if (threadIdx.x < 32) {
-      const int k = b0 + threadIdx.x;
-      rdiag[threadIdx.x] = k < R ? 1.0 / strip[k * 33 + threadIdx.x] : 0.0;
-    }
-    __syncthreads();
+    cp_async_commit();
   };
-  // forward: z_t = (g_t - sum_{u<t} z_u L[t][u]) / L[t][t]
-  for (int tb = 0; tb < nblk; ++tb) {
-    stage(tb, true);
-    if (!active) continue;
-    const int b0 = tb * 32, t = b0 + lane;
-    double acc[RW];
+  issue(0, 0);
+  for (int s = 0; s < nsteps; ++s) {
+    const int b = DB ? (s & 1) : 0;
+    if (DB && s + 1 < nsteps) {
+      issue(s + 1, (s + 1) & 1);  // the next step's strip, behind this one's math
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    const double* strip = bufs + b * buf_elems;
+    const double* dblk = strip + rp * 33;
+    const int b0 = block_of(s) * 32, t = b0 + lane;
+    if (threadIdx.x < 32) rdiag[threadIdx.x] = b0 + threadIdx.x < R ? 1.0 / dblk[threadIdx.x * 34] : 0.0;
+    __syncthreads();
+    if (active) {
+      double acc[RW];
 #pragma unroll
-    for (int q = 0; q < RW; ++q) acc[q] = z[t * RW + q];
+      for (int q = 0; q < RW; ++q) acc[q] = z[t * RW + q];
+      if (s < nblk) {
+        // forward: z_t = (g_t - sum_{u<t} z_u L[t][u]) / L[t][t]
 #pragma unroll 8
-    for (int u = 0; u < b0; ++u) {
-      const double w = strip[u * 33 + lane];
-      double zu[RW];
-      zrow<RW>(z + u * RW, zu);
+        for (int u = 0; u < b0; ++u) {
+          const double w = strip[u * 33 + lane];
+          double zu[RW];
+          zrow<RW>(z + u * RW, zu);
 #pragma unroll
-      for (int q = 0; q < RW; ++q) acc[q] = fma(-zu[q], w, acc[q]);
-    }
-    // in-block: z_b = L_bb^-1 rhs_b (a 32 x 32 GEMV, no sequential chain)
+          for (int q = 0; q < RW; ++q) acc[q] = fma(-zu[q], w, acc[q]);
+        }
+        // in-block: z_b = L_bb^-1 rhs_b (a 32 x 32 GEMV, no sequential chain)
 #pragma unroll
-    for (int q = 0; q < RW; ++q) z[t * RW + q] = acc[q];
-    __syncwarp();
-    const double rd = rdiag[lane];
+        for (int q = 0; q < RW; ++q) z[t * RW + q] = acc[q];
+        __syncwarp();
+        const double rd = rdiag[lane];
 #pragma unroll
-    for (int q = 0; q < RW; ++q) acc[q] *= rd;
+        for (int q = 0; q < RW; ++q) acc[q] *= rd;
 #pragma unroll
-    for (int u = 0; u < 31; ++u) {
-      const double w = u < lane ? dblk[u * 33 + lane] : 0.0;  // (L_bb^-1)[t][u]
-      double zu[RW];
-      zrow<RW>(z + (b0 + u) * RW, zu);
+        for (int u = 0; u < 31; ++u) {
+          const double w = u < lane ? dblk[u * 33 + lane] : 0.0;  // (L_bb^-1)[t][u]
+          double zu[RW];
+          zrow<RW>(z + (b0 + u) * RW, zu);
 #pragma unroll
-      for (int q = 0; q < RW; ++q) acc[q] = fma(w, zu[q], acc[q]);
-    }
-    __syncwarp();
-#pragma unroll
-    for (int q = 0; q < RW; ++q) z[t * RW + q] = acc[q];
-    __syncwarp();
-  }
-  // backward: x_t = (z_t - sum_{c>t} x_c L[c][t]) / L[t][t]
-  for (int tb = nblk - 1; tb >= 0; --tb) {
-    stage(tb, false);
-    if (!active) continue;
-    const int b0 = tb * 32, t = b0 + lane;
-    double acc[RW];
-#pragma unroll
-    for (int q = 0; q < RW; ++q) acc[q] = z[t * RW + q];
+          for (int q = 0; q < RW; ++q) acc[q] = fma(w, zu[q], acc[q]);
+        }
+      } else {
+        // backward: x_t = (z_t - sum_{c>t} x_c L[c][t]) / L[t][t]
 #pragma unroll 8
-    for (int c = b0 + 32; c < R; ++c) {
-      const double w = strip[c * 33 + lane];
-      double zc[RW];
-      zrow<RW>(z + c * RW, zc);
+        for (int c = b0 + 32; c < R; ++c) {
+          const double w = strip[c * 33 + lane];
+          double zc[RW];
+          zrow<RW>(z + c * RW, zc);
 #pragma unroll
-      for (int q = 0; q < RW; ++q) acc[q] = fma(-zc[q], w, acc[q]);
+          for (int q = 0; q < RW; ++q) acc[q] = fma(-zc[q], w, acc[q]);
+        }
+        // in-block: x_b = rhs_b L_bb^-1, x_t = sum_{u >= t} rhs_u (L_bb^-1)[u][t]
+#pragma unroll
+        for (int q = 0; q < RW; ++q) z[t * RW + q] = acc[q];
+        __syncwarp();
+        const double rd = rdiag[lane];
+#pragma unroll
+        for (int q = 0; q < RW; ++q) acc[q] *= rd;
+#pragma unroll
+        for (int u = 1; u < 32; ++u) {
+          const double w = u > lane ? dblk[lane * 33 + u] : 0.0;  // (L_bb^-1)[u][t]
+          double zu[RW];
+          zrow<RW>(z + (b0 + u) * RW, zu);
+#pragma unroll
+          for (int q = 0; q < RW; ++q) acc[q] = fma(w, zu[q], acc[q]);
+        }
+      }
+      __syncwarp();
+#pragma unroll
+      for (int q = 0; q < RW; ++q) z[t * RW + q] = acc[q];
+      __syncwarp();
     }
-    // in-block: x_b = rhs_b L_bb^-1, x_t = sum_{u >= t} rhs_u (L_bb^-1)[u][t]
-#pragma unroll
-    for (int q = 0; q < RW; ++q) z[t * RW + q] = acc[q];
-    __syncwarp();
-    const double rd = rdiag[lane];
-#pragma unroll
-    for (int q = 0; q < RW; ++q) acc[q] *= rd;
-#pragma unroll
-    for (int u = 1; u < 32; ++u) {
-      const double w = u > lane ? dblk[lane * 33 + u] : 0.0;  // (L_bb^-1)[u][t]
-      double zu[RW];
-      zrow<RW>(z + (b0 + u) * RW, zu);
-#pragma unroll
-      for (int q = 0; q < RW; ++q) acc[q] = fma(w, zu[q], acc[q]);
-    }
-    __syncwarp();
-#pragma unroll
-    for (int q = 0; q < RW; ++q) z[t * RW + q] = acc[q];
-    __syncwarp();
+    __syncthreads();  // buffer b is refilled two steps on (one, without DB)
+    if (!DB && s + 1 < nsteps) issue(s + 1, 0);
   }
   if (!active) return;
   for (int c = lane; c < R; c += 32)
@@ -604,14 +591,14 @@ static int chol_small(const double* gamma, int64_t R, double eps, double* L, int
   return check_launch("chol_small");
 }
 
-template <int RW>
+template <int RW, bool DB>
 static int chol_rows_launch(const double* LU, int64_t R, double* G, int64_t rows, const int* info, cudaStream_t st) {
-  const size_t smem = rows_smem(R, RW);
-  if (cudaFuncSetAttribute(chol_rows_kernel<RW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           int(rows_smem(CHOL_KERNEL_CAP, RW))) != cudaSuccess)
+  const size_t smem = rows_smem(R, RW, DB);
+  if (cudaFuncSetAttribute(chol_rows_kernel<RW, DB>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) !=
+      cudaSuccess)
     return check_launch("chol_rows smem attribute");
   const unsigned grid = unsigned((rows + ROWS_WARPS * RW - 1) / (ROWS_WARPS * RW));
-  chol_rows_kernel<RW><<<grid, ROWS_WARPS * 32, smem, st>>>(LU, int(R), G, rows, info);
+  chol_rows_kernel<RW, DB><<<grid, ROWS_WARPS * 32, smem, st>>>(LU, int(R), G, rows, info);
   return check_launch("chol_rows");
 }
 
@@ -619,7 +606,8 @@ static int chol_rows(const double* LU, int64_t R, double* G, int64_t rows, const
   if (rows <= 0) return CPK_OK;
   // 4 rows per warp: measured against 2 and 1 (fewer CTAs, but each strip
   // element feeds 4 chains; R = 256: 258 / 262 / 282 us at 128 rows)
-  return chol_rows_launch<4>(LU, R, G, rows, info, st);
+  if (rows_smem(R, 4, true) <= 227 * 1024) return chol_rows_launch<4, true>(LU, R, G, rows, info, st);
+  return chol_rows_launch<4, false>(LU, R, G, rows, info, st);
 }
 
 struct SolverCtx {
