@@ -121,3 +121,33 @@ def test_singular_gamma_takes_a_regularized_rung(monkeypatch):
     for blk in (slice(0, 20), slice(20, 64)):
         err = np.linalg.norm(x[:, blk] - want[:, blk]) / np.linalg.norm(want[:, blk])
         assert err <= TOL, (blk, err)
+
+
+@pytest.mark.parametrize("cond", [1e6, 1e10])
+def test_ill_conditioned_gamma_residual_matches_cusolver(monkeypatch, cond):
+    """Near-collinear factors make Gamma ill-conditioned; the kernels' block
+    inverses must not cost accuracy against cuSOLVER's substitutions: the
+    residual ||X Gamma - G|| / ||G|| stays within a small factor of it (and of
+    scipy's cho_solve)."""
+    rng = np.random.Generator(np.random.Philox(int(np.log10(cond))))
+    r = 256
+    q, _ = np.linalg.qr(rng.standard_normal((r, r)))
+    gamma = (q * np.logspace(0, -np.log10(cond), r)) @ q.T
+    gamma = (gamma + gamma.T) / 2
+    g = rng.standard_normal((64, r))
+
+    def resid(x):
+        return np.linalg.norm(x @ gamma - g) / np.linalg.norm(g)
+
+    monkeypatch.setenv("CPK_SOLVE", "kernel")
+    xk, ik = run_spec(gamma, g)
+    monkeypatch.setenv("CPK_SOLVE", "cusolver")
+    xc, ic = run_spec(gamma, g)
+    assert ik == 0 and ic == 0
+    rs = resid(oracle._solve_normal(gamma, g))
+    assert resid(xk) <= 10 * max(resid(xc), rs, 1e-15), (resid(xk), resid(xc), rs)
+    want = oracle._solve_normal(gamma, g)
+    # forward error is cond-limited for every method; the kernel's is no worse
+    ek = np.linalg.norm(xk - want) / np.linalg.norm(want)
+    ec = np.linalg.norm(xc - want) / np.linalg.norm(want)
+    assert ek <= 10 * max(ec, 1e-15), (ek, ec)
