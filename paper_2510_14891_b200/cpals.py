@@ -35,7 +35,7 @@ from . import _lib
 import importlib
 
 mt = importlib.import_module(".mttkrp", __package__)  # the submodule (the package re-exports a function of the same name)
-from ._device import EventTimer, require_cuda, stream_ptr, workspace
+from ._device import require_cuda, stream_ptr, workspace
 from .dtensor import DenseTensor
 from .errors import ParameterError
 from .kruskal import KruskalTensor, gram, hadamard

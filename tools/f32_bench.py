@@ -14,7 +14,7 @@ import torch
 
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 import paper_2510_14891_b200 as ck  # noqa: E402
-from paper_2510_14891_b200.mttkrp import MttkrpPlan, Variant, mttkrp_device  # noqa: E402
+from paper_2510_14891_b200.mttkrp import mttkrp_device  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--dims", type=int, nargs="+", default=[1024, 1024, 1024])

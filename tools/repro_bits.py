@@ -12,7 +12,6 @@ import torch
 
 ROOT = Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT))
-import paper_2510_14891_b200 as ck  # noqa: E402
 from paper_2510_14891_b200 import harness  # noqa: E402
 from paper_2510_14891_b200.mttkrp import MttkrpPlan, Variant, mttkrp_device, resolve_plan  # noqa: E402
 
