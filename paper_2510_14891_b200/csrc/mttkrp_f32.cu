@@ -13,9 +13,9 @@
 //                      running sum, 384 of 512 columns);
 //                      one lane issues the UMMAs
 //   warps 2-9          transform: Y and Z into "3xTF32" operands, each value
-//                      v split as hi = rna_tf32(v), lo = rna_tf32(v - hi), in
-//                      the K-major SWIZZLE_128B layout UMMA reads (2 operand
-//                      stages)
+//                      v split as hi = v's top 11 significand bits (exactly
+//                      a TF32, tf32_hi), lo = v - hi (exact), in the K-major
+//                      SWIZZLE_128B layout UMMA reads (2 operand stages)
 //   warps 10-17        drain: the tensor core's fp32 accumulation truncates,
 //                      a bias that grows with the number of accumulations
 //                      (1.1e-4 after ~4k MMAs into one accumulator), so the
@@ -126,11 +126,6 @@ __device__ __forceinline__ void tma(void* dst, const CUtensorMap* map, uint64_t*
   else
     asm volatile("cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6, %7}], [%2];\n"
                  ::"r"(d), "l"(m), "r"(b), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]) : "memory");
-}
-__device__ __forceinline__ float rna_tf32(float x) {
-  uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-  return __uint_as_float(r);
 }
 // K-major SWIZZLE_128B UMMA operand descriptor (rows of 128 B, 8-row atoms)
 __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
