@@ -16,10 +16,14 @@ namespace cpk {
 
 // ---------------------------------------------------------------- Gram
 // A^T A for A (rows x R, row-major, lda): 64x64 output tiles, 256 threads with
-// 4x4 register micro-tiles, rows staged 16 at a time.  Only tiles on or above
-// the diagonal are launched; every (a <= b) entry is written to both (a, b)
-// and (b, a) -- exact symmetry as kruskal.gram (kruskal.py:110-114).
-constexpr int GT = 64, GK = 16;
+// 4x4 register micro-tiles, rows staged GK at a time with cp.async into two
+// buffers (the next slab loads behind the current slab's FMAs; a plain
+// load-then-sync loop waited out the L2 latency every 16 rows: c3's 128 x 256
+// Gram took ~30 us).  Only tiles on or above the diagonal are launched; every
+// (a <= b) entry is written to both (a, b) and (b, a) -- exact symmetry as
+// kruskal.gram (kruskal.py:110-114).  Each entry sums its rows in order.
+constexpr int GT = 64, GK = 32, GLD = GT + 1;
+constexpr size_t GRAM_SMEM = size_t(2) * 2 * GK * GLD * sizeof(double);
 
 __global__ void __launch_bounds__(256) gram_kernel(const double* __restrict__ A, int64_t rows, int64_t R,
                                                    int64_t lda, double* __restrict__ G) {
@@ -31,32 +35,48 @@ __global__ void __launch_bounds__(256) gram_kernel(const double* __restrict__ A,
     ++ti;
   }
   const int64_t tj = ti + b;
-  __shared__ double sa[GK][GT + 1], sb[GK][GT + 1];
+  extern __shared__ double gsm[];  // [buf][panel a/b][GK][GLD]
   const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
   double acc[4][4] = {};
   const int64_t a0 = ti * GT, b0 = tj * GT;
-  for (int64_t r0 = 0; r0 < rows; r0 += GK) {
+  auto issue = [&](int64_t r0, int buf) {
+    double* sa = gsm + buf * 2 * GK * GLD;
+    double* sb = sa + GK * GLD;
     for (int e = threadIdx.x; e < GK * GT; e += 256) {
       const int kr = e / GT, c = e % GT;
       const int64_t r = r0 + kr;
-      sa[kr][c] = (r < rows && a0 + c < R) ? A[r * lda + a0 + c] : 0.0;
-      sb[kr][c] = (r < rows && b0 + c < R) ? A[r * lda + b0 + c] : 0.0;
+      const bool oka = r < rows && a0 + c < R, okb = r < rows && b0 + c < R;
+      cp_async8(sa + kr * GLD + c, oka ? A + r * lda + a0 + c : A, oka ? 8 : 0);
+      cp_async8(sb + kr * GLD + c, okb ? A + r * lda + b0 + c : A, okb ? 8 : 0);
+    }
+    cp_async_commit();
+  };
+  issue(0, 0);
+  int buf = 0;
+  for (int64_t r0 = 0; r0 < rows; r0 += GK, buf ^= 1) {
+    if (r0 + GK < rows) {
+      issue(r0 + GK, buf ^ 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
     }
     __syncthreads();
-#pragma unroll
+    const double* sa = gsm + buf * 2 * GK * GLD;
+    const double* sb = sa + GK * GLD;
+#pragma unroll 8
     for (int kr = 0; kr < GK; ++kr) {
       double x[4], y[4];
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
-        x[i] = sa[kr][ty + 16 * i];
-        y[i] = sb[kr][tx + 16 * i];
+        x[i] = sa[kr * GLD + ty + 16 * i];
+        y[i] = sb[kr * GLD + tx + 16 * i];
       }
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j) acc[i][j] = fma(x[i], y[j], acc[i][j]);
     }
-    __syncthreads();
+    __syncthreads();  // this buffer is refilled two slabs on
   }
 #pragma unroll
   for (int i = 0; i < 4; ++i)
@@ -145,19 +165,33 @@ __global__ void __launch_bounds__(1024) fit_terms_kernel(const double* __restric
   __shared__ double sh[1024];
   // lam^T (H lam): warp a-rows, lanes stride the (coalesced) columns, so the
   // loads are independent of the accumulation chain (H is symmetric)
+  // (one CTA, so every loop keeps several loads in flight: independent
+  // partial sums, combined in a fixed order)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double s0 = 0.0;
   for (int64_t a = warp; a < R; a += 32) {
-    double v = 0.0;
-    for (int64_t b = lane; b < R; b += 32) v = fma(H[a * R + b], lam[b], v);
-    s0 = fma(lam[a], v, s0);
+    double v[4] = {0.0, 0.0, 0.0, 0.0};
+    int64_t b = lane;
+    for (; b + 96 < R; b += 128)
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = fma(H[a * R + b + 32 * u], lam[b + 32 * u], v[u]);
+    for (; b < R; b += 32) v[0] = fma(H[a * R + b], lam[b], v[0]);
+    s0 = fma(lam[a], (v[0] + v[1]) + (v[2] + v[3]), s0);
   }
   double s1 = 0.0;
-  if (G && A)
-    for (int64_t idx = threadIdx.x; idx < rows * R; idx += 1024) {
-      const int64_t j = idx % R;
-      s1 = fma(G[idx] * lam[j], A[idx], s1);
-    }
+  if (G && A) {
+    double p[4] = {0.0, 0.0, 0.0, 0.0};
+    const int64_t n = rows * R;
+    int64_t idx = threadIdx.x;
+    for (; idx + 3 * 1024 < n; idx += 4 * 1024)
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t i = idx + 1024 * u;
+        p[u] = fma(G[i] * lam[i % R], A[i], p[u]);
+      }
+    for (; idx < n; idx += 1024) p[0] = fma(G[idx] * lam[idx % R], A[idx], p[0]);
+    s1 = (p[0] + p[1]) + (p[2] + p[3]);
+  }
   const double t0 = block_sum<1024>(s0, sh);
   const double t1 = block_sum<1024>(s1, sh);
   if (threadIdx.x == 0) {
@@ -640,7 +674,9 @@ extern "C" int cpk_gram_f64(const double* A, int64_t rows, int64_t rank, int64_t
   if (!A || !gram) return fail(CPK_ERR_PARAM, "NULL pointer");
   if (rows < 1 || rank < 1 || lda < rank) return fail(CPK_ERR_SHAPE, "bad gram shape");
   const int64_t nt = (rank + GT - 1) / GT;
-  gram_kernel<<<unsigned(nt * (nt + 1) / 2), 256, 0, as_stream(stream)>>>(A, rows, rank, lda, gram);
+  if (cudaFuncSetAttribute(gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(GRAM_SMEM)) != cudaSuccess)
+    return check_launch("gram smem attribute");
+  gram_kernel<<<unsigned(nt * (nt + 1) / 2), 256, GRAM_SMEM, as_stream(stream)>>>(A, rows, rank, lda, gram);
   return check_launch("gram");
 }
 
