@@ -150,14 +150,90 @@ __device__ __forceinline__ void tma_load(void* dst, const CUtensorMap* map, uint
 // becomes the only limit.  Each 8-deep k block runs as two k-steps, even k
 // then odd k (the contraction order is free), so on the K-major swizzled
 // panels one LDS.128 yields a thread's A fragments for both steps.
+// o-group accumulation (OG): a chunk's Khatri-Rao rows are A_f rows times
+// P_o, the product of the o-rows, and P_o only changes when the o-digits do
+// -- every chunks_per_f chunks (an "o-group").  So the consumers run their
+// DMMAs on the raw A_f rows and, at the end of each o-group, fold the
+// group's accumulators into a running total kept in TMEM: total += acc o P_o.
+// The same FP64 work as scaling every staged row, but issued by the
+// consumers themselves at group ends instead of by the producer warps,
+// whose DMULs starved behind the DMMAs and held up stages (c3: consumers
+// waited ~6 % on `full`).  TMEM: 256 columns; warp w uses lanes
+// 32 (w % 4).. and columns 128 (w / 4).. (its 64 doubles as 128 words).
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,"
+      "%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+        "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]),
+        "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
+        "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,"
+      "%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};\n" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+      "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]), "r"(v[16]), "r"(v[17]), "r"(v[18]),
+      "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]),
+      "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
+
+// total (TMEM) += acc o P for one o-group, acc := 0.  p_s: the stage's o-rows
+// (NO x BN); first: the total is still empty (no TMEM read).
+template <int NO, int BN>
+__device__ __forceinline__ void og_flush(double (&acc)[4][8][2], uint32_t tbase, const double* p_s, int wn0, int lk,
+                                         bool first) {
+  double pj[8][2];
+#pragma unroll
+  for (int nf = 0; nf < 8; ++nf) {
+    double2 v = *reinterpret_cast<const double2*>(p_s + wn0 + nf * 8 + 2 * lk);
+#pragma unroll
+    for (int i = 1; i < NO; ++i) {
+      const double2 w = *reinterpret_cast<const double2*>(p_s + i * BN + wn0 + nf * 8 + 2 * lk);
+      v.x *= w.x;
+      v.y *= w.y;
+    }
+    pj[nf][0] = v.x;
+    pj[nf][1] = v.y;
+  }
+#pragma unroll
+  for (int mf = 0; mf < 4; ++mf) {
+    uint32_t t[32];
+    if (!first) {
+      tmem_ld32(tbase + mf * 32, t);
+      tmem_wait_ld();
+    }
+#pragma unroll
+    for (int nf = 0; nf < 8; ++nf)
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {
+        const int w = (nf * 2 + v) * 2;
+        const double old = first ? 0.0 : __hiloint2double(int(t[w + 1]), int(t[w]));
+        const double nw = fma(acc[mf][nf][v], pj[nf][v], old);
+        t[w] = uint32_t(__double2loint(nw));
+        t[w + 1] = uint32_t(__double2hiint(nw));
+        acc[mf][nf][v] = 0.0;
+      }
+    tmem_st32(tbase + mf * 32, t);
+  }
+  tmem_wait_st();
+}
+
 // The main loop over a CTA's chunks.  TAIL: the warp's 64 columns straddle
 // the rank R, so only the first nf_act 8-column fragments do math (the rank
 // tail of R = 2000 at tile 64 is 16 columns: 2 of 8 fragments).
-template <bool KMAJ, bool TAIL, int BM, int BN, int BK, int STAGE_BYTES, int A_BYTES>
+template <bool KMAJ, bool TAIL, bool OG, int NO, int BM, int BN, int BK, int STAGE_BYTES, int A_BYTES>
 __device__ __forceinline__ void ws_dmma_loop(double (&acc)[4][8][2], const uint8_t* smem, uint64_t* full,
                                              uint64_t* empty, int nst, int stages, int wm0, int wn0, int lane,
-                                             int nf_act) {
+                                             int nf_act, uint32_t tbase, int64_t q0, int64_t chunks_per_f) {
   const int lr = lane >> 2, lk = lane & 3;
+  bool first = true;
+  int64_t qf = OG ? q0 % chunks_per_f : 0;  // position inside the o-group
   for (int it = 0; it < nst; ++it) {
     const int s = it % stages;
     mbar_wait(&full[s], (it / stages) & 1);
@@ -201,15 +277,22 @@ __device__ __forceinline__ void ws_dmma_loop(double (&acc)[4][8][2], const uint8
             dmma_8x8x4(acc[mf][nf], a[mf][ph], b[nf][ph]);
           }
     }
+    if constexpr (OG) {
+      if (++qf == chunks_per_f || it == nst - 1) {  // o-group ends: fold it into the total
+        og_flush<NO, BN>(acc, tbase, reinterpret_cast<const double*>(st + A_BYTES + BK * BN * 8), wn0, lk, first);
+        first = false;
+        qf = 0;
+      }
+    }
     __syncwarp();
     if ((lane & 31) == 0) mbar_arrive(&empty[s]);
   }
 }
 
-template <bool KMAJ, int BM, int BN, int BK, int STAGE_BYTES, int A_BYTES>
+template <bool KMAJ, bool OG, int NO, int BM, int BN, int BK, int STAGE_BYTES, int A_BYTES>
 __device__ __forceinline__ void ws_consume_dmma(const uint8_t* smem, uint64_t* full, uint64_t* empty, int nst,
                                                 const WsParams& p, int n0, int j0, int warp, int lane,
-                                                int stages) {
+                                                int stages, uint32_t tmem, int64_t q0) {
   constexpr int WARPS_N = BN / 64;
   const int wm0 = (warp / WARPS_N) * 32, wn0 = (warp % WARPS_N) * 64;
   const int lr = lane >> 2, lk = lane & 3;
@@ -220,12 +303,31 @@ __device__ __forceinline__ void ws_consume_dmma(const uint8_t* smem, uint64_t* f
     for (int j = 0; j < 8; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
   const int nf_act = (p.R - j0 - wn0 + 7) >> 3;  // warp-uniform
+  // this warp's TMEM window: lanes 32 (warp % 4).., columns 128 (warp / 4)..
+  const uint32_t tbase = tmem + (uint32_t((warp & 3) * 32) << 16) + uint32_t((warp >> 2) * 128);
   if (nf_act >= 8)
-    ws_dmma_loop<KMAJ, false, BM, BN, BK, STAGE_BYTES, A_BYTES>(acc, smem, full, empty, nst, stages, wm0, wn0, lane,
-                                                                8);
+    ws_dmma_loop<KMAJ, false, OG, NO, BM, BN, BK, STAGE_BYTES, A_BYTES>(acc, smem, full, empty, nst, stages, wm0, wn0,
+                                                                        lane, 8, tbase, q0, p.chunks_per_f);
   else
-    ws_dmma_loop<KMAJ, true, BM, BN, BK, STAGE_BYTES, A_BYTES>(acc, smem, full, empty, nst, stages, wm0, wn0, lane,
-                                                               nf_act);
+    ws_dmma_loop<KMAJ, true, OG, NO, BM, BN, BK, STAGE_BYTES, A_BYTES>(acc, smem, full, empty, nst, stages, wm0, wn0,
+                                                                       lane, nf_act, tbase, q0, p.chunks_per_f);
+  if constexpr (OG) {
+    if (nst > 0) {  // the total -> acc registers for the epilogue
+#pragma unroll
+      for (int mf = 0; mf < 4; ++mf) {
+        uint32_t t[32];
+        tmem_ld32(tbase + mf * 32, t);
+        tmem_wait_ld();
+#pragma unroll
+        for (int nf = 0; nf < 8; ++nf)
+#pragma unroll
+          for (int v = 0; v < 2; ++v) {
+            const int w = (nf * 2 + v) * 2;
+            acc[mf][nf][v] = __hiloint2double(int(t[w + 1]), int(t[w]));
+          }
+      }
+    }
+  }
 
   double* out = p.out + int64_t(blockIdx.z + p.z0) * p.out_split_stride;
   const bool fold = p.lam != nullptr;
@@ -302,6 +404,10 @@ __global__ void __launch_bounds__(WS_THREADS, 1) mttkrp_f64_ws_sm100(const __gri
   uint64_t* full = bar + STAGES;        // Khatri-Rao rows formed
   uint64_t* empty = bar + 2 * STAGES;   // consumers done
 
+  // DMMA tiles with o-modes fold the o-row product per o-group (OG, see
+  // og_flush); the producer warps then only issue TMA
+  constexpr bool OG = TM == 0 && NO > 0;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 3 * STAGES);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t q0 = int64_t(blockIdx.z + p.z0) * p.chunks_per_split;
   const int nst = int(min(p.n_chunks, q0 + p.chunks_per_split) - q0);
@@ -316,7 +422,19 @@ __global__ void __launch_bounds__(WS_THREADS, 1) mttkrp_f64_ws_sm100(const __gri
     }
     fence_barrier_init();
   }
+  if constexpr (OG) {
+    if (warp == 0) {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;\n" ::"r"(smem_u32(tslot)));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  }
   __syncthreads();
+  uint32_t tmem = 0;
+  if constexpr (OG) {
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    tmem = *tslot;
+  }
 
   if (warp >= WS_CONSUMERS) {
     // ================================================================ producer
@@ -398,6 +516,11 @@ __global__ void __launch_bounds__(WS_THREADS, 1) mttkrp_f64_ws_sm100(const __gri
     };
     if (issuer)
       for (int t = 0; t < STAGES - 1 && t < nst; ++t) issue(t);
+    if constexpr (OG) {  // nothing to scale: just keep the TMA ring full
+      if (issuer)
+        for (int t = STAGES - 1; t < nst; ++t) issue(t);
+      return;
+    }
     constexpr int PAIRS = BN / 2;                  // column pairs per row
     constexpr int ROW_STEP = 128 / PAIRS;          // producer threads per pair
     const int pair = pt % PAIRS, row0 = pt / PAIRS;
@@ -455,8 +578,17 @@ __global__ void __launch_bounds__(WS_THREADS, 1) mttkrp_f64_ws_sm100(const __gri
   // ================================================================== consumers
   setmaxnreg_inc<WsRegs<TM>::consumer>();
   if constexpr (TM == 0) {
-    ws_consume_dmma<KMAJ, BM, BN, BK, C::STAGE_BYTES, C::A_BYTES>(smem, full, empty, nst, p, n0, j0, warp, lane,
-                                                                  STAGES);
+    // with OG the consumers take a stage as soon as its bytes land
+    ws_consume_dmma<KMAJ, OG, NO, BM, BN, BK, C::STAGE_BYTES, C::A_BYTES>(smem, OG ? full_tma : full, empty, nst, p,
+                                                                          n0, j0, warp, lane, STAGES, tmem, q0);
+    if constexpr (OG) {  // all consumers are done with TMEM before warp 0 frees it
+      asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+      asm volatile("bar.sync 1, %0;\n" ::"n"(WS_CONSUMERS * 32) : "memory");
+      if (warp == 0) {
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;\n" ::"r"(tmem));
+      }
+    }
     return;
   }
   if constexpr (TM != 0) {
