@@ -76,6 +76,12 @@ typedef struct cpk_plan {
 #define CPK_MERGE_NONE (-1)
 #define CPK_MERGE_PREV 1
 #define CPK_MERGE_NEXT 2
+/* KR: for d >= 4, the two fastest non-k modes run as one virtual mode whose
+ * factor is their Khatri-Rao product, materialized in the workspace (longer
+ * o-groups for the kernel's per-group scaling).  AUTO picks it for automatic
+ * plans when those modes are short and the factor small; resolve reports
+ * KR, and passing it back runs the same merged problem. */
+#define CPK_MERGE_KR 3
 
 /* engine: AUTO picks the warp-specialized TMA kernel with DMMA consumers
  * when the problem is aligned (even I_0 and leading dimensions, 16-byte

@@ -448,6 +448,60 @@ __global__ static void merged_contract_f64(const double* __restrict__ gp, int64_
   }
 }
 
+// Khatri-Rao merge of the two fastest non-k modes.  The DMMA kernel folds
+// the o-row product into a TMEM total once per o-group (the chunks_per_f =
+// I_f / BK chunks that share the o-digits, mttkrp_ws.cu og_flush), so short
+// o-groups cost flushes: c3 (128^4) has 4 chunks per group.  For d >= 4 the
+// two fastest non-k modes f and f + 1 (adjacent, both before the last mode)
+// are merged into one virtual mode whose factor W[i_f + I_f i_g, :] =
+// A_f[i_f, :] o A_g[i_g, :] is materialized in the workspace (c3: 128 x 128
+// rows x R = 32 MB); the (d-1)-way problem then has I_f I_g / BK chunks per
+// o-group.  The slowest mode is untouched, so streamed (landed) calls keep
+// their slab contract.  Automatic plans only; off when a small-mode merge
+// applies or W would exceed kKrMergeBytes.
+constexpr size_t kKrMergeBytes = size_t(256) << 20;
+constexpr int64_t kKrMergeMinGroup = 64;  // merge while an o-group is shorter than this many chunks
+
+struct KrMerge {
+  bool on = false;
+  int f = -1, d2 = 0, mode2 = 0;
+  int64_t dims2[CPK_MAX_MODES] = {};
+  int64_t ldw = 0;
+  size_t w_bytes = 0;
+};
+
+static KrMerge choose_kr_merge(const Problem& pr, const cpk_plan* plan_in) {
+  KrMerge m;
+  const bool forced = plan_in && plan_in->merge == CPK_MERGE_KR;
+  if (!forced && (!plan_is_auto(plan_in) || (plan_in && plan_in->merge != CPK_MERGE_AUTO))) return m;
+  const int f = pr.f, g = f + 1;
+  if (pr.d < 4 || f < 0 || g == pr.k || g >= pr.d - 1) return m;
+  if (!forced && pr.dims[f] / 16 >= kKrMergeMinGroup) return m;  // o-groups already long (BK >= 16)
+  m.ldw = (pr.R + 1) & ~int64_t(1);
+  m.w_bytes = size_t(pr.dims[f]) * size_t(pr.dims[g]) * size_t(m.ldw) * sizeof(double);
+  if (!forced && m.w_bytes > kKrMergeBytes) return m;
+  m.on = true;
+  m.f = f;
+  m.d2 = pr.d - 1;
+  for (int i = 0, j = 0; i < pr.d; ++i) {
+    if (i == g) continue;
+    m.dims2[j++] = i == f ? pr.dims[f] * pr.dims[g] : pr.dims[i];
+  }
+  m.mode2 = pr.k < f ? pr.k : pr.k - 1;
+  return m;
+}
+
+__global__ static void kr_pair_f64(const double* __restrict__ Af, int64_t ldf, const double* __restrict__ Ag,
+                                   int64_t ldg, int64_t If, int64_t rows, int64_t R, double* __restrict__ W,
+                                   int64_t ldw) {
+  for (int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; idx < rows * R;
+       idx += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t row = idx / R, j = idx - row * R;
+    const int64_t i_g = row / If, i_f = row - i_g * If;
+    W[row * ldw + j] = Af[i_f * ldf + j] * Ag[i_g * ldg + j];
+  }
+}
+
 extern "C" int cpk_plan_resolve(int d, const int64_t* dims, int mode, int64_t rank, cpk_plan* plan) {
   if (!plan) return fail(CPK_ERR_PARAM, "plan is NULL");
   Problem pr;
@@ -461,9 +515,18 @@ extern "C" int cpk_plan_resolve(int d, const int64_t* dims, int mode, int64_t ra
     plan->merge = mg.a < mode ? CPK_MERGE_PREV : CPK_MERGE_NEXT;
     return resolve(p2, plan);
   }
-  if (plan->merge != CPK_MERGE_AUTO && plan->merge != CPK_MERGE_NONE)
+  if (plan->merge != CPK_MERGE_AUTO && plan->merge != CPK_MERGE_NONE && plan->merge != CPK_MERGE_KR)
     return fail(CPK_ERR_PARAM, "merge %d impossible for mode %d of a %d-way tensor", plan->merge, mode, d);
-  plan->merge = CPK_MERGE_NONE;
+  const KrMerge km = choose_kr_merge(pr, plan);
+  if (plan->merge == CPK_MERGE_KR && !km.on)
+    return fail(CPK_ERR_PARAM, "Khatri-Rao merge impossible for mode %d of a %d-way tensor", mode, d);
+  plan->merge = km.on ? CPK_MERGE_KR : CPK_MERGE_NONE;
+  if (km.on) {  // the plan of the (d-1)-way problem with f and f + 1 merged
+    Problem p2;
+    rc = make_problem(km.d2, km.dims2, km.mode2, rank, &p2);
+    if (rc) return rc;
+    return resolve(p2, plan);
+  }
   return resolve(pr, plan);
 }
 
@@ -482,6 +545,17 @@ extern "C" int cpk_mttkrp_workspace_bytes(int d, const int64_t* dims, int mode, 
     rc = resolve(p2, &q);
     if (rc) return rc;
     *bytes = align256(ws_bytes_for(p2, q)) + merged_out_bytes(pr, mg);
+    return CPK_OK;
+  }
+  const KrMerge km = choose_kr_merge(pr, plan);
+  if (km.on) {
+    Problem p2;
+    rc = make_problem(km.d2, km.dims2, km.mode2, rank, &p2);
+    if (rc) return rc;
+    cpk_plan q = *plan;
+    rc = resolve(p2, &q);
+    if (rc) return rc;
+    *bytes = align256(ws_bytes_for(p2, q)) + km.w_bytes;
     return CPK_OK;
   }
   cpk_plan p = *plan;
@@ -582,6 +656,41 @@ static int mttkrp_impl(const double* y, int d, const int64_t* dims, int mode, co
     merged_contract_f64<<<blocks, 256, 0, st>>>(gp, pr.Ik, pr.dims[mg.a], rank, mg.a < mode ? 1 : 0, factors[mg.a],
                                                 ld ? ld[mg.a] : rank, G, ldg);
     return check_launch("merged_contract");
+  }
+  if (allow_merge) {
+    const KrMerge km = choose_kr_merge(pr, plan_in);
+    if (!km.on && plan_in && plan_in->merge == CPK_MERGE_KR)
+      return fail(CPK_ERR_PARAM, "Khatri-Rao merge impossible for mode %d of a %d-way tensor", mode, d);
+    if (km.on) {
+      Problem p2;
+      rc = make_problem(km.d2, km.dims2, km.mode2, rank, &p2);
+      if (rc) return rc;
+      cpk_plan q = plan_in ? *plan_in : cpk_plan{0, 0, 0, 0, 0, 0, 0, 0};
+      rc = resolve(p2, &q);
+      if (rc) return rc;
+      const size_t inner = align256(ws_bytes_for(p2, q));
+      if (!workspace || ws_bytes < inner + km.w_bytes)
+        return fail(CPK_ERR_RESOURCE, "Khatri-Rao merge workspace needs %zu bytes, got %zu", inner + km.w_bytes,
+                    ws_bytes);
+      double* W = reinterpret_cast<double*>(static_cast<char*>(workspace) + inner);
+      const int f = km.f, g = f + 1;
+      const int64_t wrows = dims[f] * dims[g];
+      const unsigned blocks = unsigned(std::max<int64_t>(1, std::min<int64_t>(ceil_div(wrows * rank, 256), 148 * 8)));
+      kr_pair_f64<<<blocks, 256, 0, st>>>(factors[f], ld ? ld[f] : rank, factors[g], ld ? ld[g] : rank, dims[f],
+                                          wrows, rank, W, km.ldw);
+      rc = check_launch("kr_pair");
+      if (rc) return rc;
+      const double* f2[CPK_MAX_MODES];
+      int64_t ld2[CPK_MAX_MODES];
+      for (int i = 0, j = 0; i < d; ++i) {
+        if (i == g) continue;
+        f2[j] = i == f ? W : factors[i];
+        ld2[j] = i == f ? km.ldw : (ld ? ld[i] : rank);
+        ++j;
+      }
+      return mttkrp_impl(y, km.d2, km.dims2, km.mode2, f2, ld2, lam, rank, G, ldg, &q, workspace, inner, stream,
+                         landed_lo, landed_hi, false);
+    }
   }
   if (pr.n_o > 3)
     return fail(CPK_ERR_PARAM, "order d=%d > 5 is not supported by the sm_100a kernel", d);
