@@ -638,8 +638,13 @@ static int chol_rows_launch(const double* LU, int64_t R, double* G, int64_t rows
 
 static int chol_rows(const double* LU, int64_t R, double* G, int64_t rows, const int* info, cudaStream_t st) {
   if (rows <= 0) return CPK_OK;
-  // 4 rows per warp: measured against 2 and 1 (fewer CTAs, but each strip
-  // element feeds 4 chains; R = 256: 258 / 262 / 282 us at 128 rows)
+  // few rows: one row per warp (more CTAs, the strips' loads are hidden);
+  // many: 4 per warp (each strip element feeds 4 chains).  R = 256
+  // (tools/solve_bench.py, factor + rows): 128 rows 233 / 244 / 252 us for
+  // RW = 1 / 2 / 4, 1024 rows 285 / 244 / 252, 4096 rows 542 / 430 / 324.
+  if (rows <= 256 && rows_smem(R, 1, true) <= 227 * 1024) return chol_rows_launch<1, true>(LU, R, G, rows, info, st);
+  if (rows <= 1024 && rows_smem(R, 2, true) <= 227 * 1024)
+    return chol_rows_launch<2, true>(LU, R, G, rows, info, st);
   if (rows_smem(R, 4, true) <= 227 * 1024) return chol_rows_launch<4, true>(LU, R, G, rows, info, st);
   return chol_rows_launch<4, false>(LU, R, G, rows, info, st);
 }
