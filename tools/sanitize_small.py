@@ -1,0 +1,25 @@
+"""Small runs of every new device path, for compute-sanitizer (memcheck /
+racecheck): 4-way MTTKRP (Khatri-Rao merge + o-group TMEM accumulation),
+3-way with rank tails, the solve kernels (both buffering modes), CP-ALS."""
+import os
+import sys
+from pathlib import Path
+
+import numpy as np
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import paper_2510_14891_b200 as ck  # noqa: E402
+from paper_2510_14891_b200.mttkrp import MttkrpPlan, Variant  # noqa: E402
+
+rng = np.random.Generator(np.random.Philox(5))
+for dims, r in (((32, 24, 20, 6), 70), ((40, 36, 34), 130), ((6, 5, 4, 7, 3), 9)):
+    y = ck.DenseTensor(dims, rng.random(int(np.prod(dims))))
+    m = ck.KruskalTensor(np.ones(r), [rng.random((n, r)) for n in dims])
+    for k in range(len(dims)):
+        ck.run(y, m, MttkrpPlan(Variant.B200, k))
+y = ck.DenseTensor((20, 18, 16, 6), rng.random(20 * 18 * 16 * 6))
+ck.cp_als(y, ck.AlsConfig(rank=40, max_iters=3, tol=0.0), graph=False)
+os.environ["CPK_SOLVE"] = "kernel"
+ck.cp_als(ck.DenseTensor((24, 20, 18), rng.random(24 * 20 * 18)), ck.AlsConfig(rank=300, max_iters=2, tol=0.0),
+          graph=False)
+print("ok")
