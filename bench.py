@@ -183,7 +183,10 @@ def run_b200(args):
         local = local % torch.cuda.device_count()
         torch.cuda.set_device(local)
         if backend == "nccl":
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+            # CUDA tensors go over NCCL; the group also carries a gloo
+            # backend so a stray CPU tensor could never hang the run (the
+            # sharded sweep's communicator is strict and raises on one)
+            dist.init_process_group("cpu:gloo,cuda:nccl", device_id=torch.device("cuda", local))
         else:
             dist.init_process_group(backend)
     else:
@@ -435,7 +438,7 @@ def run_b200(args):
     c5 = None
     if args.c5_iters > 0:
         try:
-            c5 = bench_c5(dev, args.c5_iters)
+            c5 = bench_c5(dev, args.c5_iters, tuple(int(x) for x in args.c5_dims.split(",")), args.c5_rank)
         except Exception as exc:  # report, do not lose the headline line
             c5 = {"error": f"{type(exc).__name__}: {exc}"[:300]}
         torch.cuda.empty_cache()
@@ -529,39 +532,43 @@ def bench_cpals(ck, dev, iters):
     return res
 
 
-def bench_c5(dev, iters):
+def bench_c5(dev, iters, dims=(4096, 2048, 2048), r=512):
     """Sharded CP-ALS at config 5 (4096 x 2048 x 2048, R = 512): seconds per
-    sweep, max over ranks.  Each rank generates its mode-0 slab on its GPU."""
+    sweep (CUDA events on each rank, max over ranks).  Each rank generates
+    its mode-0 slab on its GPU; the sweep is the single-GPU engine with the
+    NCCL exchange steps (sharded.py)."""
     import torch
 
     from paper_2510_14891_b200 import sharded
     from paper_2510_14891_b200.cpals import AlsConfig
 
-    dims, r = (4096, 2048, 2048), 512
-    comm = sharded.Comm()
+    comm = sharded.Comm(device=dev)
     part = sharded.partition_for(dims, comm.world)
     y = sharded.uniform_slab(part, comm.rank, seed=SEED, device=dev)
-    sharded.cp_als_sharded(y, part, AlsConfig(rank=r, tol=0.0, max_iters=1, seed=0), comm, gather=False)
-    comm.seconds, comm.bytes = 0.0, 0
+    sharded.cp_als_sharded(y, part, AlsConfig(rank=r, tol=0.0, max_iters=1, seed=0), comm, gather=False)  # warm-up
+    comm.reset()
     _, tr = sharded.cp_als_sharded(y, part, AlsConfig(rank=r, tol=0.0, max_iters=iters, seed=0), comm,
                                    gather=False)
     sec = statistics.median(tr.sweep_seconds)
     mt = statistics.median(sum(s) for s in tr.mttkrp_seconds)
+    comm_s = tr.comm_seconds / max(1, len(tr.fits))
     if comm.world > 1:
-        t = torch.tensor([sec, mt], dtype=torch.float64, device=dev)
+        t = torch.tensor([sec, mt, comm_s], dtype=torch.float64, device=dev)
         comm.dist.all_reduce(t, op=comm.dist.ReduceOp.MAX)
-        sec, mt = (float(v) for v in t.tolist())
+        sec, mt, comm_s = (float(v) for v in t.tolist())
     del y
-    flops = 3 * 2 * 4096 * 2048 * 2048 * r * 2
+    flops = 3 * algo_flops(dims, r)
     from paper_2510_14891_b200.perfmodel import roofline_seconds
 
     # the sweep's 3 MTTKRPs of the whole tensor at the roofline of this many GPUs
     roof = 3 * roofline_seconds(dims, r) / comm.world
-    return {"config": "c5: 3-way 4096x2048x2048 f64, rank 512, mode-0 block partition", "gpus": comm.world,
-            "iters": iters, "sec_per_iter": sec, "roofline_sec_per_iter": roof, "roofline_frac": roof / sec,
-            "mttkrp_sec_per_iter": mt,
-            "mttkrp_gflops": flops / mt / 1e9, "comm_seconds_total": comm.seconds,
-            "comm_bytes_total": comm.bytes, "fits": tr.fits}
+    return {"config": f"c5: 3-way {'x'.join(map(str, dims))} f64, rank {r}, mode-{part.mode} block partition",
+            "gpus": comm.world, "iters": iters, "sec_per_iter": sec, "roofline_sec_per_iter": roof,
+            "roofline_frac": roof / sec, "mttkrp_sec_per_iter": mt,
+            "mttkrp_gflops": flops / mt / 1e9, "mttkrp_gflops_per_gpu": flops / mt / 1e9 / comm.world,
+            "comm_sec_per_iter": comm_s, "comm_bytes_per_iter": tr.comm_bytes // max(1, len(tr.fits)),
+            "comm_calls_per_iter": tr.comm_calls / max(1, len(tr.fits)), "rollbacks": tr.rollbacks,
+            "timing": "CUDA events per sweep (sweep start -> stats readback), max over ranks", "fits": tr.fits}
 
 
 def main():
@@ -577,6 +584,8 @@ def main():
     ap.add_argument("--f32-steps", type=int, default=2)
     ap.add_argument("--cpals-iters", type=int, default=10)
     ap.add_argument("--c5-iters", type=int, default=3)
+    ap.add_argument("--c5-dims", default="4096,2048,2048", help="CP-ALS leg shape (tests shrink it)")
+    ap.add_argument("--c5-rank", type=int, default=512)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--ref-seconds", type=float, default=0.0, help="reference arm: CPU seconds per step (0 = auto)")

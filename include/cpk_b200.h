@@ -254,8 +254,11 @@ int cpk_fill_uniform_slab_f64(double* x, int d, const int64_t* global_dims,
                               void* stream);
 
 /* DTEN v1 files (dtensor.py:334-382): shape of the file's tensor (header
- * validated as the reference does; FormatError -> CPK_ERR_FORMAT).  dims
- * must hold CPK_MAX_MODES entries. */
+ * validated as the reference does, 1..64 modes; FormatError ->
+ * CPK_ERR_FORMAT).  dims must hold CPK_DTEN_MAX_MODES entries.  Files with
+ * more modes than the kernels take (CPK_MAX_MODES) still load: the limit
+ * applies to the MTTKRP, not to ingest. */
+#define CPK_DTEN_MAX_MODES 64
 int cpk_dten_read_header(const char* path, int* d, int64_t* dims);
 
 /* Load the slab [lo, hi) along `mode` of a DTEN file straight into device

@@ -34,13 +34,17 @@ def stream_ptr(device: torch.device) -> int:
 
 
 def workspace(device: torch.device, nbytes: int, tag: str = "mttkrp") -> torch.Tensor:
-    """Grow-only per-(device, tag) scratch buffer (float64, 256-B aligned).
+    """Grow-only scratch buffer per (device, tag, current stream), float64.
 
-    Reused across calls on the same stream; stream order serializes users.
+    Keyed on the stream, so only calls ordered on one stream share a buffer:
+    stream order serializes them, and calls on other streams (or threads
+    using other streams) get buffers of their own.  A buffer is allocated
+    while its stream is current, so when it grows the caching allocator
+    recycles the old block in that same stream's order.
     """
     if nbytes <= 0:
         return None
-    key = (device.index, tag)
+    key = (device.index, tag, torch.cuda.current_stream(device).cuda_stream)
     with _ws_lock:
         buf = _workspaces.get(key)
         if buf is None or buf.numel() * 8 < nbytes:

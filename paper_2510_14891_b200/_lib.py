@@ -37,6 +37,7 @@ _CODE_TO_EXC = {
 }
 CPK_ERR_NOT_PD = 6
 CPK_MAX_MODES = 8
+CPK_DTEN_MAX_MODES = 64
 CPK_SUMSQ_PARTIALS = 1024
 
 

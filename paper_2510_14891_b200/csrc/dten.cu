@@ -71,7 +71,6 @@ int read_header(int fd, int* d, int64_t* dims, int64_t* data_offset, int64_t* fi
   }
   if (version != kVersion) return fail(CPK_ERR_FORMAT, "unsupported DTEN version %u", version);
   if (nd < 1 || nd > 64) return fail(CPK_ERR_FORMAT, "implausible mode count %u", nd);
-  if (nd > CPK_MAX_MODES) return fail(CPK_ERR_FORMAT, "%u modes: this build supports up to %d", nd, CPK_MAX_MODES);
   std::vector<unsigned char> raw(8 * nd + 4);
   if (!pread_all(fd, raw.data(), raw.size(), 12)) return fail(CPK_ERR_FORMAT, "truncated DTEN dimension block");
   uint32_t etype;
@@ -128,7 +127,7 @@ extern "C" int cpk_dten_load_slab_f64(const char* path, int mode, int64_t lo, in
   f.fd = open(path, O_RDONLY);
   if (f.fd < 0) return fail(CPK_ERR_FORMAT, "cannot open %s", path);
   int d;
-  int64_t dims[CPK_MAX_MODES], data_off, file_bytes;
+  int64_t dims[CPK_DTEN_MAX_MODES], data_off, file_bytes;
   int rc = read_header(f.fd, &d, dims, &data_off, &file_bytes);
   if (rc) return rc;
   if (mode < 0 || mode >= d) return fail(CPK_ERR_INDEX, "mode %d out of range [0, %d]", mode, d - 1);

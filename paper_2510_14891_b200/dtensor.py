@@ -57,10 +57,18 @@ def _is_torch(x) -> bool:
     return isinstance(x, torch.Tensor)
 
 
+def _payload_key(x):
+    """Identity of a payload for cache validation: the object, its buffer
+    address and (torch) its in-place version counter."""
+    if _is_torch(x):
+        return (id(x), x.data_ptr(), x._version)
+    return (id(x), x.__array_interface__["data"][0])
+
+
 class DenseTensor:
     """Dense tensor backed by one flat float64 buffer in first-mode-fastest order."""
 
-    __slots__ = ("dims", "data", "_dev", "_landing", "_even")
+    __slots__ = ("dims", "data", "_dev", "_landing", "_even", "_src")
 
     def __init__(self, dims, data, copy=False):
         self.dims = check_dims(dims)
@@ -84,6 +92,7 @@ class DenseTensor:
         self._dev = arr if (_is_torch(arr) and arr.is_cuda) else None
         self._landing = None  # (slab bounds, copy events) while a streamed upload is in flight
         self._even = None  # zero-padded copy with an even first extent (even_device_data)
+        self._src = _payload_key(arr)  # which payload the cached device copies were made from
 
     @classmethod
     def zeros(cls, dims) -> "DenseTensor":
@@ -128,6 +137,24 @@ class DenseTensor:
     def is_device(self) -> bool:
         return _is_torch(self.data) and self.data.is_cuda
 
+    def _check_cache(self) -> None:
+        """Drop the cached device copies when `data` is no longer the payload
+        they were made from: reassigned, or (torch payloads) modified in
+        place (tensor version counter).  An in-place write into a host
+        *numpy* payload after the first GPU call cannot be seen; call
+        `invalidate()` after one (the reference object holds no cache)."""
+        key = _payload_key(self.data)
+        if key != self._src:
+            self.invalidate()
+            self._src = key
+
+    def invalidate(self) -> None:
+        """Forget every device copy of a host payload (re-uploaded on next use)."""
+        cuda_payload = _is_torch(self.data) and self.data.is_cuda
+        self._dev = self.data.reshape(-1) if cuda_payload else None
+        self._landing = None
+        self._even = None
+
     def device_data(self, device=None, wait: bool = True) -> torch.Tensor:
         """The flat float64 payload on the CUDA device (cached H2D copy).
 
@@ -135,6 +162,7 @@ class DenseTensor:
         wait for it (``wait=False``: the caller orders itself on the slab
         events)."""
         dev = require_cuda(device)
+        self._check_cache()
         if self._dev is not None and self._dev.device == dev:
             if wait and self.landing is not None:
                 torch.cuda.current_stream(dev).wait_event(self._landing[1][-1])
@@ -150,6 +178,7 @@ class DenseTensor:
     def needs_upload(self, device=None) -> bool:
         """True when the payload lives on the host and no device copy is cached."""
         dev = require_cuda(device)
+        self._check_cache()
         return not (self._dev is not None and self._dev.device == dev)
 
     def host_view(self) -> torch.Tensor:
@@ -181,6 +210,7 @@ class DenseTensor:
         gives the same G for every mode k > 0, and G's first I_0 rows for
         k = 0, with A_0 extended by any one row."""
         dev = require_cuda(device)
+        self._check_cache()
         if self._even is None or self._even.device != dev:
             i0 = self.dims[0]
             src = self.device_data(dev).view(-1, i0)
@@ -258,7 +288,7 @@ def read_dten_header(path) -> tuple:
     from . import _lib
 
     d = ctypes.c_int(0)
-    dims = (ctypes.c_int64 * _lib.CPK_MAX_MODES)()
+    dims = (ctypes.c_int64 * _lib.CPK_DTEN_MAX_MODES)()
     _lib.check(_lib.load().cpk_dten_read_header(str(path).encode(), ctypes.byref(d), dims), "DTEN header")
     return tuple(int(dims[i]) for i in range(d.value))
 

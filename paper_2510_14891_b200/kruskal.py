@@ -81,18 +81,39 @@ class KruskalTensor:
         return tuple(int(a.shape[0]) for a in self.factors)
 
     def device_factors(self, device=None):
-        """Device copies (contiguous float64) of all factors, cached."""
+        """Device copies (contiguous float64) of all factors.
+
+        CUDA float64 factors are used in place.  Other torch factors are
+        converted once and the copy is reused while the source tensor is the
+        same object at the same address and version (no in-place write since);
+        numpy factors are uploaded on every call -- they are I_m x R, and the
+        reference packs them on every call too (`pack_factors`,
+        _kernels.py:25-36) -- so reassigning `factors[k]` or writing into
+        one is always seen."""
         dev = require_cuda(device)
         if self._dev is None or self._dev[0] != dev:
-            fs = [_to_device(a, dev) for a in self.factors]
-            self._dev = [dev, fs, None]  # weights copied on first use only
-        return self._dev[1]
+            self._dev = [dev, {}]
+        cache = self._dev[1]
+        return [self._device_copy(cache, ("A", m), a, dev) for m, a in enumerate(self.factors)]
 
     def device_weights(self, device=None):
-        self.device_factors(device)
-        if self._dev[2] is None:
-            self._dev[2] = _to_device(self.weights, self._dev[0])
-        return self._dev[2]
+        dev = require_cuda(device)
+        if self._dev is None or self._dev[0] != dev:
+            self._dev = [dev, {}]
+        return self._device_copy(self._dev[1], "lam", self.weights, dev)
+
+    @staticmethod
+    def _device_copy(cache, slot, a, dev):
+        if not _is_torch(a):
+            cache.pop(slot, None)
+            return _to_device(a, dev)
+        key = (id(a), a.data_ptr(), a._version)
+        hit = cache.get(slot)
+        if hit is not None and hit[0] == key:
+            return hit[1]
+        t = _to_device(a, dev)
+        cache[slot] = (key, t)
+        return t
 
     def hadamard_gram(self, skip=None):
         """(*) of the factor Grams, optionally skipping one mode (kruskal.py:74-83)."""

@@ -55,7 +55,8 @@ def test_b200_arm_multi_rank_path():
     env = dict(os.environ, BENCH_DIST_BACKEND="gloo")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
            "--master-addr=127.0.0.1", "--master-port=29517", str(ROOT / "bench.py"), "--gpus", "2", "--steps",
-           "1", "--warmup", "3", "--e2e-steps", "1", "--c5-iters", "0", "--cpu-seconds", "0.5"]
+           "1", "--warmup", "3", "--e2e-steps", "1", "--c5-iters", "2", "--c5-dims", "96,40,36", "--c5-rank", "16",
+           "--cpu-seconds", "0.5"]
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=1200, cwd=ROOT, env=env)
     assert out.returncode == 0, out.stderr[-3000:]
     lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
@@ -63,3 +64,8 @@ def test_b200_arm_multi_rank_path():
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["value"] > 0 and d["e2e"]["value"] > 0
     assert d["config"]["parallelism"] == "mode-0 block partition x2"
+    # the sharded CP-ALS leg ran through the strict (device-only) communicator
+    c5 = d["cp_als_c5"]
+    assert "error" not in c5, c5
+    assert c5["gpus"] == 2 and c5["sec_per_iter"] > 0 and len(c5["fits"]) == 2
+    assert c5["comm_calls_per_iter"] >= 5 and c5["rollbacks"] == 0

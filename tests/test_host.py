@@ -228,3 +228,18 @@ def test_model_command_text_and_errors(capsys):
         harness.main(["model", "--shape", "4,4", "--modes", "3"])
     with pytest.raises(ck.ParameterError):
         harness.main(["model"])
+
+
+def test_dten_files_with_many_modes_load(tmp_path):
+    """The reference format takes 1..64 modes (dtensor.py:369); ingest is not
+    limited by the kernels' CPK_MAX_MODES (a 12-way file with singleton
+    modes, and a 64-way one, read back whole)."""
+    dims = (3, 1, 2, 1, 1, 2, 1, 1, 1, 1, 2, 1)
+    y = np.arange(float(np.prod(dims)))
+    path = tmp_path / "t12.dten"
+    ck.write_dten(path, ck.DenseTensor(dims, y))
+    assert ck.read_dten_header(path) == dims
+    assert np.array_equal(ck.read_dten(path).data, y)
+    dims64 = (2,) + (1,) * 63
+    ck.write_dten(tmp_path / "t64.dten", ck.DenseTensor(dims64, np.array([1.0, 2.0])))
+    assert ck.read_dten_header(tmp_path / "t64.dten") == dims64

@@ -12,7 +12,7 @@ import torch
 import paper_2510_14891_b200 as ck
 from conftest import instances, rng_for
 from oracle import gen, oracle
-from paper_2510_14891_b200.mttkrp import MttkrpPlan, Variant
+from paper_2510_14891_b200.mttkrp import MttkrpPlan, Variant, mttkrp_device
 
 pytestmark = pytest.mark.gpu
 TOL = 1e-10
@@ -509,3 +509,66 @@ def test_random_shapes_every_mode_fuzz():
             worst = max(worst, err)
             assert err <= TOL, (case, dims, r, k, err)
     assert worst < 1e-13
+
+
+def test_device_caches_follow_the_payloads():
+    """Reassigning or mutating factors / the tensor payload after a first GPU
+    call is seen by the next call (the reference objects hold no cache)."""
+    dims, r = (12, 10, 8), 5
+    rng = np.random.Generator(np.random.Philox(21))
+    y = rng.random(int(np.prod(dims)))
+    fs = [rng.random((n, r)) for n in dims]
+    t = ck.DenseTensor(dims, y.copy())
+    m = ck.KruskalTensor(np.ones(r), [f.copy() for f in fs])
+    ck.run(t, m, MttkrpPlan(Variant.B200, 0))
+    # numpy factor: reassigned, then written in place
+    m.factors[1] = fs[1] * 2.0
+    got = ck.run(t, m, MttkrpPlan(Variant.B200, 0)).matrix
+    assert oracle.rel_err(got, oracle.mttkrp_ref(y, dims, 0, [fs[0], fs[1] * 2.0, fs[2]])) <= 1e-12
+    m.factors[2][:] = 0.5
+    got = ck.run(t, m, MttkrpPlan(Variant.B200, 0)).matrix
+    assert oracle.rel_err(got, oracle.mttkrp_ref(y, dims, 0, [fs[0], fs[1] * 2.0, np.full_like(fs[2], 0.5)])) <= 1e-12
+    # torch factors: an in-place write bumps the version counter
+    tf = [torch.from_numpy(f.copy()) for f in fs]
+    mt_ = ck.KruskalTensor(np.ones(r), tf)
+    ck.run(t, mt_, MttkrpPlan(Variant.B200, 1))
+    mt_.factors[0].mul_(3.0)
+    got = ck.run(t, mt_, MttkrpPlan(Variant.B200, 1)).matrix
+    assert oracle.rel_err(got, oracle.mttkrp_ref(y, dims, 1, [fs[0] * 3.0, fs[1], fs[2]])) <= 1e-12
+    # tensor payload reassigned (host) and mutated in place (torch host payload)
+    t.data = y * 2.0
+    got = ck.run(t, m, MttkrpPlan(Variant.B200, 2)).matrix
+    ref_f = [fs[0], fs[1] * 2.0, np.full_like(fs[2], 0.5)]
+    assert oracle.rel_err(got, oracle.mttkrp_ref(y * 2.0, dims, 2, ref_f)) <= 1e-12
+    th = ck.DenseTensor(dims, torch.from_numpy(y.copy()))
+    ck.run(th, m, MttkrpPlan(Variant.B200, 2))
+    th.data.mul_(-1.0)
+    got = ck.run(th, m, MttkrpPlan(Variant.B200, 2)).matrix
+    assert oracle.rel_err(got, oracle.mttkrp_ref(-y, dims, 2, ref_f)) <= 1e-12
+
+
+def test_workspaces_are_per_stream():
+    """Concurrent MTTKRPs on two streams do not share split-K scratch: both
+    results are bit-identical to the serial ones."""
+    from paper_2510_14891_b200._device import workspace
+
+    dev = torch.device("cuda", 0)
+    s1, s2 = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    with torch.cuda.stream(s1):
+        a = workspace(dev, 1 << 20)
+    with torch.cuda.stream(s2):
+        b = workspace(dev, 1 << 20)
+    assert a.data_ptr() != b.data_ptr()
+    dims, r = (64, 48, 40), 24
+    y = ck.DenseTensor.uniform(dims, seed=3, device=dev)
+    fs = [torch.rand((n, r), dtype=torch.float64, device=dev) for n in dims]
+    plan = MttkrpPlan(Variant.B200, 1, splits=4)
+    ref = [mttkrp_device(y.data, dims, fs, 1, None, plan)[0].clone() for _ in range(2)]
+    torch.cuda.synchronize()
+    outs = []
+    for s in (s1, s2):
+        s.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(s):
+            outs.append(mttkrp_device(y.data, dims, fs, 1, None, plan)[0])
+    torch.cuda.synchronize()
+    assert torch.equal(outs[0], ref[0]) and torch.equal(outs[1], ref[1])

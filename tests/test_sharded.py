@@ -7,9 +7,11 @@ oracle cp_als trajectory (cpals.py:92-171 restated in oracle/)."""
 
 import os
 import socket
+import time
 
 import numpy as np
 import pytest
+import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
@@ -19,57 +21,99 @@ from paper_2510_14891_b200.cpals import AlsConfig
 from paper_2510_14891_b200.dtensor import DenseTensor
 
 
-class NumpyOps:
-    """Test-only compute backend for the sharded protocol (the oracle)."""
+class _Clock:
+    def record(self):
+        self.t = time.perf_counter()
 
-    def prepare_tensor(self, y):
-        return np.asarray(y.data if isinstance(y, DenseTensor) else y, dtype=np.float64).ravel()
+    def seconds_to(self, other):
+        return other.t - self.t
 
-    def asarray(self, a):
-        return np.array(a, dtype=np.float64)
+    def synchronize(self):
+        pass
 
-    def ones(self, r):
-        return np.ones(r)
 
-    def copy(self, a):
-        return a.copy()
+class CpuOracleBackend:
+    """Test-only backend for als_sweep.run_sweeps: torch CPU tensors, the
+    oracle's kernels (oracle/, restating cpals.py / kruskal.py / _kernels.py).
+    Same interface as als_sweep.DeviceBackend, so the engine and its
+    collectives are the production ones."""
 
-    def all_finite(self, y):
-        return bool(np.all(np.isfinite(y)))
+    graphable = False
 
-    def sumsq(self, y):
-        return np.array([float(y @ y)])
+    def __init__(self, y, run_dims):
+        self.y = torch.as_tensor(np.asarray(y.data if isinstance(y, DenseTensor) else y, dtype=np.float64)).ravel()
+        self.dims = tuple(run_dims)
+        self._chol = None
 
-    def mttkrp(self, y, local_dims, factors, k):
-        return oracle.mttkrp_ref(y, local_dims, k, factors)
+    def tensor(self, *shape, dtype=torch.float64):
+        return torch.zeros(shape, dtype=dtype)
 
-    def gram(self, a):
-        return oracle.gram(a) if a.shape[0] else np.zeros((a.shape[1], a.shape[1]))
+    def upload(self, a):
+        return torch.from_numpy(np.array(a, dtype=np.float64))
 
-    def hadamard(self, grams, skip):
-        out = np.ones_like(grams[0])
+    def host_buffer(self, n):
+        return torch.zeros(n, dtype=torch.float64)
+
+    def stamp(self):
+        return _Clock()
+
+    def sumsq(self, x, out):
+        v = x.numpy()
+        out[0] = float(v @ v)
+
+    def gram(self, a, out):
+        out.copy_(torch.from_numpy(oracle.gram(a.numpy())))
+
+    def hadamard(self, grams, skip, out):
+        h = np.ones(tuple(out.shape))
         for m, g in enumerate(grams):
             if m != skip:
-                out = out * g
-        return out
+                h = h * g.numpy()
+        out.copy_(torch.from_numpy(h))
 
-    def solve(self, gamma, g):
-        return oracle._solve_normal(gamma, g) if g.shape[0] else g
+    def mttkrp(self, factors, k, out):
+        out.copy_(torch.from_numpy(oracle.mttkrp_ref(self.y.numpy(), self.dims, k, [f.numpy() for f in factors])))
 
-    def colnorms_sq(self, a):
-        return np.sum(a * a, axis=0)
+    def factor_spec(self, gamma, info_k):
+        from scipy.linalg import cho_factor
 
-    def scale_columns(self, a, nsq):
-        nrm = np.sqrt(nsq)
+        try:
+            self._chol = cho_factor(gamma.numpy().copy(), check_finite=False)
+            info_k[0] = 0
+        except np.linalg.LinAlgError:
+            self._chol = None
+            info_k[0] = 1
+
+    def apply_spec(self, g, info_k):
+        from scipy.linalg import cho_solve
+
+        if int(info_k[0]) == 0:
+            g.copy_(torch.from_numpy(cho_solve(self._chol, g.numpy().T, check_finite=False).T.copy()))
+
+    def solve_ladder(self, gamma, g):
+        g.copy_(torch.from_numpy(np.ascontiguousarray(oracle._solve_normal(gamma.numpy(), g.numpy()))))
+
+    def colnorms_sq(self, a, out):
+        v = a.numpy()
+        out.copy_(torch.from_numpy(np.sum(v * v, axis=0)))
+
+    def scale_columns(self, a, normsq, lam):
+        nrm = np.sqrt(normsq.numpy())
         nz = nrm > 0
-        a[:, nz] /= nrm[nz]
-        return np.where(nz, nrm, 0.0)
+        v = a.numpy()
+        v[:, nz] /= nrm[nz]
+        lam.copy_(torch.from_numpy(np.where(nz, nrm, 0.0)))
 
-    def fit_terms(self, h, lam, g, a):
-        return np.array([float(lam @ h @ lam), float(np.sum((g * lam) * a))])
+    def fit_terms(self, h, lam, g, a, out):
+        lv = lam.numpy()
+        out[0] = float(lv @ h.numpy() @ lv)
+        out[1] = float(np.sum((g.numpy() * lv) * a.numpy()))
 
-    def to_host(self, x):
-        return np.asarray(x)
+    def readback(self, src, dst):
+        dst.copy_(src)
+
+    def synchronize(self):
+        pass
 
 
 def _free_port():
@@ -86,9 +130,11 @@ def _worker(rank, world, port, dims, rank_r, mode, iters, out_q):
         data = rng.random(int(np.prod(dims)))
         part = sharded.partition_for(dims, world, mode)
         y_local = sharded.local_slab(DenseTensor(dims, data), part, rank)
+        be = CpuOracleBackend(y_local, part.local_dims(rank))
         model, tr = sharded.cp_als_sharded(y_local, part, AlsConfig(rank=rank_r, tol=0.0, max_iters=iters, seed=3),
-                                           sharded.Comm(), NumpyOps())
-        out_q.put((rank, tr.fits, [np.asarray(a) for a in model.factors], np.asarray(model.weights), tr.comm_bytes))
+                                           sharded.Comm(), backend=be)
+        out_q.put((rank, tr.fits, [np.asarray(a) for a in model.factors], np.asarray(model.weights), tr.comm_bytes,
+                   tr.comm_calls))
     finally:
         dist.destroy_process_group()
 
@@ -117,13 +163,17 @@ def test_sharded_protocol_matches_single_process(world, dims, mode):
     data = rng.random(int(np.prod(dims)))
     lam_ref, f_ref, fits_ref = oracle.cp_als(data, dims, rank_r, max_iters=iters, tol=0.0, seed=3, mttkrp="ref")
     res = _run(world, dims, rank_r, mode, iters)
-    for rank, fits, factors, lam, nbytes in res:
+    d = len(dims)
+    for rank, fits, factors, lam, nbytes, calls in res:
         assert np.max(np.abs(np.asarray(fits) - np.asarray(fits_ref))) <= 1e-10, rank
         assert oracle.rel_err(lam, lam_ref) <= 1e-9
         for a, b in zip(factors, f_ref):
             assert a.shape == b.shape
             assert oracle.rel_err(a, b) <= 1e-9
         assert nbytes > 0
+        # per sweep: d-1 partial G_k, the shard Gram and column norms, the
+        # stats vector; plus ||Y||^2 and the initial shard Gram
+        assert calls == 2 + iters * (d + 2), calls
     # every rank holds the same model
     for r in res[1:]:
         assert r[1] == res[0][1]
@@ -152,3 +202,53 @@ def test_local_slab_is_the_mode_block():
         sl = sharded.local_slab(DenseTensor(dims, data), part, r)
         assert sl.dims == part.local_dims(r)
         assert np.array_equal(np.asarray(sl.data).reshape(sl.dims, order="F"), full[:, lo:hi, :])
+
+
+def test_strict_comm_rejects_host_tensors():
+    """A communicator bound to a CUDA device raises on anything but a CUDA
+    tensor on that device -- before NCCL sees it (an NCCL group has no CPU
+    backend; round 1's numpy flag died there)."""
+    from paper_2510_14891_b200.errors import DeviceError
+
+    comm = sharded.Comm(device=torch.device("cuda", 0))
+    with pytest.raises(DeviceError):
+        comm.allreduce_(torch.zeros(2, dtype=torch.float64))
+    with pytest.raises(DeviceError):
+        comm.allreduce_(np.zeros(2))
+    with pytest.raises(DeviceError):
+        comm.allgather_rows(torch.zeros((2, 2)), [(0, 2)])
+    # the CPU test communicator accepts host tensors (world 1: a no-op)
+    t = torch.ones(3, dtype=torch.float64)
+    assert sharded.Comm().allreduce_(t) is t
+
+
+def _graph_worker(rank, world, port, out_q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        dims = (6, 5, 4)
+        data = np.random.Generator(np.random.Philox(1)).random(120)
+        part = sharded.partition_for(dims, world)
+        y_local = sharded.local_slab(DenseTensor(dims, data), part, rank)
+        be = CpuOracleBackend(y_local, part.local_dims(rank))
+        try:
+            sharded.cp_als_sharded(y_local, part, AlsConfig(rank=2, max_iters=2), sharded.Comm(), backend=be,
+                                   graph=True)
+            out_q.put((rank, "no error"))
+        except Exception as exc:  # noqa: BLE001
+            out_q.put((rank, type(exc).__name__))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_graph_replay_is_single_rank_only():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_graph_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=240) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    assert res == [(0, "ParameterError"), (1, "ParameterError")]
