@@ -109,7 +109,10 @@ const char* cpk_version(void);
 int cpk_plan_resolve(int d, const int64_t* dims, int mode, int64_t rank,
                      cpk_plan* plan);
 
-/* Bytes of split-K workspace the resolved plan needs (0 when splits == 1). */
+/* Bytes of workspace cpk_mttkrp_f64 needs for the same (request) plan:
+ * split-K partials plus, for merged plans, the merged output or the
+ * Khatri-Rao factor (0 when nothing is needed).  plan may be NULL: the
+ * all-zero automatic request, as cpk_mttkrp_f64 treats a NULL plan. */
 int cpk_mttkrp_workspace_bytes(int d, const int64_t* dims, int mode,
                                int64_t rank, const cpk_plan* plan,
                                size_t* bytes);

@@ -531,8 +531,11 @@ extern "C" int cpk_plan_resolve(int d, const int64_t* dims, int mode, int64_t ra
 }
 
 extern "C" int cpk_mttkrp_workspace_bytes(int d, const int64_t* dims, int mode, int64_t rank,
-                                          const cpk_plan* plan, size_t* bytes) {
-  if (!plan || !bytes) return fail(CPK_ERR_PARAM, "NULL argument");
+                                          const cpk_plan* plan_or_null, size_t* bytes) {
+  if (!bytes) return fail(CPK_ERR_PARAM, "NULL argument");
+  // a NULL plan is the all-zero request, exactly as cpk_mttkrp_f64 reads it
+  const cpk_plan auto_plan{0, 0, 0, 0, 0, 0, 0, 0};
+  const cpk_plan* plan = plan_or_null ? plan_or_null : &auto_plan;
   Problem pr;
   int rc = make_problem(d, dims, mode, rank, &pr);
   if (rc) return rc;

@@ -34,7 +34,7 @@ import torch
 from . import _lib
 from ._device import EventTimer, require_cuda, stream_ptr, workspace
 from .dtensor import DenseTensor, check_dims, num_elements
-from .errors import DeviceError, IndexRangeError, ParameterError, ShapeError
+from .errors import DeviceError, IndexRangeError, ParameterError, ResourceError, ShapeError
 from .kruskal import KruskalTensor
 
 
@@ -323,8 +323,12 @@ def _run_gpu(y: DenseTensor, m: KruskalTensor, plan: MttkrpPlan):
         g, p, timer = _mttkrp_even(y, fac, plan, lam, dev)
     else:
         g, p, timer = mttkrp_device(y.device_data(dev), y.dims, fac, plan.mode, lam, plan)
-    host = not isinstance(y.data, torch.Tensor)
-    matrix = np.ascontiguousarray(g.cpu().numpy()) if host else g
+    # results live where the payload lives: numpy in, numpy out; a host
+    # torch payload gets a host tensor; a CUDA payload keeps G on the device
+    if not isinstance(y.data, torch.Tensor):
+        matrix = np.ascontiguousarray(g.cpu().numpy())
+    else:
+        matrix = g if y.data.is_cuda else g.cpu()
     return matrix, p, timer
 
 
@@ -600,15 +604,85 @@ def mttkrp_b200(y: DenseTensor, m: KruskalTensor, plan: MttkrpPlan) -> MttkrpOut
     )
 
 
+DEFAULT_KRP_BUDGET = 2 * 1024 ** 3  # bytes allowed for an explicit KRP (mttkrp.py:41)
+
+
+def full_krp_bytes(dims, rank: int, mode: int) -> int:
+    """Bytes of the explicit Khatri-Rao product of the other factors (mttkrp.py:166-168)."""
+    return 8 * (num_elements(dims) // dims[mode]) * rank
+
+
+def _split_extents(dims, mode: int) -> tuple:
+    i_l = num_elements(dims[:mode]) if mode > 0 else 1
+    i_r = num_elements(dims[mode + 1:]) if mode < len(dims) - 1 else 1
+    return i_l, i_r
+
+
+def gemm_scratch_bytes(dims, rank: int, mode: int) -> int:
+    """Temporary bytes the dense GEMM baseline allocates for `mode` (mttkrp.py:213-221)."""
+    d = len(dims)
+    i_l, i_r = _split_extents(dims, mode)
+    if mode == 0:
+        return 8 * rank * i_r
+    if mode == d - 1:
+        return 8 * rank * i_l
+    return 8 * (rank * (i_l + i_r) + i_l * dims[mode] * rank)
+
+
+def gemm_model_bytes(dims, rank: int, mode: int) -> int:
+    """Model footprint of the GEMM baseline: tensor + partial KRPs + output (mttkrp.py:224-227)."""
+    i_l, i_r = _split_extents(dims, mode)
+    return 8 * (num_elements(dims) + rank * (i_l + i_r + dims[mode]))
+
+
+def mttkrp_full_krp(y: DenseTensor, m: KruskalTensor, mode: int,
+                    budget_bytes: int = DEFAULT_KRP_BUDGET) -> MttkrpOutput:
+    """mttkrp.py:173-203 contract: the reference's checks and budget
+    (ResourceError when the explicit KRP would exceed ``budget_bytes``), and
+    its stats accounting; the product itself runs on the matrix-free sm_100a
+    kernel, so no KRP is ever formed here."""
+    _check_inputs(y, m, mode)
+    if y.ndim < 2:
+        raise ParameterError("full-krp needs at least two modes")
+    z_bytes = full_krp_bytes(y.dims, m.rank, mode)
+    if z_bytes > budget_bytes:
+        raise ResourceError(f"explicit KRP needs {z_bytes} bytes, budget is {budget_bytes}")
+    plan = MttkrpPlan(Variant.FULL_KRP, int(mode))
+    mat, p, t = _run_gpu(y, m, plan)
+    return MttkrpOutput(mat, _stats(Variant.FULL_KRP, y, m, plan, p, t, element_visits=y.size, atomic_updates=0,
+                                    scratch=z_bytes + (0 if mode == 0 else 8 * y.size)))
+
+
+def mttkrp_gemm(y: DenseTensor, m: KruskalTensor, mode: int, scratch_cap_bytes: int | None = None) -> MttkrpOutput:
+    """mttkrp.py:230-276 contract: the reference's checks, scratch cap
+    (ResourceError above ``scratch_cap_bytes``) and stats accounting; the
+    product runs on the matrix-free sm_100a kernel (the partial-KRP + DGEMM
+    form of the baseline itself is `baselines.mttkrp_gemm_cublas`)."""
+    _check_inputs(y, m, mode)
+    if y.ndim < 2:
+        raise ParameterError("gemm baseline needs at least two modes")
+    scratch = gemm_scratch_bytes(y.dims, m.rank, mode)
+    if scratch_cap_bytes is not None and scratch > scratch_cap_bytes:
+        raise ResourceError(f"gemm baseline needs {scratch} scratch bytes, cap is {scratch_cap_bytes}")
+    plan = MttkrpPlan(Variant.GEMM, int(mode))
+    mat, p, t = _run_gpu(y, m, plan)
+    return MttkrpOutput(mat, _stats(Variant.GEMM, y, m, plan, p, t, element_visits=y.size, atomic_updates=0,
+                                    scratch=scratch, footprint=gemm_model_bytes(y.dims, m.rank, mode)))
+
+
 def run(y: DenseTensor, m: KruskalTensor, plan: MttkrpPlan, **kwargs) -> MttkrpOutput:
     """Dispatch one MTTKRP according to the plan's variant (mttkrp.py:378-391).
 
-    Budget kwargs of the CPU oracles (budget_bytes, scratch_cap_bytes) are
-    accepted and ignored: the matrix-free kernel allocates no KRP.
+    As in the reference, ``**kwargs`` (budget_bytes / scratch_cap_bytes) go
+    to the FULL_KRP / GEMM variants, which keep their budget semantics.
     """
     v = Variant(plan.variant)
     if v == Variant.REFERENCE:
         return mttkrp_reference(y, m, plan.mode)
+    if v == Variant.FULL_KRP:
+        return mttkrp_full_krp(y, m, plan.mode, **kwargs)
+    if v == Variant.GEMM:
+        return mttkrp_gemm(y, m, plan.mode, **kwargs)
     if v == Variant.ELEM:
         return mttkrp_elem(y, m, plan)
     if v == Variant.SLICE:

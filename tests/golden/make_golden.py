@@ -23,6 +23,12 @@ Fixtures (numpy .npz, float64):
   model.json -- cpkern.perfmodel traffic models / predicted times (sweep columns)
   model_cli.json -- `cpkern model --json` documents (cli.py:470-545) for
                 presets / shapes / machines / ranks / modes
+  step.npz   -- one CP-ALS mode update from identical factors (SURVEY.md 8(c)
+                plan (i)): the CP-ALS init factors (Philox(seed)), then for
+                each mode G_k (unit-weight MTTKRP), Gamma_k, the reference's
+                _solve_normal and column normalization (cpals.py:122-140);
+                config 3 (modes 0 and 3) and a rank-512 3-way case (all
+                modes) that takes the R > 256 solve path
   als.npz    -- cp_als fit trajectories: the planted suites of test_cpals.py
                 (REFERENCE and GEMM plans), and config 3 for 10 sweeps (GEMM)
 Inputs for c1-c3 follow the reference CLI recipe (cli.py:133-141):
@@ -126,6 +132,39 @@ def make_config(name, dims, rank, use_gemm, sample_rows=0):
             store[f"Grows{k}"] = sampled_rows_reference(y, m, k, rows)
     np.savez_compressed(OUT / f"{name}.npz", **store)
     print(f"{name}: {time.time() - t0:.1f} s", flush=True)
+
+
+def make_step():
+    """One mode update per mode, from the same (init) factors, through the
+    reference's own gram / Gamma loop / _solve_normal / normalization."""
+    from cpkern.cpals import _solve_normal
+    from cpkern.kruskal import gram
+
+    t0 = time.time()
+    store = {}
+    for name, dims, rank, modes in (("c3", (128, 128, 128, 128), 256, (0, 3)), ("r512", (64, 56, 48), 512, (0, 1, 2))):
+        y = ck.DenseTensor(dims, rng_for(0).random(int(np.prod(dims))))
+        rng = np.random.Generator(np.random.Philox(0))  # cp_als init, seed 0 (cpals.py:108-109)
+        factors = [rng.random((i, rank)) for i in dims]
+        grams = [gram(a) for a in factors]
+        unit = np.ones(rank)
+        store[f"{name}/dims"] = np.asarray(dims, dtype=np.int64)
+        for k in modes:
+            g = ck.mttkrp_gemm(y, ck.KruskalTensor(unit, factors, validate=False), k).matrix
+            gamma = np.ones((rank, rank))
+            for m in range(len(dims)):
+                if m != k:
+                    gamma *= grams[m]
+            a_hat = _solve_normal(gamma, g.copy())
+            nrm = np.linalg.norm(a_hat, axis=0)
+            nz = nrm > 0
+            a_hat[:, nz] /= nrm[nz]
+            store[f"{name}/G{k}"] = g
+            store[f"{name}/A{k}"] = np.ascontiguousarray(a_hat)
+            store[f"{name}/lam{k}"] = np.where(nz, nrm, 0.0)
+            store[f"{name}/cond{k}"] = np.float64(np.linalg.cond(gamma))
+    np.savez_compressed(OUT / "step.npz", **store)
+    print(f"step: {time.time() - t0:.1f} s", flush=True)
 
 
 def planted(dims, rank, seed):
@@ -251,7 +290,7 @@ def make_dten():
 
 
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["small", "c1", "c2", "c3", "als", "dten", "model", "model_cli"]
+    which = sys.argv[1:] or ["small", "c1", "c2", "c3", "als", "dten", "model", "model_cli", "step"]
     if "model" in which:
         make_model()
     if "model_cli" in which:
@@ -268,4 +307,6 @@ if __name__ == "__main__":
         make_config("c3", (128, 128, 128, 128), 256, use_gemm=True)
     if "als" in which:
         make_als()
+    if "step" in which:
+        make_step()
     print("done")

@@ -572,3 +572,32 @@ def test_workspaces_are_per_stream():
             outs.append(mttkrp_device(y.data, dims, fs, 1, None, plan)[0])
     torch.cuda.synchronize()
     assert torch.equal(outs[0], ref[0]) and torch.equal(outs[1], ref[1])
+
+
+def test_gemm_and_full_krp_names_keep_reference_budgets():
+    """mttkrp_gemm / mttkrp_full_krp (mttkrp.py:173-276): same names, checks,
+    ResourceError budgets and stats accounting as the reference; the product
+    is the matrix-free kernel's (<= 1e-10 vs the oracle)."""
+    dims, r = (14, 9, 11, 6), 7
+    rng = np.random.Generator(np.random.Philox(8))
+    y = rng.random(int(np.prod(dims)))
+    fs = [rng.random((n, r)) for n in dims]
+    lam = rng.random(r) + 0.5
+    t, m = ck.DenseTensor(dims, y), ck.KruskalTensor(lam, fs)
+    for k in range(4):
+        ref = oracle.mttkrp_ref(y, dims, k, fs, lam)
+        g = ck.mttkrp_gemm(t, m, k)
+        assert oracle.rel_err(g.matrix, ref) <= TOL and g.stats.variant == Variant.GEMM
+        n_s = t.size // dims[k]
+        i_l, i_r = int(np.prod(dims[:k])), int(np.prod(dims[k + 1:]))
+        want = 8 * r * i_r if k == 0 else 8 * r * i_l if k == 3 else 8 * (r * (i_l + i_r) + i_l * dims[k] * r)
+        assert g.stats.scratch_bytes == want
+        f = ck.run(t, m, MttkrpPlan(Variant.FULL_KRP, k))
+        assert oracle.rel_err(f.matrix, ref) <= TOL
+        assert f.stats.scratch_bytes == 8 * n_s * r + (0 if k == 0 else 8 * t.size)
+    with pytest.raises(ck.ResourceError, match="explicit KRP needs"):
+        ck.run(t, m, MttkrpPlan(Variant.FULL_KRP, 0), budget_bytes=100)
+    with pytest.raises(ck.ResourceError, match="scratch bytes, cap is"):
+        ck.mttkrp_gemm(t, m, 1, scratch_cap_bytes=10)
+    with pytest.raises(ck.ParameterError):
+        ck.mttkrp_gemm(ck.DenseTensor((5,), np.ones(5)), ck.KruskalTensor(np.ones(2), [np.ones((5, 2))]), 0)

@@ -110,3 +110,32 @@ def test_splitmix_twin_slices():
     a = gen.splitmix_uniform(50, seed=1, offset=0)
     b = gen.splitmix_uniform(20, seed=1, offset=30)
     assert np.array_equal(a[30:], b)
+
+
+def test_oracle_single_mode_update_matches_reference(golden):
+    """SURVEY 8(c) plan (i): the oracle's Gram / Gamma / _solve_normal /
+    normalization (cpals.py:122-140) reproduce the reference's single mode
+    update (tests/golden/step.npz) -- the MTTKRP too at the rank-512 case."""
+    st = golden("step")
+    for name in ("c3", "r512"):
+        dims = tuple(int(x) for x in st[f"{name}/dims"])
+        rank = st[f"{name}/A{[k for k in range(len(dims)) if f'{name}/A{k}' in st][0]}"].shape[1]
+        rng = np.random.Generator(np.random.Philox(0))
+        factors = [rng.random((i, rank)) for i in dims]
+        grams = [oracle.gram(a) for a in factors]
+        y = np.random.Generator(np.random.Philox(0)).random(int(np.prod(dims))) if name == "r512" else None
+        for k in range(len(dims)):
+            if f"{name}/A{k}" not in st:
+                continue
+            g = st[f"{name}/G{k}"]
+            if y is not None:
+                assert oracle.rel_err(oracle.mttkrp_gemm(y, dims, k, factors), g) <= 1e-13
+            gamma = np.ones((rank, rank))
+            for m in range(len(dims)):
+                if m != k:
+                    gamma *= grams[m]
+            a = oracle._solve_normal(gamma, g.copy())
+            nrm = np.linalg.norm(a, axis=0)
+            a[:, nrm > 0] /= nrm[nrm > 0]
+            assert oracle.rel_err(a, st[f"{name}/A{k}"]) <= 1e-13
+            assert oracle.rel_err(np.where(nrm > 0, nrm, 0.0), st[f"{name}/lam{k}"]) <= 1e-13
