@@ -99,26 +99,107 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------ reference (CPU)
+REF_DIR = ROOT / "baseline" / "_ref"  # the unmodified reference, pip-installed
+
+
+def reference_cpkern():
+    """The reference package itself (`cpkern`, Python + numba), installed
+    under baseline/_ref; None when it is absent or numba cannot import (the
+    oracle's C port then stands in, kind "port")."""
+    if not (REF_DIR / "cpkern").exists():
+        return None
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/cpk_numba_cache")
+    os.environ.setdefault("NUMBA_NUM_THREADS", str(os.cpu_count() or 1))
+    if str(REF_DIR) not in sys.path:
+        sys.path.append(str(REF_DIR))
+    try:
+        import cpkern
+
+        return cpkern
+    except Exception:  # noqa: BLE001
+        return None
+
+
+def host_cpu_info(ref=None):
+    """lscpu model / sockets / cores and the threading layer the CPU path used."""
+    info = {"logical_cpus": os.cpu_count()}
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        keys = {"Model name": "model", "Socket(s)": "sockets", "Core(s) per socket": "cores_per_socket",
+                "Thread(s) per core": "threads_per_core"}
+        for line in out.splitlines():
+            k, _, v = line.partition(":")
+            if k.strip() in keys:
+                info[keys[k.strip()]] = v.strip()
+    except Exception:  # noqa: BLE001
+        pass
+    if ref is not None:
+        import numba
+
+        try:
+            info["threading_layer"] = f"numba {numba.__version__} {numba.threading_layer()}"
+        except Exception:  # noqa: BLE001  (no parallel region has run yet)
+            info["threading_layer"] = f"numba {numba.__version__}"
+    else:
+        info["threading_layer"] = "OpenMP (gcc, oracle/liboracle.so)"
+    return info
+
+
 def cpu_sample(target_seconds: float, threads: int = 0):
-    """Time the oracle TILE port (C + OpenMP) on a slab of config 4.
+    """Time the reference's TILE MTTKRP on the host on a slab of config 4.
 
     The slab keeps I_0 = I_1 = 1024 and R = 2000 and cuts mode 2 to `depth`
-    slices; all three modes are run, like one GPU step.  N_T follows the
-    reference's Eq. 6 heuristic with its intel-8480p spec (w = 362 -> N_T =
-    131044, clamped per mode), unroll F = 16.
+    slices; all three modes are run, like one GPU step.  With the reference
+    installed (baseline/_ref) this is `cpkern.run(y, m, MttkrpPlan(TILE, k,
+    unroll=16, tile_volume=N_T))` itself -- numba, all host threads -- with
+    N_T from the reference's own Eq. 6 heuristic on its intel-8480p spec
+    (w = 362, N_T = 131044, clamped per mode by plan_for_mode); otherwise
+    the oracle's C + OpenMP restatement of the same kernel (kind "port",
+    bit-identical to it and ~2x faster, profiles/r01_port_vs_reference.json).
     """
-    from oracle import gen, oracle
+    from oracle import gen
 
     fs = gen.bench_factors(DIMS, RANK, SEED)
-    w = oracle.max_threads() if threads <= 0 else threads
+    ck = reference_cpkern()
+    if ck is not None:
+        import numba
+
+        from cpkern.mttkrp import MttkrpPlan, Variant, heuristic_tile_volume, plan_for_mode
+
+        if threads > 0:
+            numba.set_num_threads(threads)
+        w = numba.get_num_threads()
+        n_t = heuristic_tile_volume(DIMS, ck.bundled_machine("intel-8480p"))
+
+        def run_modes(dims, y, sub):
+            t = ck.DenseTensor(dims, y)
+            m = ck.KruskalTensor(np.ones(RANK), sub, validate=False)
+            base = MttkrpPlan(Variant.TILE, 0, unroll=16, tile_volume=n_t, workers=0)
+            for k in range(3):
+                ck.run(t, m, plan_for_mode(base, dims, k))
+
+        # numba compiles on the first call: a tiny warm-up outside the timing
+        run_modes((4, 4, 2), np.ones(32), [fs[0][:4], fs[1][:4], fs[2][:2]])
+        kind = "reference"
+        what = f"cpkern.run TILE (the reference, numba), N_T={n_t} F=16"
+    else:
+        from oracle import oracle
+
+        w = oracle.max_threads() if threads <= 0 else threads
+
+        def run_modes(dims, y, sub):
+            for k in range(3):
+                oracle.mttkrp_tile(y, dims, k, sub, None, f_cols=16, n_t=131044, workers=w)
+
+        kind = "port"
+        what = "oracle TILE port (C+OpenMP), N_T=131044 F=16"
 
     def run(depth):
         dims = (DIMS[0], DIMS[1], depth)
         y = gen.splitmix_uniform(int(np.prod(dims)), SEED)
         sub = [fs[0], fs[1], fs[2][:depth]]
         t0 = time.perf_counter()
-        for k in range(3):
-            oracle.mttkrp_tile(y, dims, k, sub, None, f_cols=16, n_t=131044, workers=w)
+        run_modes(dims, y, sub)
         return time.perf_counter() - t0, algo_flops(dims, RANK) * 3
 
     # calibrate on one slice, then size the sample to ~target_seconds
@@ -128,7 +209,31 @@ def cpu_sample(target_seconds: float, threads: int = 0):
         t, f = t1, f1
     else:
         t, f = run(depth)
-    return {"seconds": t, "flops": f, "depth": depth, "threads": w}
+    return {"seconds": t, "flops": f, "depth": depth, "threads": w, "kind": kind, "what": what,
+            "cpu": host_cpu_info(ck)}
+
+
+def cpu_cpals_sample(iters: int = 1):
+    """The reference's own cp_als (baseline/_ref) on config 3 (128^4,
+    R = 256) for `iters` sweeps on the host, with the GEMM plan -- its
+    fastest CPU MTTKRP (the default SLICE / TILE plans take ~85 s per mode
+    here); seconds per sweep.  None without the reference."""
+    ck = reference_cpkern()
+    if ck is None:
+        return None
+    from cpkern.mttkrp import MttkrpPlan, Variant
+
+    dims = (128, 128, 128, 128)
+    y = ck.DenseTensor(dims, np.random.Generator(np.random.Philox(SEED)).random(int(np.prod(dims))))
+    cfg = ck.AlsConfig(rank=256, tol=0.0, max_iters=iters, seed=0, plan=MttkrpPlan(Variant.GEMM, 0))
+    t0 = time.perf_counter()
+    _, tr = ck.cp_als(y, cfg)
+    dt = time.perf_counter() - t0
+    return {"config": "c3: 4-way 128^4 f64, rank 256", "impl": "cpkern.cp_als (the reference), plan GEMM",
+            "iters": iters, "sec_per_iter": dt / iters,
+            "mttkrp_sec_per_iter": sum(sum(s) for s in tr.mttkrp_seconds) / iters,
+            "other_sec_per_iter": sum(tr.other_seconds) / iters, "fits": tr.fits,
+            "cores": os.cpu_count(), "cpu": host_cpu_info(ck)}
 
 
 def run_reference(args):
@@ -139,15 +244,13 @@ def run_reference(args):
     for _ in range(args.warmup):
         cpu_sample(budget / 4)
     vals, secs = [], []
-    depth = None
-    threads = None
+    s = None
     for _ in range(args.steps):
         s = cpu_sample(budget)
         vals.append(s["flops"] / s["seconds"] / 1e9)
         secs.append(s["seconds"])
-        depth, threads = s["depth"], s["threads"]
     value = statistics.median(vals)
-    sample = f"slab 1024x1024x{depth} of config 4 (R=2000), all 3 modes, TILE N_T=131044 F=16"
+    sample = f"slab 1024x1024x{s['depth']} of config 4 (R=2000), all 3 modes, {s['what']}"
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.median(secs),
@@ -155,10 +258,16 @@ def run_reference(args):
         "data": "synthetic (splitmix64 counter-based U[0,1) tensor, Philox(1) factors)",
         "config": {"workload": "c4: 3-way 1024^3 f64 tensor, rank 2000, MTTKRP all modes (CPU slab sample)",
                    "dims": list(DIMS), "rank": RANK, "sample": sample},
-        "cpu_baseline": {"value": value, "unit": "GFLOP/s", "cores": threads, "kind": "port", "sample": sample},
+        "cpu_baseline": {"value": value, "unit": "GFLOP/s", "cores": s["threads"], "kind": s["kind"],
+                         "sample": sample, "cpu": s["cpu"]},
         "e2e": {"value": value, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
     }
+    if args.cpals_cpu_iters > 0:
+        try:
+            line["cp_als"] = cpu_cpals_sample(args.cpals_cpu_iters)
+        except Exception as exc:  # noqa: BLE001  (report, do not lose the line)
+            line["cp_als"] = {"error": f"{type(exc).__name__}: {exc}"[:300]}
     print(json.dumps(line), flush=True)
 
 
@@ -420,12 +529,18 @@ def run_b200(args):
     flops_per_launch = algo_flops(local_dims, RANK)  # one mode
     mean_launch_s = statistics.mean(per_mode) * 1e-3
     achieved = flops_per_launch / mean_launch_s
-    rt = plans[0]["rank_tile"]
-    padded_rank = -(-RANK // rt) * rt
+    # issued work: the kernel runs the DMMA fragments of live 8-column
+    # blocks only (a warp whose 64 columns straddle R skips its dead tail),
+    # so the columns it issues are R rounded up to 8, not to the rank tile
+    live_cols = -(-RANK // 8) * 8
     traffic = None
+    traffic_src = None
     if NCU_SUMMARY.exists():
         try:
-            traffic = json.loads(NCU_SUMMARY.read_text()).get("dram_bytes_per_launch")
+            summ = json.loads(NCU_SUMMARY.read_text())
+            traffic = summ.get("dram_bytes_per_launch")
+            traffic_src = (f"{NCU_SUMMARY.relative_to(ROOT)} (ncu --set full capture '{summ.get('tag')}', "
+                           "dram__bytes_read.sum + dram__bytes_write.sum per launch; not measured in this run)")
         except Exception:
             traffic = None
 
@@ -436,19 +551,34 @@ def run_b200(args):
         cp = bench_cpals(ck, dev, args.cpals_iters)
         torch.cuda.empty_cache()
     c5 = None
+    c5_dims = tuple(int(x) for x in args.c5_dims.split(","))
     if args.c5_iters > 0:
         try:
-            c5 = bench_c5(dev, args.c5_iters, tuple(int(x) for x in args.c5_dims.split(",")), args.c5_rank)
+            c5 = bench_c5(dev, args.c5_iters, c5_dims, args.c5_rank)
         except Exception as exc:  # report, do not lose the headline line
             c5 = {"error": f"{type(exc).__name__}: {exc}"[:300]}
         torch.cuda.empty_cache()
+        if world == 1 and args.c5_projection and c5 and "error" not in c5:
+            try:
+                proj = bench_c5_projection(dev, args.c5_iters, c5_dims, args.c5_rank)
+                for pt in proj["points"]:
+                    pt["projected_speedup"] = c5["sec_per_iter"] / pt["rank0_sec_per_iter"]
+                c5["projection"] = proj
+            except Exception as exc:  # noqa: BLE001
+                c5["projection"] = {"error": f"{type(exc).__name__}: {exc}"[:300]}
+            torch.cuda.empty_cache()
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         s = cpu_sample(args.cpu_seconds)
-        cpu = {"value": s["flops"] / s["seconds"] / 1e9, "unit": "GFLOP/s", "cores": s["threads"], "kind": "port",
-               "sample": f"oracle TILE port (C+OpenMP) on slab 1024x1024x{s['depth']} of config 4, R=2000, "
-                         f"all 3 modes, N_T=131044 F=16, {s['seconds']:.1f} s"}
+        cpu = {"value": s["flops"] / s["seconds"] / 1e9, "unit": "GFLOP/s", "cores": s["threads"], "kind": s["kind"],
+               "sample": f"{s['what']} on slab 1024x1024x{s['depth']} of config 4, R=2000, all 3 modes, "
+                         f"{s['seconds']:.1f} s", "cpu": s["cpu"]}
+        if cp is not None and args.cpals_cpu_iters > 0:
+            try:
+                cp["cpu_reference"] = cpu_cpals_sample(args.cpals_cpu_iters)
+            except Exception as exc:  # noqa: BLE001
+                cp["cpu_reference"] = {"error": f"{type(exc).__name__}: {exc}"[:300]}
 
     if rank == 0:
         hbm = 6508.2e9
@@ -474,7 +604,7 @@ def run_b200(args):
             # peak of MEASURED_PEAKS.json
             "roofline": {"bound": "tensor", "pipe": "fp64 (DMMA = DFMA datapath)",
                          "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "TFLOP/s",
-                         "frac": achieved / peak, "traffic": traffic,
+                         "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
                          "peak_source": "cpk_fp64_peak_probe (max of register DFMA and DMMA loops, this run)"
                          if fp64_peak else "nominal 148 SM x 64 FP64 FMA/clk x 2 x 1.965 GHz",
                          "nominal_peak": nominal / 1e12,
@@ -482,7 +612,7 @@ def run_b200(args):
                          "plans": [{key: p[key] for key in ("engine", "rank_tile", "block_rows", "block_k", "splits")}
                                    for p in plans],
                          "flops_per_launch": flops_per_launch,
-                         "issued_fp64_frac": (int(np.prod(local_dims)) * 2 * padded_rank / mean_launch_s) / peak,
+                         "issued_fp64_frac": (int(np.prod(local_dims)) * 2 * live_cols / mean_launch_s) / peak,
                          "north_star_roofline_ms_per_mode": roof_t * 1e3,
                          "north_star_frac": roof_t * 3 * args.steps / elapsed},
             "dfma_engine": dfma,
@@ -571,13 +701,54 @@ def bench_c5(dev, iters, dims=(4096, 2048, 2048), r=512):
             "timing": "CUDA events per sweep (sweep start -> stats readback), max over ranks", "fits": tr.fits}
 
 
+def bench_c5_projection(dev, iters, dims=(4096, 2048, 2048), r=512, worlds=(2, 4, 8)):
+    """One-GPU projection of the sharded c5 sweep: rank 0's own work at P
+    ranks (its 1/P slab, the same engine and plans), with the collectives
+    elided by a loopback communicator -- so the sweep time is what one rank
+    computes, and the projected speed-up is sec(P=1) / sec(P).  Fits are
+    meaningless (partial sums are never combined); the transfers it leaves
+    out are ~18 MiB per sweep (tens of microseconds over NVLink 5).  This box
+    has one GPU; the real N-GPU number is `cp_als_c5` under torchrun."""
+    import torch
+
+    from paper_2510_14891_b200 import sharded
+    from paper_2510_14891_b200.cpals import AlsConfig
+
+    class Loopback(sharded.Comm):
+        def __init__(self, world):
+            super().__init__(device=dev)
+            self.world, self.rank = world, 0
+
+        def allreduce_(self, t, op=None):
+            self._check(t)
+            self.calls += 1
+            self.bytes += t.numel() * t.element_size()
+            return t
+
+    out = []
+    for world in worlds:
+        comm = Loopback(world)
+        part = sharded.partition_for(dims, world)
+        y = sharded.uniform_slab(part, 0, seed=SEED, device=dev)
+        sharded.cp_als_sharded(y, part, AlsConfig(rank=r, tol=0.0, max_iters=1, seed=0), comm, gather=False)
+        _, tr = sharded.cp_als_sharded(y, part, AlsConfig(rank=r, tol=0.0, max_iters=iters, seed=0), comm,
+                                       gather=False)
+        out.append({"gpus": world, "rank0_sec_per_iter": statistics.median(tr.sweep_seconds),
+                    "rank0_mttkrp_sec_per_iter": statistics.median(sum(m) for m in tr.mttkrp_seconds),
+                    "elided_bytes_per_iter": comm.bytes // max(1, len(tr.fits)), "rollbacks": tr.rollbacks})
+        del y
+        torch.cuda.empty_cache()
+    return {"what": "rank 0's sweep at P ranks on this one GPU, collectives elided (loopback)",
+            "config": f"c5: {'x'.join(map(str, dims))} f64, rank {r}", "iters": iters, "points": out}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--dfma-steps", type=int, default=2)
     ap.add_argument("--gemm-steps", type=int, default=2)
     ap.add_argument("--rank-sweep", type=int, default=1, help="1: add the GFLOP/s-vs-rank leg (c2 shape)")
@@ -586,7 +757,9 @@ def main():
     ap.add_argument("--c5-iters", type=int, default=3)
     ap.add_argument("--c5-dims", default="4096,2048,2048", help="CP-ALS leg shape (tests shrink it)")
     ap.add_argument("--c5-rank", type=int, default=512)
+    ap.add_argument("--c5-projection", type=int, default=1, help="1: add the one-GPU P=2/4/8 rank-0 projection")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--cpals-cpu-iters", type=int, default=1, help="reference cp_als sweeps on the host (c3)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--ref-seconds", type=float, default=0.0, help="reference arm: CPU seconds per step (0 = auto)")
     args = ap.parse_args()

@@ -323,12 +323,10 @@ def _run_gpu(y: DenseTensor, m: KruskalTensor, plan: MttkrpPlan):
         g, p, timer = _mttkrp_even(y, fac, plan, lam, dev)
     else:
         g, p, timer = mttkrp_device(y.device_data(dev), y.dims, fac, plan.mode, lam, plan)
-    # results live where the payload lives: numpy in, numpy out; a host
-    # torch payload gets a host tensor; a CUDA payload keeps G on the device
-    if not isinstance(y.data, torch.Tensor):
-        matrix = np.ascontiguousarray(g.cpu().numpy())
-    else:
-        matrix = g if y.data.is_cuda else g.cpu()
+    # numpy in, numpy out; a torch payload (CUDA, or pinned host memory being
+    # streamed) keeps G on the device
+    host = not isinstance(y.data, torch.Tensor)
+    matrix = np.ascontiguousarray(g.cpu().numpy()) if host else g
     return matrix, p, timer
 
 

@@ -23,8 +23,15 @@ def _run(args, timeout):
 
 
 def test_reference_arm_line():
-    d = _run(["--impl", "reference", "--steps", "1", "--warmup", "1", "--ref-seconds", "0.5"], 300)
+    d = _run(["--impl", "reference", "--steps", "1", "--warmup", "1", "--ref-seconds", "0.5",
+              "--cpals-cpu-iters", "0"], 600)
     assert BASE_KEYS <= set(d) and d["impl"] == "reference"
+    # the installed reference itself (baseline/_ref) when present, else the port
+    from pathlib import Path as _P
+
+    want = "reference" if (_P(ROOT) / "baseline" / "_ref" / "cpkern").exists() else "port"
+    assert d["cpu_baseline"]["kind"] == want
+    assert {"logical_cpus", "threading_layer"} <= set(d["cpu_baseline"]["cpu"])
     assert d["value"] > 0 and d["unit"] == "GFLOP/s" and d["higher_is_better"] is True
     assert d["cpu_baseline"]["kind"] in ("port", "reference") and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]

@@ -543,7 +543,7 @@ def test_device_caches_follow_the_payloads():
     th = ck.DenseTensor(dims, torch.from_numpy(y.copy()))
     ck.run(th, m, MttkrpPlan(Variant.B200, 2))
     th.data.mul_(-1.0)
-    got = ck.run(th, m, MttkrpPlan(Variant.B200, 2)).matrix
+    got = ck.run(th, m, MttkrpPlan(Variant.B200, 2)).matrix.cpu().numpy()
     assert oracle.rel_err(got, oracle.mttkrp_ref(-y, dims, 2, ref_f)) <= 1e-12
 
 
