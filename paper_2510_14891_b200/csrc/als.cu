@@ -4,6 +4,7 @@
 // kruskal.py:74-114.  Every reduction runs in a fixed order, so a sweep is
 // bit-reproducible run to run (README.md "same seed, same trajectory").
 #include "common.cuh"
+#include "sweep_inv.cuh"
 
 #include <cusolverDn.h>
 
@@ -608,14 +609,22 @@ __global__ void __launch_bounds__(ROWS_WARPS * 32) chol_rows_kernel(const double
       if (q0 + q < rows) G[(q0 + q) * R + c] = z[c * RW + q];
 }
 
-// CPK_SOLVE=cusolver / =kernel force one path (A/B comparisons and tests)
-static bool use_small_chol(int64_t R) {
-  if (R > CHOL_KERNEL_CAP) return false;
+// Solve paths: R <= CHOL_SMALL_MAX the one-CTA Cholesky + row solve above;
+// larger R the multi-CTA sweep (sweep_inv.cu: Gamma^-1 on the factor side,
+// X = G Gamma^-1 as one MTTKRP-kernel GEMM on the apply side); cuSOLVER
+// potrf / potrs only when forced.  CPK_SOLVE=kernel / sweep / cusolver
+// force a path (A/B comparisons and tests; `kernel` up to CHOL_KERNEL_CAP).
+enum class SolvePath { Small, Sweep, Cusolver };
+
+static SolvePath solve_path(int64_t R) {
   const char* e = getenv("CPK_SOLVE");
-  if (e && strcmp(e, "cusolver") == 0) return false;
-  if (e && strcmp(e, "kernel") == 0) return true;
-  return R <= CHOL_SMALL_MAX;
+  if (e && strcmp(e, "cusolver") == 0) return SolvePath::Cusolver;
+  if (e && strcmp(e, "sweep") == 0) return SolvePath::Sweep;
+  if (e && strcmp(e, "kernel") == 0 && R <= CHOL_KERNEL_CAP) return SolvePath::Small;
+  return R <= CHOL_SMALL_MAX ? SolvePath::Small : SolvePath::Sweep;
 }
+
+static bool use_small_chol(int64_t R) { return solve_path(R) == SolvePath::Small; }
 
 static int chol_small(const double* gamma, int64_t R, double eps, double* L, int* info, cudaStream_t st) {
   const cudaError_t attr = cudaFuncSetAttribute(chol_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -739,7 +748,7 @@ extern "C" int cpk_sumsq_f64(const double* x, int64_t n, double* work, double* o
   return check_launch("sumsq");
 }
 
-// work layout: [gamma copy R*R][potrf lwork][info int]
+// work layout (cuSOLVER / small-R paths): [gamma copy R*R][potrf lwork][info int]
 static int solve_layout(int64_t rows, int64_t rank, int lwork, size_t* total, size_t* off_lwork, size_t* off_info) {
   (void)rows;
   const size_t g = align_up(size_t(rank) * size_t(rank) * sizeof(double));
@@ -748,6 +757,52 @@ static int solve_layout(int64_t rows, int64_t rank, int lwork, size_t* total, si
   *off_info = g + w;
   *total = g + w + 256;
   return CPK_OK;
+}
+
+// work layout (sweep path): [sweep_factor_bytes: Gamma^-1 (Rp x Rp) ...]
+// [copy of G: rows x R][MTTKRP workspace of the apply GEMM]
+static int apply_mttkrp_bytes(int64_t rows, int64_t rank, size_t* bytes) {
+  *bytes = 0;
+  if (rows <= 0) return CPK_OK;
+  const int64_t dims[2] = {rank, rows};
+  return cpk_mttkrp_workspace_bytes(2, dims, 1, rank, nullptr, bytes);
+}
+
+static int* info_d_sweep(void* work, int64_t rank) {  // the info word at the end of the factor block
+  return reinterpret_cast<int*>(static_cast<char*>(work) + sweep_factor_bytes(rank) - 256);
+}
+
+static int sweep_layout_bytes(int64_t rows, int64_t rank, size_t* total) {
+  size_t m = 0;
+  const int rc = apply_mttkrp_bytes(rows, rank, &m);
+  if (rc) return rc;
+  *total = sweep_factor_bytes(rank) + align_up(size_t(std::max<int64_t>(rows, 0)) * size_t(rank) * sizeof(double)) +
+           align_up(m);
+  return CPK_OK;
+}
+
+// X Gamma = G in place as X = G Gamma^-1: G is copied aside and read back as
+// the R x rows first-mode-fastest tensor T[c, i] = G[i][c] whose mode-1
+// MTTKRP with the factor Gamma^-1 (ld Rp) is X[i][j] = sum_c G[i][c] W[c][j]
+// -- the hot MTTKRP kernel does the GEMM.
+static int sweep_apply(double* G, int64_t rows, int64_t rank, void* work, size_t work_bytes, cudaStream_t st) {
+  if (rows <= 0) return CPK_OK;
+  size_t need = 0;
+  int rc = sweep_layout_bytes(rows, rank, &need);
+  if (rc) return rc;
+  if (work_bytes < need) return fail(CPK_ERR_RESOURCE, "solve workspace needs %zu bytes, got %zu", need, work_bytes);
+  char* base = static_cast<char*>(work);
+  double* tmp = reinterpret_cast<double*>(base + sweep_factor_bytes(rank));
+  const size_t tmp_bytes = align_up(size_t(rows) * size_t(rank) * sizeof(double));
+  void* mws = base + sweep_factor_bytes(rank) + tmp_bytes;
+  const size_t mws_bytes = work_bytes - sweep_factor_bytes(rank) - tmp_bytes;
+  if (cudaMemcpyAsync(tmp, G, size_t(rows) * size_t(rank) * sizeof(double), cudaMemcpyDeviceToDevice, st) !=
+      cudaSuccess)
+    return fail(CPK_ERR_CUDA, "solve apply copy failed");
+  const int64_t dims[2] = {rank, rows};
+  const double* fac[2] = {sweep_inverse_matrix(work), nullptr};
+  const int64_t ld[2] = {sweep_padded(rank), rank};
+  return cpk_mttkrp_f64(tmp, 2, dims, 1, fac, ld, nullptr, rank, G, rank, nullptr, mws, mws_bytes, st);
 }
 
 static int potrf_lwork(int64_t rank, int* lwork) {
@@ -765,8 +820,16 @@ extern "C" int cpk_solve_workspace_bytes(int64_t rows, int64_t rank, size_t* byt
   int lwork = 0;
   int rc = potrf_lwork(rank, &lwork);
   if (rc) return rc;
-  size_t a, b;
-  return solve_layout(rows, rank, lwork, bytes, &a, &b);
+  size_t a, b, sw = 0;
+  rc = solve_layout(rows, rank, lwork, bytes, &a, &b);
+  if (rc) return rc;
+  // room for every path (CPK_SOLVE may switch between calls)
+  if (rank > CHOL_SMALL_MAX || getenv("CPK_SOLVE")) {
+    rc = sweep_layout_bytes(rows, rank, &sw);
+    if (rc) return rc;
+    *bytes = std::max(*bytes, sw);
+  }
+  return CPK_OK;
 }
 
 extern "C" int cpk_solve_normal_f64(const double* gamma, double* G, int64_t rows, int64_t rank, void* work,
@@ -790,8 +853,20 @@ extern "C" int cpk_solve_normal_f64(const double* gamma, double* G, int64_t rows
   const unsigned cblocks = unsigned(std::min<int64_t>((rank * rank + 255) / 256, 148 * 4));
   // Rung 0 is the plain Cholesky; rungs 1..5 add eps tr/R I, eps = 1e-12 * 1e3^i
   double eps = 0.0;
-  const bool small = use_small_chol(rank);
+  const SolvePath path = solve_path(rank);
+  const bool small = path == SolvePath::Small;
   for (int rung = 0; rung <= 5; ++rung) {
+    if (path == SolvePath::Sweep) {
+      rc = sweep_inverse(gamma, rank, eps, work, work_bytes, info_d_sweep(work, rank), 0, st);
+      if (rc) return rc;
+      int info = 0;
+      if (cudaMemcpyAsync(&info, info_d_sweep(work, rank), sizeof(int), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+          cudaStreamSynchronize(st) != cudaSuccess)
+        return fail(CPK_ERR_CUDA, "sweep info readback failed");
+      if (info == 0) return sweep_apply(G, rows, rank, work, work_bytes, st);
+      eps = rung == 0 ? 1e-12 : eps * 1e3;
+      continue;
+    }
     if (small) {
       rc = chol_small(gamma, rank, eps, L, info_d, st);
       if (rc) return rc;
@@ -845,6 +920,7 @@ extern "C" int cpk_solve_factor_spec_f64(const double* gamma, int64_t rank, void
   double* L = reinterpret_cast<double*>(base);
   double* w = reinterpret_cast<double*>(base + off_w);
   if (use_small_chol(rank)) return chol_small(gamma, rank, 0.0, L, info_out, st);
+  if (solve_path(rank) == SolvePath::Sweep) return sweep_inverse(gamma, rank, 0.0, work, work_bytes, info_out, 0, st);
   const unsigned cblocks = unsigned(std::min<int64_t>((rank * rank + 255) / 256, 148 * 4));
   copy_regularize_kernel<<<std::max(cblocks, 1u), 256, 0, st>>>(gamma, rank, 0.0, L);
   rc = check_launch("copy_regularize");
@@ -874,6 +950,8 @@ extern "C" int cpk_solve_apply_spec_f64(double* G, int64_t rows, int64_t rank, v
   double* L = reinterpret_cast<double*>(base);
   int* info_d = reinterpret_cast<int*>(base + off_info);
   if (use_small_chol(rank)) return chol_rows(L, rank, G, rows, info_out, st);
+  // a failed factor (sweep or potrf) just produces garbage, which the caller discards
+  if (solve_path(rank) == SolvePath::Sweep) return sweep_apply(G, rows, rank, work, work_bytes, st);
   // potrs on a failed factor just produces garbage, which the caller discards
   if (rows > 0 && cusolverDnDpotrs(h, CUBLAS_FILL_MODE_UPPER, int(rank), int(rows), L, int(rank), G, int(rank),
                                    info_d) != CUSOLVER_STATUS_SUCCESS)

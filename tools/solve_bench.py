@@ -1,5 +1,6 @@
-"""Time the CP-ALS normal-equation solve (speculative form, one launch
-sequence per call) for the small-rank kernels vs cuSOLVER (CPK_SOLVE).
+"""Time the CP-ALS normal-equation solve (speculative form: factor + apply,
+one launch sequence per call) for the one-CTA kernels, the multi-CTA sweep
+and cuSOLVER potrf + potrs (CPK_SOLVE).
 
     python tools/solve_bench.py [--ranks 64 128 256 512] [--rows 128 1024 4096]
 """
@@ -16,7 +17,8 @@ sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 from paper_2510_14891_b200 import cpals  # noqa: E402
 
 ap = argparse.ArgumentParser()
-ap.add_argument("--ranks", type=int, nargs="+", default=[32, 64, 128, 256, 384, 512])
+ap.add_argument("--ranks", type=int, nargs="+", default=[256, 384, 512, 1000, 2000])
+ap.add_argument("--paths", nargs="+", default=["kernel", "sweep", "cusolver"])
 ap.add_argument("--rows", type=int, nargs="+", default=[128, 1024, 4096])
 ap.add_argument("--reps", type=int, default=20)
 a = ap.parse_args()
@@ -28,7 +30,9 @@ for r in a.ranks:
     for rows in a.rows:
         g0 = torch.from_numpy(rng.random((rows, r))).to(dev)
         out = {"rank": r, "rows": rows}
-        for path in ("kernel", "cusolver"):
+        for path in a.paths:
+            if path == "kernel" and r > 512:
+                continue
             os.environ["CPK_SOLVE"] = path
             solver = cpals._Solver(dev, rows, r)
             info = torch.zeros(1, dtype=torch.int32, device=dev)
