@@ -42,6 +42,21 @@ PEAKS_FILE = ROOT / "MEASURED_PEAKS.json"
 NCU_SUMMARY = ROOT / "profiles" / "ncu_summary.json"
 
 
+def _hbm_peak_gbs():
+    """The pod's measured copy bandwidth (MEASURED_PEAKS.json), else the
+    B200_PROFILING.md fallback the perfmodel carries."""
+    try:
+        return float(json.loads(PEAKS_FILE.read_text())["hbm_gbs"])
+    except Exception:  # noqa: BLE001
+        from paper_2510_14891_b200.perfmodel import B200_HBM_BYTES_PER_S
+
+        return B200_HBM_BYTES_PER_S / 1e9
+
+
+HBM_PEAK_GBS = _hbm_peak_gbs()
+FP64_NOMINAL_TFS = 37.22496  # 148 SMs x 64 FP64 FMA/clk x 2 x 1965 MHz
+
+
 def algo_flops(dims, rank):
     n = int(np.prod(dims))
     return 2 * n * rank * (len(dims) - 1)
@@ -403,21 +418,34 @@ def run_b200(args):
         y2 = torch.empty(int(np.prod(d2)), dtype=torch.float64, device=dev)
         _lib.check(lib.cpk_fill_uniform_f64(y2.data_ptr(), y2.numel(), SEED, 0,
                                             torch.cuda.current_stream().cuda_stream), "fill")
-        rank_sweep = {"shape": list(d2), "roofline": "max(8N/HBM, 2NR(d-1)/FP64 nominal)", "points": []}
-        for r in (16, 32, 64, 128, 256, 512, 1000, 2000):
+        n2 = int(np.prod(d2))
+        rank_sweep = {"shape": list(d2), "roofline": "max(8N/HBM, 2NR(d-1)/FP64 nominal)",
+                      "timing": "per call, calls issued back to back between two CUDA events (host work "
+                                "overlaps the previous call, as inside a CP-ALS sweep)",
+                      "hbm_peak_gbs": HBM_PEAK_GBS, "points": []}
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        for r in (8, 16, 24, 32, 48, 64, 128, 256, 512, 1000, 2000):
             rng = np.random.Generator(np.random.Philox(1))
             f2 = [torch.from_numpy(rng.random((n, r))).to(dev) for n in d2]
-            ms = []
+            ms, tiles = [], []
             for k in range(3):
-                ts = []
-                for _ in range(3):
-                    _, _, t = mttkrp_device(y2, d2, f2, k, None, MttkrpPlan(Variant.B200, k))
-                    ts.append(t.seconds)
-                ms.append(min(ts[1:]) * 1e3)
+                plan = MttkrpPlan(Variant.B200, k)
+                mttkrp_device(y2, d2, f2, k, None, plan)  # warm-up (plan, workspace, tensor maps)
+                reps = 20 if r <= 64 else 5
+                e0.record()
+                for _ in range(reps):
+                    mttkrp_device(y2, d2, f2, k, None, plan)
+                e1.record()
+                e1.synchronize()
+                ms.append(e0.elapsed_time(e1) / reps)
+                tiles.append(resolve_plan(plan, d2, r)["rank_tile"])
             roof = roofline_seconds(d2, r) * 1e3  # nominal FP64 peak (37.2 TF/s at 1965 MHz)
-            rank_sweep["points"].append({"rank": r, "ms_per_mode": ms,
+            t_mode = sum(ms) / 3 * 1e-3
+            rank_sweep["points"].append({"rank": r, "ms_per_mode": ms, "rank_tiles": tiles,
                                          "gflops": algo_flops(d2, r) * 3 / (sum(ms) * 1e-3) / 1e9,
-                                         "roofline_frac": 3 * roof / sum(ms)})
+                                         "roofline_frac": 3 * roof / sum(ms),
+                                         "hbm_frac": 8 * n2 / t_mode / (HBM_PEAK_GBS * 1e9),
+                                         "fp64_issued_frac": 2 * n2 * r / t_mode / (FP64_NOMINAL_TFS * 1e12)})
         del y2, f2
         torch.cuda.empty_cache()
 

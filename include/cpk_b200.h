@@ -56,8 +56,8 @@ enum {
  * one output tile along the contraction (the reference's tiles-per-slice,
  * mttkrp.py:354-355).  Zero in any field means "choose" (cpk_plan_resolve). */
 typedef struct cpk_plan {
-  int32_t rank_tile;    /* 0 | 32 | 64 | 128                          */
-  int32_t block_rows;   /* 0 | 64 | 128 (mode-k rows per CTA)          */
+  int32_t rank_tile;    /* 0 | 16 | 32 | 64 | 128 | 256 (engine-dependent) */
+  int32_t block_rows;   /* 0, else the tile's mode-k rows per CTA     */
   int64_t tile_volume;  /* in-slice elements per CTA work item, 0=auto */
   int32_t splits;       /* split-K factor, 0 = derive from tile_volume */
   int32_t sm_count;     /* 0 = query the device                        */

@@ -207,6 +207,7 @@ struct TileChoice {
 static const TileChoice kChoices[] = {
     {CPK_ENGINE_TMA, 256, 0.95}, {CPK_ENGINE_TMA, 128, 1.00}, {CPK_ENGINE_TMA, 64, 0.93},
     {CPK_ENGINE_DMMA, 256, 1.02}, {CPK_ENGINE_DMMA, 128, 1.23}, {CPK_ENGINE_DMMA, 64, 1.26},
+    {CPK_ENGINE_DMMA, 32, 1.15}, {CPK_ENGINE_DMMA, 16, 0.90},
     {CPK_ENGINE_CPDMMA, 128, 0.97}, {CPK_ENGINE_CPDMMA, 64, 0.88},
     {CPK_ENGINE_CPASYNC, 128, 0.92}, {CPK_ENGINE_CPASYNC, 64, 0.78}, {CPK_ENGINE_CPASYNC, 32, 0.55},
 };

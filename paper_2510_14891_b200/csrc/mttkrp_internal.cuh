@@ -27,7 +27,7 @@ struct WsRequest {
   const double* lam;
 };
 
-// TMA tile for a rank tile (64 | 128 | 256) and math: rows per CTA and chunk depth.
+// TMA tile for a rank tile (DMMA 16 | 32 | 64 | 128 | 256, DFMA 64 | 128 | 256) and math: rows per CTA and chunk depth.
 bool ws_shape(int rank_tile, int math, int* block_rows, int* block_k);
 bool ws_eligible(const WsRequest& r);
 int launch_ws(const WsRequest& r, cudaStream_t st);

@@ -17,17 +17,21 @@
 // out-of-range rows / chunk tails / rank tails, so there is no masking.
 //
 // Tensor tile layouts in shared memory:
-//   mode 0 (M-major): box {BM, BK} -> As[k][m], no swizzle.
+//   mode 0 (M-major): DFMA consumers: box {BM, BK} -> As[k][m], no swizzle;
+//     DMMA consumers: BM / 16 boxes {16, BK} with the 128-byte swizzle ->
+//     panels [k][16] (and the factor rows likewise, BN / 16 boxes {16, BK}).
 //   mode k>0 (K-major): two boxes {16, BM} (one per 16-deep panel) with the
 //     128-byte swizzle -> panel[m][16] where the 16-byte chunk c of row m
-//     lives at chunk c ^ (m & 7): the 4 rows a warp quarter reads land in
-//     distinct banks.
+//     lives at chunk c ^ (m & 7).
+// The DMMA consumers' fragment mapping keeps every shared load at one
+// wavefront per quarter warp (see ws_dmma_loop).
 #include "common.cuh"
 #include "mttkrp_internal.cuh"
 
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
 #include <mutex>
 
 namespace cpk {
@@ -56,6 +60,7 @@ struct alignas(64) WsParams {
   int64_t ldo, out_split_stride;
   const double* lam;
   int32_t y0, z0;  // first row block / split of this launch
+  int32_t a_one_box;  // mode 0, DMMA: tm_y views the tensor as (16, I_1, I_0 / 16, ...) -> one box per stage
 };
 
 // ---------------------------------------------------------------- PTX wrappers
@@ -184,53 +189,89 @@ __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
 
 // total (TMEM) += acc o P for one o-group, acc := 0.  p_s: the stage's o-rows
-// (NO x BN); first: the total is still empty (no TMEM read).
-template <int NO, int BN>
-__device__ __forceinline__ void og_flush(double (&acc)[4][8][2], uint32_t tbase, const double* p_s, int wn0, int lk,
+// (NO x BN); first: the total is still empty (no TMEM read).  The warp's
+// 4 x NF fragments are 16 NF words per thread, moved 32 words (8 fragments)
+// at a time: fragment (mf, nf) is words 4 (mf NF + nf) .. + 3.
+template <int NO, int BN, int NF>
+__device__ __forceinline__ void og_flush(double (&acc)[4][NF][2], uint32_t tbase, const double* p_s, int wn0, int lk,
                                          bool first) {
-  double pj[8][2];
+  // fragment nf = 2 q + e, accumulator v sits at column 16 q + 4 lk + 2 v + e
+  // (dmma_col): the thread's columns of a fragment pair are 4 contiguous doubles
+  double pj[NF][2];
 #pragma unroll
-  for (int nf = 0; nf < 8; ++nf) {
-    double2 v = *reinterpret_cast<const double2*>(p_s + wn0 + nf * 8 + 2 * lk);
+  for (int q = 0; q < NF / 2; ++q)
 #pragma unroll
-    for (int i = 1; i < NO; ++i) {
-      const double2 w = *reinterpret_cast<const double2*>(p_s + i * BN + wn0 + nf * 8 + 2 * lk);
-      v.x *= w.x;
-      v.y *= w.y;
+    for (int v = 0; v < 2; ++v) {
+      const int c = wn0 + 16 * q + 4 * lk + 2 * v;
+      double2 x = *reinterpret_cast<const double2*>(p_s + c);
+#pragma unroll
+      for (int i = 1; i < NO; ++i) {
+        const double2 w = *reinterpret_cast<const double2*>(p_s + i * BN + c);
+        x.x *= w.x;
+        x.y *= w.y;
+      }
+      pj[2 * q][v] = x.x;
+      pj[2 * q + 1][v] = x.y;
     }
-    pj[nf][0] = v.x;
-    pj[nf][1] = v.y;
-  }
+  constexpr int GROUPS = NF / 2;  // 32-word groups
 #pragma unroll
-  for (int mf = 0; mf < 4; ++mf) {
+  for (int g = 0; g < GROUPS; ++g) {
     uint32_t t[32];
     if (!first) {
-      tmem_ld32(tbase + mf * 32, t);
+      tmem_ld32(tbase + g * 32, t);
       tmem_wait_ld();
     }
 #pragma unroll
-    for (int nf = 0; nf < 8; ++nf)
+    for (int f = 0; f < 8; ++f) {
+      const int idx = g * 8 + f, mf = idx / NF, nf = idx % NF;
 #pragma unroll
       for (int v = 0; v < 2; ++v) {
-        const int w = (nf * 2 + v) * 2;
+        const int w = (f * 2 + v) * 2;
         const double old = first ? 0.0 : __hiloint2double(int(t[w + 1]), int(t[w]));
         const double nw = fma(acc[mf][nf][v], pj[nf][v], old);
         t[w] = uint32_t(__double2loint(nw));
         t[w + 1] = uint32_t(__double2hiint(nw));
         acc[mf][nf][v] = 0.0;
       }
-    tmem_st32(tbase + mf * 32, t);
+    }
+    tmem_st32(tbase + g * 32, t);
   }
   tmem_wait_st();
 }
 
-// The main loop over a CTA's chunks.  TAIL: the warp's 64 columns straddle
-// the rank R, so only the first nf_act 8-column fragments do math (the rank
-// tail of R = 2000 at tile 64 is 16 columns: 2 of 8 fragments).
-template <bool KMAJ, bool TAIL, bool OG, int NO, int BM, int BN, int BK, int STAGE_BYTES, int A_BYTES>
-__device__ __forceinline__ void ws_dmma_loop(double (&acc)[4][8][2], const uint8_t* smem, uint64_t* full,
+// The main loop over a CTA's chunks.  NA: fragments that do math (a warp
+// whose 8 NF columns straddle the rank R runs only its live 16-column pairs:
+// the rank tail of R = 2000 at tile 64 is 16 columns, 2 of 8 fragments; a
+// warp with no live column, NA = 0, only keeps the stage protocol).  NA is a
+// template argument so every variant is a fully unrolled, branch-free loop.
+//
+// Shared-memory layout and fragment mapping (conflict-free, every load an
+// LDS.128 at its minimum of one wavefront per quarter warp):
+//   * the k order inside each 16-deep panel is free, so k-step s in {0, 1}
+//     of a panel gives lane quad lk the 16-byte k chunk
+//     c = 2 lk + ((lk >> 1) ^ s) (s = 0: chunks 0 2 5 7, s = 1: 1 3 4 6),
+//     i.e. k = 2 c + ph for the two DMMAs ph of the step;
+//   * K-major tensor tiles (modes k > 0, TMA 128-byte swizzle, 16-deep
+//     panels [m][16]): row m = 8 mf + lane / 4 reads chunk c ^ (m & 7); the
+//     chunk set of a step holds no pair {x, x ^ 1}, so the two rows of a
+//     quarter warp land on disjoint banks;
+//   * M-major tensor tiles (mode 0) and the factor rows arrive as 16-wide
+//     panels [k][16] (TMA boxes {16, BK}, 128-byte swizzle): row k holds
+//     16 rows (columns) of the tile, chunk j at j ^ (k & 7); lanes read the
+//     pair 2 (lane / 4), +1, so fragment 2 q + e covers tile rows (columns)
+//     16 q + 2 (lane / 4) + e (dmma_row / dmma_col); k & 7 = (2 c + ph) & 7
+//     takes 4 distinct even/odd values per step, so again no conflicts.
+// The epilogue and the o-group scaling use the same row / column maps.
+template <bool KMAJ>
+__device__ __forceinline__ int dmma_row(int mf, int lr) {
+  return KMAJ ? mf * 8 + lr : 16 * (mf >> 1) + 2 * lr + (mf & 1);
+}
+__device__ __forceinline__ int dmma_kchunk(int lk, int s) { return 2 * lk + ((lk >> 1) ^ s); }
+
+template <bool KMAJ, int NA, bool OG, int NO, int BM, int BN, int NF, int BK, int STAGE_BYTES, int A_BYTES>
+__device__ __forceinline__ void ws_dmma_loop(double (&acc)[4][NF][2], const uint8_t* smem, uint64_t* full,
                                              uint64_t* empty, int nst, int stages, int wm0, int wn0, int lane,
-                                             int nf_act, uint32_t tbase, int64_t q0, int64_t chunks_per_f) {
+                                             uint32_t tbase, int64_t q0, int64_t chunks_per_f) {
   const int lr = lane >> 2, lk = lane & 3;
   bool first = true;
   int64_t qf = OG ? q0 % chunks_per_f : 0;  // position inside the o-group
@@ -239,47 +280,56 @@ __device__ __forceinline__ void ws_dmma_loop(double (&acc)[4][8][2], const uint8
     mbar_wait(&full[s], (it / stages) & 1);
     const uint8_t* st = smem + s * STAGE_BYTES;
     const double* a_s = reinterpret_cast<const double*>(st);
-    const double* b_s = reinterpret_cast<const double*>(st + A_BYTES) + wn0 + lr;
+    const double* b_s = reinterpret_cast<const double*>(st + A_BYTES) + (wn0 >> 4) * (16 * BK);
 #pragma unroll 2
-    for (int kk = 0; kk < BK; kk += 8) {
-      double a[4][2], b[8][2];
+    for (int kk = 0; kk < (NA > 0 ? BK : 0); kk += 8) {
+      const int c = dmma_kchunk(lk, (kk >> 3) & 1);
+      const int kr0 = (kk & ~15) + 2 * c;  // tile k of this lane's ph = 0 DMMA
+      double a[4][2], b[NF][2];
       if constexpr (KMAJ) {
-        const double* panel = a_s + (kk >> 4) * (BM * 16) + (wm0 + lr) * 16;
-        const int chunk = ((((kk & 15) >> 1) + lk) ^ lr) << 1;  // (m & 7) == lr
+        const double* panel = a_s + (kk >> 4) * (BM * 16) + (wm0 + lr) * 16 + ((c ^ lr) << 1);
 #pragma unroll
         for (int mf = 0; mf < 4; ++mf) {
-          const double2 v = *reinterpret_cast<const double2*>(panel + mf * 8 * 16 + chunk);
+          const double2 v = *reinterpret_cast<const double2*>(panel + mf * 8 * 16);
           a[mf][0] = v.x;
           a[mf][1] = v.y;
         }
       } else {
-        const double* col = a_s + (kk + 2 * lk) * BM + wm0 + lr;
+        const double* panel = a_s + (wm0 >> 4) * (16 * BK);
 #pragma unroll
-        for (int mf = 0; mf < 4; ++mf) {
-          a[mf][0] = col[mf * 8];
-          a[mf][1] = col[BM + mf * 8];
+        for (int ph = 0; ph < 2; ++ph) {
+          const int kr = kr0 + ph;
+          const double* row = panel + kr * 16 + ((lr ^ (kr & 7)) << 1);
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            const double2 v = *reinterpret_cast<const double2*>(row + q * (16 * BK));
+            a[2 * q][ph] = v.x;
+            a[2 * q + 1][ph] = v.y;
+          }
         }
       }
-      const double* brow = b_s + (kk + 2 * lk) * BN;
 #pragma unroll
-      for (int nf = 0; nf < 8; ++nf) {
-        if (TAIL && nf >= nf_act) break;
-        b[nf][0] = brow[nf * 8];
-        b[nf][1] = brow[BN + nf * 8];
+      for (int ph = 0; ph < 2; ++ph) {
+        const int kr = kr0 + ph;
+        const double* row = b_s + kr * 16 + ((lr ^ (kr & 7)) << 1);
+#pragma unroll
+        for (int q = 0; q < NA / 2; ++q) {
+          const double2 v = *reinterpret_cast<const double2*>(row + q * (16 * BK));
+          b[2 * q][ph] = v.x;
+          b[2 * q + 1][ph] = v.y;
+        }
       }
 #pragma unroll
       for (int ph = 0; ph < 2; ++ph)
 #pragma unroll
         for (int mf = 0; mf < 4; ++mf)
 #pragma unroll
-          for (int nf = 0; nf < 8; ++nf) {
-            if (TAIL && nf >= nf_act) break;
-            dmma_8x8x4(acc[mf][nf], a[mf][ph], b[nf][ph]);
-          }
+          for (int nf = 0; nf < NA; ++nf) dmma_8x8x4(acc[mf][nf], a[mf][ph], b[nf][ph]);
     }
-    if constexpr (OG) {
+    if constexpr (OG && NA > 0) {
       if (++qf == chunks_per_f || it == nst - 1) {  // o-group ends: fold it into the total
-        og_flush<NO, BN>(acc, tbase, reinterpret_cast<const double*>(st + A_BYTES + BK * BN * 8), wn0, lk, first);
+        og_flush<NO, BN, NF>(acc, tbase, reinterpret_cast<const double*>(st + A_BYTES + BK * BN * 8), wn0, lk,
+                             first);
         first = false;
         qf = 0;
       }
@@ -289,42 +339,68 @@ __device__ __forceinline__ void ws_dmma_loop(double (&acc)[4][8][2], const uint8
   }
 }
 
+// DMMA warp tiles: 32 rows x 8 NF rank columns, NF = min(8, BN / 8); narrow
+// rank tiles (BN = 16, 32) keep 8 warps along the rows (BM = 256) with 16 /
+// 32 accumulators per thread, and their small stages let more of them be in
+// flight (the low-rank end streams the tensor at HBM rate).
+template <int BN>
+struct DmmaWarps {
+  static constexpr int NF = BN >= 64 ? 8 : BN / 8;
+  static constexpr int WARPS_N = BN >= 64 ? BN / 64 : 1;
+};
+
 template <bool KMAJ, bool OG, int NO, int BM, int BN, int BK, int STAGE_BYTES, int A_BYTES>
 __device__ __forceinline__ void ws_consume_dmma(const uint8_t* smem, uint64_t* full, uint64_t* empty, int nst,
                                                 const WsParams& p, int n0, int j0, int warp, int lane,
                                                 int stages, uint32_t tmem, int64_t q0) {
-  constexpr int WARPS_N = BN / 64;
-  const int wm0 = (warp / WARPS_N) * 32, wn0 = (warp % WARPS_N) * 64;
+  constexpr int WARPS_N = DmmaWarps<BN>::WARPS_N, NF = DmmaWarps<BN>::NF;
+  const int wm0 = (warp / WARPS_N) * 32, wn0 = (warp % WARPS_N) * (8 * NF);
   const int lr = lane >> 2, lk = lane & 3;
-  double acc[4][8][2];
+  double acc[4][NF][2];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int j = 0; j < 8; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int j = 0; j < NF; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-  const int nf_act = (p.R - j0 - wn0 + 7) >> 3;  // warp-uniform
+  // this warp's live rank columns (warp-uniform; <= 0: none)
+  const int live = p.R - j0 - wn0;
   // this warp's TMEM window: lanes 32 (warp % 4).., columns 128 (warp / 4)..
   const uint32_t tbase = tmem + (uint32_t((warp & 3) * 32) << 16) + uint32_t((warp >> 2) * 128);
-  if (nf_act >= 8)
-    ws_dmma_loop<KMAJ, false, OG, NO, BM, BN, BK, STAGE_BYTES, A_BYTES>(acc, smem, full, empty, nst, stages, wm0, wn0,
-                                                                        lane, 8, tbase, q0, p.chunks_per_f);
-  else
-    ws_dmma_loop<KMAJ, true, OG, NO, BM, BN, BK, STAGE_BYTES, A_BYTES>(acc, smem, full, empty, nst, stages, wm0, wn0,
-                                                                       lane, nf_act, tbase, q0, p.chunks_per_f);
+#define CPK_DMMA_LOOP(NA_)                                                                                     \
+  ws_dmma_loop<KMAJ, NA_, OG, NO, BM, BN, NF, BK, STAGE_BYTES, A_BYTES>(acc, smem, full, empty, nst, stages, wm0, \
+                                                                        wn0, lane, tbase, q0, p.chunks_per_f)
+  // every branch runs exactly one loop (a warp that skipped it would never
+  // release its stages); plain compares, the last case catches the rest
+  if (live <= 0) {
+    CPK_DMMA_LOOP(0);
+  } else if constexpr (NF == 2) {
+    CPK_DMMA_LOOP(2);
+  } else if constexpr (NF == 4) {
+    if (live <= 16) CPK_DMMA_LOOP(2);
+    else CPK_DMMA_LOOP(4);
+  } else {
+    if (live <= 16) CPK_DMMA_LOOP(2);
+    else if (live <= 32) CPK_DMMA_LOOP(4);
+    else if (live <= 48) CPK_DMMA_LOOP(6);
+    else CPK_DMMA_LOOP(8);
+  }
+#undef CPK_DMMA_LOOP
   if constexpr (OG) {
-    if (nst > 0) {  // the total -> acc registers for the epilogue
+    if (nst > 0 && live > 0) {  // the total -> acc registers for the epilogue
 #pragma unroll
-      for (int mf = 0; mf < 4; ++mf) {
+      for (int g = 0; g < NF / 2; ++g) {
         uint32_t t[32];
-        tmem_ld32(tbase + mf * 32, t);
+        tmem_ld32(tbase + g * 32, t);
         tmem_wait_ld();
 #pragma unroll
-        for (int nf = 0; nf < 8; ++nf)
+        for (int f = 0; f < 8; ++f) {
+          const int idx = g * 8 + f, mf = idx / NF, nf = idx % NF;
 #pragma unroll
           for (int v = 0; v < 2; ++v) {
-            const int w = (nf * 2 + v) * 2;
+            const int w = (f * 2 + v) * 2;
             acc[mf][nf][v] = __hiloint2double(int(t[w + 1]), int(t[w]));
           }
+        }
       }
     }
   }
@@ -333,24 +409,27 @@ __device__ __forceinline__ void ws_consume_dmma(const uint8_t* smem, uint64_t* f
   const bool fold = p.lam != nullptr;
 #pragma unroll
   for (int mf = 0; mf < 4; ++mf) {
-    const int n = n0 + wm0 + mf * 8 + lr;
+    const int n = n0 + wm0 + dmma_row<KMAJ>(mf, lr);
     if (n >= p.Ik) continue;
 #pragma unroll
-    for (int nf = 0; nf < 8; ++nf) {
-      const int j = j0 + wn0 + nf * 8 + 2 * lk;
-      double v0 = acc[mf][nf][0], v1 = acc[mf][nf][1];
-      if (fold) {
-        if (j < p.R) v0 *= p.lam[j];
-        if (j + 1 < p.R) v1 *= p.lam[j + 1];
+    for (int q = 0; q < NF / 2; ++q)
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {
+        // fragments 2q, 2q + 1 hold columns j, j + 1 (dmma_col)
+        const int j = j0 + wn0 + 16 * q + 4 * lk + 2 * v;
+        double v0 = acc[mf][2 * q][v], v1 = acc[mf][2 * q + 1][v];
+        if (fold) {
+          if (j < p.R) v0 *= p.lam[j];
+          if (j + 1 < p.R) v1 *= p.lam[j + 1];
+        }
+        double* dst = out + int64_t(n) * p.ldo + j;
+        if (j + 1 < p.R && ((p.ldo & 1) == 0)) {
+          *reinterpret_cast<double2*>(dst) = make_double2(v0, v1);
+        } else {
+          if (j < p.R) dst[0] = v0;
+          if (j + 1 < p.R) dst[1] = v1;
+        }
       }
-      double* dst = out + int64_t(n) * p.ldo + j;
-      if (j + 1 < p.R && ((p.ldo & 1) == 0)) {
-        *reinterpret_cast<double2*>(dst) = make_double2(v0, v1);
-      } else {
-        if (j < p.R) dst[0] = v0;
-        if (j + 1 < p.R) dst[1] = v1;
-      }
-    }
   }
 }
 
@@ -371,7 +450,7 @@ struct WsTile {
 };
 template <int BN>
 struct WsTile<0, BN> {
-  static constexpr int WARPS_N = BN / 64, WARPS_M = 8 / WARPS_N;
+  static constexpr int WARPS_N = DmmaWarps<BN>::WARPS_N, WARPS_M = 8 / WARPS_N;
   static constexpr int TX = 8, TY = 0, BM = 32 * WARPS_M;
 };
 
@@ -387,7 +466,7 @@ struct WsCfg {
   static constexpr int TX_BYTES = A_BYTES + B_BYTES + P_BYTES;
   static constexpr size_t SMEM = size_t(STAGES) * STAGE_BYTES + 256 /*barriers*/;
   static_assert(TM % 2 == 0 && BK % 16 == 0 && BM <= 256 && BN <= 256, "tile shape");
-  static_assert(TM != 0 || (BN >= 64 && BN % 64 == 0), "DMMA rank tile is a multiple of 64");
+  static_assert(TM != 0 || BN == 16 || BN == 32 || (BN >= 64 && BN % 64 == 0), "DMMA rank tile 16, 32 or 64 k");
   static_assert((TX >= 8) && (TX % 8 == 0), "8 lanes per warp row");
 };
 
@@ -493,11 +572,40 @@ __global__ void __launch_bounds__(WS_THREADS, 1) mttkrp_f64_ws_sm100(const __gri
             c[0] = if0 + 16 * pn;
             tma_load<C::D>(a_s + pn * (BM * 16), &p.tm_y, &full_tma[s], c);
           }
+        } else if (TM == 0) {
+          bool done = false;
+          if constexpr (C::D < 5) {
+            if (p.a_one_box) {  // all BM / 16 panels as one box {16, BK, BM / 16}
+              int c1[C::D + 1];
+              c1[0] = 0;
+              c1[1] = if0;
+              c1[2] = n0 >> 4;
+#pragma unroll
+              for (int m = 2; m < C::D; ++m) c1[m + 1] = od[m - 2];
+              tma_load<C::D + 1>(a_s, &p.tm_y, &full_tma[s], c1);
+              done = true;
+            }
+          }
+          if (!done) {
+#pragma unroll
+            for (int pm = 0; pm < BM / 16; ++pm) {  // 16-row swizzled panels [k][16] (DMMA layout)
+              c[0] = n0 + 16 * pm;
+              tma_load<C::D>(a_s + pm * (16 * BK), &p.tm_y, &full_tma[s], c);
+            }
+          }
         } else {
           tma_load<C::D>(a_s, &p.tm_y, &full_tma[s], c);
         }
-        const int cf[2] = {j0, if0};
-        tma_load<2>(b_s, &p.tm_f, &full_tma[s], cf);
+        if (TM == 0) {
+#pragma unroll
+          for (int pc = 0; pc < BN / 16; ++pc) {  // 16-column swizzled panels [k][16]
+            const int cf[2] = {j0 + 16 * pc, if0};
+            tma_load<2>(b_s + pc * (16 * BK), &p.tm_f, &full_tma[s], cf);
+          }
+        } else {
+          const int cf[2] = {j0, if0};
+          tma_load<2>(b_s, &p.tm_f, &full_tma[s], cf);
+        }
 #pragma unroll
         for (int i = 0; i < NO; ++i) {
           const int co[2] = {j0, od[i]};
@@ -753,7 +861,9 @@ template <bool KMAJ, int NO, int TM, int BN, int BK>
 static void ws_kernel(const void** fn, size_t* smem) {
   constexpr int stage = WsCfg<KMAJ, NO, TM, BN, BK, 1>::STAGE_BYTES;
   constexpr int fit = (227 * 1024 - 256) / stage;
-  constexpr int S = fit > 4 ? 4 : fit;
+  // narrow rank tiles are HBM-bound: more of their (small) stages in flight
+  constexpr int cap = (TM == 0 && BN < 64) ? 6 : 4;
+  constexpr int S = fit > cap ? cap : fit;
   static_assert(S >= 2, "two stages must fit");
   *fn = reinterpret_cast<const void*>(&mttkrp_f64_ws_sm100<KMAJ, NO, TM, BN, BK, S>);
   *smem = WsCfg<KMAJ, NO, TM, BN, BK, S>::SMEM;
@@ -777,6 +887,8 @@ static void ws_pick(bool kmaj, int no, const void** fn, size_t* smem) {
 bool ws_shape(int rank_tile, int math, int* block_rows, int* block_k) {
   if (math == WS_MATH_DMMA) {
     switch (rank_tile) {
+      case 16: *block_rows = 256; *block_k = 16; return true;
+      case 32: *block_rows = 256; *block_k = 16; return true;
       case 64: *block_rows = 256; *block_k = 16; return true;
       case 128: *block_rows = 128; *block_k = 32; return true;
       case 256: *block_rows = 64; *block_k = 16; return true;
@@ -823,11 +935,33 @@ int launch_ws(const WsRequest& r, cudaStream_t st) {
   }
   cuuint32_t box[5];
   int rc;
-  if (k == 0) {
+  const bool dmma = r.math == WS_MATH_DMMA;  // DMMA consumers read 16-wide swizzled panels
+  static const bool one_box_off = getenv("CPK_WS_PANEL_BOXES") != nullptr;  // A/B switch: per-panel boxes
+  if (k == 0 && dmma && d < 5 && r.dims[0] % 16 == 0 && !one_box_off) {
+    // (i_0 mod 16, i_1, i_0 / 16, i_2, ...): one box {16, BK, BM / 16} lands
+    // the BM / 16 swizzled panels [k][16] of a stage in order
+    cuuint64_t pdim[5], pstr[4];
+    cuuint32_t pbox[5];
+    pdim[0] = 16;
+    pdim[1] = gdim[1];
+    pdim[2] = gdim[0] / 16;
+    pstr[0] = gstr[0];  // i_1
+    pstr[1] = 16 * 8;   // i_0 / 16
+    pbox[0] = 16;
+    pbox[1] = cuuint32_t(BK);
+    pbox[2] = cuuint32_t(BM / 16);
+    for (int m = 2; m < d; ++m) {
+      pdim[m + 1] = gdim[m];
+      pstr[m] = gstr[m - 1];
+      pbox[m + 1] = 1;
+    }
+    rc = encode(&p.tm_y, r.y, d + 1, pdim, pstr, pbox, CU_TENSOR_MAP_SWIZZLE_128B);
+    p.a_one_box = 1;
+  } else if (k == 0) {
     for (int m = 0; m < d; ++m) box[m] = 1;
-    box[0] = cuuint32_t(BM);
+    box[0] = cuuint32_t(dmma ? 16 : BM);
     box[1] = cuuint32_t(BK);
-    rc = encode(&p.tm_y, r.y, d, gdim, gstr, box, CU_TENSOR_MAP_SWIZZLE_NONE);
+    rc = encode(&p.tm_y, r.y, d, gdim, gstr, box, dmma ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE);
   } else {
     for (int m = 0; m < d; ++m) box[m] = 1;
     box[0] = 16;
@@ -838,8 +972,8 @@ int launch_ws(const WsRequest& r, cudaStream_t st) {
   {
     const cuuint64_t fd[2] = {cuuint64_t(r.rank), cuuint64_t(r.dims[f])};
     const cuuint64_t fs[1] = {cuuint64_t(r.ld[f] * 8)};
-    const cuuint32_t fb[2] = {cuuint32_t(BN), cuuint32_t(BK)};
-    rc = encode(&p.tm_f, r.factors[f], 2, fd, fs, fb, CU_TENSOR_MAP_SWIZZLE_NONE);
+    const cuuint32_t fb[2] = {cuuint32_t(dmma ? 16 : BN), cuuint32_t(BK)};
+    rc = encode(&p.tm_f, r.factors[f], 2, fd, fs, fb, dmma ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE);
     if (rc) return rc;
   }
   int oi = 0;
@@ -875,6 +1009,8 @@ int launch_ws(const WsRequest& r, cudaStream_t st) {
   if (r.math == WS_MATH_DMMA) {
     if (BN == 128) ws_pick<0, 128, 32>(kmaj, no, &fn, &smem);
     else if (BN == 256) ws_pick<0, 256, 16>(kmaj, no, &fn, &smem);
+    else if (BN == 32) ws_pick<0, 32, 16>(kmaj, no, &fn, &smem);
+    else if (BN == 16) ws_pick<0, 16, 16>(kmaj, no, &fn, &smem);
     else ws_pick<0, 64, 16>(kmaj, no, &fn, &smem);
   } else if (BN == 128) ws_pick<8, 128, 32>(kmaj, no, &fn, &smem);
   else if (BN == 256) ws_pick<12, 256, 16>(kmaj, no, &fn, &smem);

@@ -58,7 +58,7 @@ class MttkrpPlan:
     ``unroll`` (F), ``team_width`` (b_x) and ``vector_width`` (b_y) keep the
     paper's meaning; on the GPU the column block is the rank tile, so they
     are validated (>= 1) but the kernel's register tile is fixed at 8x8.
-    ``rank_tile`` (0 = auto, else 32/64/128/256), ``splits`` (0 = auto) and
+    ``rank_tile`` (0 = auto, else 16/32/64/128/256), ``splits`` (0 = auto) and
     ``block_k`` (chunk depth, 0 = auto, else 16/32) are the B200
     realization of the rank tiling and of N_T; ``engine`` picks the data
     movement ("auto", "tma" = warp-specialized TMA kernel, "cpasync").
@@ -91,8 +91,8 @@ class MttkrpPlan:
             raise ParameterError("team_width and vector_width must be >= 1")
         if rank < 1:
             raise ParameterError(f"rank must be >= 1, got {rank}")
-        if self.rank_tile not in (0, 32, 64, 128, 256):
-            raise ParameterError(f"rank_tile must be 0, 32, 64, 128 or 256, got {self.rank_tile}")
+        if self.rank_tile not in (0, 16, 32, 64, 128, 256):
+            raise ParameterError(f"rank_tile must be 0, 16, 32, 64, 128 or 256, got {self.rank_tile}")
         if self.splits < 0:
             raise ParameterError(f"splits must be >= 0, got {self.splits}")
         if self.engine not in _ENGINES:
@@ -774,6 +774,7 @@ def heuristic_tile_volume(dims, machine) -> int:
 _TILE_CHOICES = (  # same order as kChoices (ties go to the earlier entry)
     ("tma", 256, 96, 0.95), ("tma", 128, 128, 1.00), ("tma", 64, 256, 0.93),
     ("dmma", 256, 64, 1.02), ("dmma", 128, 128, 1.23), ("dmma", 64, 256, 1.26),
+    ("dmma", 32, 256, 1.15), ("dmma", 16, 256, 0.90),
     ("cpdmma", 128, 128, 0.97), ("cpdmma", 64, 256, 0.88),
     ("cpasync", 128, 128, 0.92), ("cpasync", 64, 128, 0.78), ("cpasync", 32, 64, 0.55),
 )

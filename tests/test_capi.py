@@ -60,9 +60,14 @@ def test_plan_resolution_fills_waves():
     # c2: R=64 -> rank tile 64
     rc, p = plan((512, 512, 512), 1, 64)
     assert rc == 0 and p.rank_tile == 64
-    # tiny rank -> 32-wide tile, 64-row blocks
+    # low rank -> the narrow 16-column DMMA tile (256-row blocks; the small
+    # mode 0 is merged with its neighbour into 4096 rows)
     rc, p = plan((64, 64, 64), 0, 16)
-    assert rc == 0 and p.rank_tile == 32 and p.block_rows == 64
+    assert rc == 0 and p.rank_tile == 16 and p.block_rows == 256 and p.engine == 3
+    # R = 24 and 96 -> 32-wide tiles; 40 -> one 64-wide tile
+    for r, rt in ((24, 32), (96, 32), (40, 64)):
+        rc, p = plan((512, 512, 512), 1, r)
+        assert rc == 0 and p.rank_tile == rt, (r, p.rank_tile)
 
 
 def test_tiny_tile_volume_is_capped():

@@ -168,7 +168,7 @@ def test_c2_rank_tile_sweep_parity(golden):
     g, dims, rank, y, fs = _config(golden, "c2")
     t = ck.DenseTensor(dims, y)
     m = ck.KruskalTensor(np.ones(rank), fs, validate=False)
-    for rt in (32, 64, 128):
+    for rt in (16, 32, 64, 128):
         for k in range(3):
             got = ck.run(t, m, MttkrpPlan(Variant.B200, k, rank_tile=rt)).matrix
             assert oracle.rel_err(got, g[f"G{k}"]) <= TOL
@@ -212,6 +212,26 @@ def test_tma_engine_parity(dims, rank_tile, engine):
             ref = oracle.mttkrp_ref(y, dims, k, fs, lam)
             for splits in (0, 1, 5):
                 plan = MttkrpPlan(Variant.B200, k, rank_tile=rank_tile, splits=splits, engine=engine)
+                got = ck.run(t, m, plan).matrix
+                assert oracle.rel_err(got, ref) <= TOL, (dims, rank, k, splits)
+
+
+@pytest.mark.parametrize("rank_tile", [16, 32])
+@pytest.mark.parametrize("dims", [(40, 36, 34), (300, 66, 3), (34, 40, 70, 6), (6, 4, 8, 10, 4), (64, 2)])
+def test_narrow_dmma_tiles_parity(dims, rank_tile):
+    """The 16- and 32-column DMMA tiles (low-rank end): ragged rows (I_k not a
+    multiple of 256), rank tails inside a fragment, several rank tiles,
+    d = 2..5, splits; mode 0 exercises the permuted M-major fragment rows."""
+    for rank in (2, 10, 24, 40):
+        y = rng_for(sum(dims) * rank + 1).random(int(np.prod(dims)))
+        fs = [rng_for(rank + 5 * j).random((n, rank)) for j, n in enumerate(dims)]
+        lam = rng_for(13).random(rank) + 0.5
+        m = ck.KruskalTensor(lam, fs)
+        t = ck.DenseTensor(dims, y)
+        for k in range(len(dims)):
+            ref = oracle.mttkrp_ref(y, dims, k, fs, lam)
+            for splits in (0, 1, 5):
+                plan = MttkrpPlan(Variant.B200, k, rank_tile=rank_tile, splits=splits, engine="dmma")
                 got = ck.run(t, m, plan).matrix
                 assert oracle.rel_err(got, ref) <= TOL, (dims, rank, k, splits)
 

@@ -133,7 +133,10 @@ if __name__ == "__main__":
     ap.add_argument("--launches")
     ap.add_argument("--aux", action="store_true",
                     help="not the bench's dominant kernel: write the .txt summaries only, leave ncu_summary.json")
+    ap.add_argument("--out", default=None, help="directory for the summaries (default profiles/)")
     a = ap.parse_args()
+    if a.out:
+        PROF = Path(a.out)
     PROF.mkdir(exist_ok=True)
     if a.launches:
         summarize_launches(Path(a.launches), a.tag)

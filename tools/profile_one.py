@@ -10,6 +10,10 @@ import numpy as np
 import torch
 
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+if "--lib" in sys.argv:  # A/B: another build of the library
+    from paper_2510_14891_b200 import _lib as _l  # noqa: E402
+
+    _l.LIB_PATH = Path(sys.argv[sys.argv.index("--lib") + 1]).resolve()
 import paper_2510_14891_b200 as ck  # noqa: E402
 from paper_2510_14891_b200.mttkrp import MttkrpPlan, Variant, mttkrp_device  # noqa: E402
 
@@ -22,6 +26,7 @@ ap.add_argument("--rank-tile", type=int, default=0)
 ap.add_argument("--splits", type=int, default=0)
 ap.add_argument("--block-k", type=int, default=0)
 ap.add_argument("--engine", default="auto")
+ap.add_argument("--lib", default=None)
 a = ap.parse_args()
 dev = torch.device("cuda", 0)
 t = ck.DenseTensor.uniform(tuple(a.dims), seed=0, device=dev)
