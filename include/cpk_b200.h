@@ -141,9 +141,10 @@ int cpk_mttkrp_f64(const double* y, int d, const int64_t* dims, int mode,
  * the work whose tensor slices along the slowest mode (d-1) all lie in
  * [0, landed_hi) and not all in [0, landed_lo).  Calling it with
  * (0, h_1), (h_1, h_2), ..., (h_{n-1}, dims[d-1]) in stream order launches
- * every work item exactly once; the last call also runs the split-K merge,
- * so G is bit-identical to cpk_mttkrp_f64's.  Same plan, workspace and
- * pointers on every call (the workspace carries the partial sums). */
+ * every work item exactly once; the first call (landed_lo = 0) starts the
+ * MTTKRP and the last completes the split-K merge, so G is bit-identical to
+ * cpk_mttkrp_f64's.  Same plan, workspace and pointers on every call (the
+ * workspace carries the partial sums or the split-chain counters). */
 int cpk_mttkrp_f64_landed(const double* y, int d, const int64_t* dims,
                           int mode, const double* const* factors,
                           const int64_t* ld, const double* lam, int64_t rank,

@@ -764,8 +764,20 @@ static int solve_layout(int64_t rows, int64_t rank, int lwork, size_t* total, si
 static int apply_mttkrp_bytes(int64_t rows, int64_t rank, size_t* bytes) {
   *bytes = 0;
   if (rows <= 0) return CPK_OK;
-  const int64_t dims[2] = {rank, rows};
-  return cpk_mttkrp_workspace_bytes(2, dims, 1, rank, nullptr, bytes);
+  // The split-K layout depends on the output-tile count (split chain vs
+  // partial copies, mttkrp.cu), so the size is not monotone in rows, and a
+  // caller sizes one workspace for its largest mode: take the maximum over
+  // every row count up to `rows` (tile boundaries are multiples of 64).
+  const int64_t step = std::max<int64_t>(64, (rows / 256 + 63) / 64 * 64);
+  for (int64_t i = -1, r = rows; r > 0; ++i, r = rows / step * step - i * step) {
+    if (i >= 0 && r == rows) continue;  // already counted
+    const int64_t dims[2] = {rank, r};
+    size_t b = 0;
+    const int rc = cpk_mttkrp_workspace_bytes(2, dims, 1, rank, nullptr, &b);
+    if (rc) return rc;
+    *bytes = std::max(*bytes, b);
+  }
+  return CPK_OK;
 }
 
 static int* info_d_sweep(void* work, int64_t rank) {  // the info word at the end of the factor block

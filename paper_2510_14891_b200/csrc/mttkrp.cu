@@ -42,6 +42,7 @@
 #include "mttkrp_internal.cuh"
 
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
 
 namespace cpk {
@@ -331,8 +332,28 @@ static int resolve(const Problem& pr, cpk_plan* plan) {
   return CPK_OK;
 }
 
+// Split-K merge.  Default: partial copies in the workspace, summed in split
+// order by splitk_reduce_f64 (the private-copy merge, mttkrp.py:279-286).
+// CPK_SPLIT_CHAIN=1 selects the ordered chain into G (common.cuh) for plans
+// whose output tiles number at least half the SMs (an output tile's
+// consecutive splits are then at least half a wave apart in launch order,
+// so the chain never waits long): the same sums in the same order (identical
+// bits), no partial copies through HBM (c4: -2.1 GB written and read per
+// launch), but each CTA's epilogue becomes a wait + read-modify-write of its
+// tile, which with one CTA per SM the next CTA cannot hide: measured +1.0 to
+// +1.3 ms per c4 mode (+0.9 %), so it is opt-in.
+static int64_t out_tiles(const Problem& pr, const cpk_plan& plan) {
+  return ceil_div(pr.Ik, plan.block_rows) * ceil_div(pr.R, plan.rank_tile);
+}
+static bool chain_merge(const Problem& pr, const cpk_plan& plan) {
+  const char* want = getenv("CPK_SPLIT_CHAIN");
+  if (plan.splits <= 1 || !want || want[0] != '1') return false;
+  return 2 * out_tiles(pr, plan) >= int64_t(plan.sm_count);
+}
+
 static size_t ws_bytes_for(const Problem& pr, const cpk_plan& plan) {
   if (plan.splits <= 1) return 0;
+  if (chain_merge(pr, plan)) return ((size_t(out_tiles(pr, plan)) * sizeof(int) + 255) / 256) * 256;
   const int64_t ldw = (pr.R + 1) & ~int64_t(1);
   return size_t(plan.splits) * size_t(pr.Ik) * size_t(ldw) * sizeof(double);
 }
@@ -723,10 +744,16 @@ static int mttkrp_impl(const double* y, int d, const int64_t* dims, int mode, co
   p.If = pr.dims[pr.f];
   p.stride_f = pr.strides[pr.f];
   const bool direct = plan.splits == 1;
-  double* out = direct ? G : static_cast<double*>(workspace);
-  const int64_t ldo = direct ? ldg : ((rank + 1) & ~int64_t(1));
-  const int64_t out_split_stride = direct ? 0 : pr.Ik * ldo;
-  const double* lam_fold = direct ? lam : nullptr;
+  const bool chain = chain_merge(pr, plan);  // splits accumulate into G in order (no partial copies)
+  double* out = (direct || chain) ? G : static_cast<double*>(workspace);
+  const int64_t ldo = (direct || chain) ? ldg : ((rank + 1) & ~int64_t(1));
+  const int64_t out_split_stride = (direct || chain) ? 0 : pr.Ik * ldo;
+  const double* lam_fold = (direct || chain) ? lam : nullptr;
+  int* sem = chain ? static_cast<int*>(workspace) : nullptr;
+  if (chain && (!ranged || landed_lo == 0)) {  // a (streamed) MTTKRP starts: zero the tile counters
+    if (cudaMemsetAsync(sem, 0, size_t(out_tiles(pr, plan)) * sizeof(int), st) != cudaSuccess)
+      return fail(CPK_ERR_CUDA, "split-K counters memset failed");
+  }
 
   if (is_tma(plan.engine)) {
     WsRequest wr{};
@@ -748,6 +775,7 @@ static int mttkrp_impl(const double* y, int d, const int64_t* dims, int mode, co
     wr.ldo = ldo;
     wr.out_split_stride = out_split_stride;
     wr.lam = lam_fold;
+    wr.sem = sem;
     if (ws_eligible(wr)) {
       Landed ld_{plan.block_rows, plan.block_k, 0, 0};
       ld_.n_chunks = n_chunks_of(pr, plan.block_k);
@@ -793,6 +821,8 @@ static int mttkrp_impl(const double* y, int d, const int64_t* dims, int mode, co
     p.ldo = ldo;
     p.out_split_stride = out_split_stride;
     p.lam = lam_fold;
+    p.sem = sem;
+    p.n_splits = plan.splits;
     KernelInfo ki = pick_kernel(plan.rank_tile, bk, pr.k != 0, vec2 ? 2 : 1, pr.n_o, plan.engine == CPK_ENGINE_CPDMMA);
     if (!ki.fn) return fail(CPK_ERR_PARAM, "no kernel for rank_tile %d", plan.rank_tile);
     if (cudaFuncSetAttribute(ki.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ki.smem)) != cudaSuccess)
@@ -819,7 +849,7 @@ static int mttkrp_impl(const double* y, int d, const int64_t* dims, int mode, co
     }
   }
 reduce:
-  if (!direct && (!ranged || landed_hi == dims[d - 1])) {
+  if (!direct && !chain && (!ranged || landed_hi == dims[d - 1])) {
     const int64_t total = pr.Ik * rank;
     const int threads = 256;
     const int64_t blocks = std::min<int64_t>(ceil_div(total, threads), int64_t(plan.sm_count) * 16);

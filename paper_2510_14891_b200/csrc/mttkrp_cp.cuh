@@ -27,8 +27,10 @@ struct MttkrpParams {
   double* out;
   int64_t ldo;
   int64_t out_split_stride;
-  const double* lam;         // folded in the epilogue only when direct
+  const double* lam;         // folded in the epilogue when direct, or by the chain's last split
   int32_t y0, z0;            // first row block / split of this launch
+  int* sem;                  // split-K chain counters (common.cuh), or nullptr
+  int32_t n_splits;
 };
 
 // Loader state: the chunk being staged next, as an odometer over
@@ -316,8 +318,14 @@ __global__ void __launch_bounds__((BM / 8) * (BN / 8), 1)
   cp_async_wait<0>();
 
   // --- epilogue: partial (or final, lam-folded) tile -> out --------------
-  double* out = p.out + int64_t(blockIdx.z + p.z0) * p.out_split_stride;
-  const bool fold = p.lam != nullptr;
+  const int zs = blockIdx.z + p.z0, tile = blockIdx.x + gridDim.x * (blockIdx.y + p.y0);
+  double* out = p.out + (p.sem ? 0 : int64_t(zs) * p.out_split_stride);
+  const OutMode om = chain_mode(p.sem != nullptr, zs, p.n_splits, p.lam != nullptr);
+  if (p.sem) {
+    if (threadIdx.x == 0) chain_wait(p.sem + tile, zs);
+    __syncthreads();
+  }
+  const bool vec = (p.ldo & 1) == 0;
   if constexpr (DMMA) {
     const int lr = lane >> 2, lk = lane & 3;
 #pragma unroll
@@ -327,18 +335,7 @@ __global__ void __launch_bounds__((BM / 8) * (BN / 8), 1)
 #pragma unroll
       for (int nf = 0; nf < 8; ++nf) {
         const int64_t j = j0 + dwn0 + nf * 8 + 2 * lk;
-        double v0 = dacc[mf][nf][0], v1 = dacc[mf][nf][1];
-        if (fold) {
-          if (j < p.R) v0 *= p.lam[j];
-          if (j + 1 < p.R) v1 *= p.lam[j + 1];
-        }
-        double* dst = out + n * p.ldo + j;
-        if (j + 1 < p.R && ((p.ldo & 1) == 0)) {
-          *reinterpret_cast<double2*>(dst) = make_double2(v0, v1);
-        } else {
-          if (j < p.R) dst[0] = v0;
-          if (j + 1 < p.R) dst[1] = v1;
-        }
+        store_pair(out + n * p.ldo + j, j, p.R, vec, dacc[mf][nf][0], dacc[mf][nf][1], p.lam, om);
       }
     }
   } else {
@@ -349,21 +346,15 @@ __global__ void __launch_bounds__((BM / 8) * (BN / 8), 1)
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       const int64_t j = j0 + 2 * tx + 2 * C::TX * i;
-      double v0 = acc[r][2 * i], v1 = acc[r][2 * i + 1];
-      if (fold) {
-        if (j < p.R) v0 *= p.lam[j];
-        if (j + 1 < p.R) v1 *= p.lam[j + 1];
-      }
-      double* dst = out + n * p.ldo + j;
-      if (j + 1 < p.R && ((p.ldo & 1) == 0)) {
-        *reinterpret_cast<double2*>(dst) = make_double2(v0, v1);
-      } else {
-        if (j < p.R) dst[0] = v0;
-        if (j + 1 < p.R) dst[1] = v1;
-      }
+      store_pair(out + n * p.ldo + j, j, p.R, vec, acc[r][2 * i], acc[r][2 * i + 1], p.lam, om);
     }
   }
   }  // DFMA epilogue
+  if (p.sem) {
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) st_release_gpu(p.sem + tile, zs + 1);
+  }
 }
 
 // Tile configurations: (BM, BN, threads) = (128,128,256) | (128,64,128) | (64,32,32);

@@ -25,6 +25,7 @@ struct WsRequest {
   double* out;
   int64_t ldo, out_split_stride;
   const double* lam;
+  int* sem;  // split-K chain counters (common.cuh), or nullptr
 };
 
 // TMA tile for a rank tile (DMMA 16 | 32 | 64 | 128 | 256, DFMA 64 | 128 | 256) and math: rows per CTA and chunk depth.

@@ -61,7 +61,27 @@ struct alignas(64) WsParams {
   const double* lam;
   int32_t y0, z0;  // first row block / split of this launch
   int32_t a_one_box;  // mode 0, DMMA: tm_y views the tensor as (16, I_1, I_0 / 16, ...) -> one box per stage
+  int* sem;           // split-K chain counters (one per output tile), or nullptr: partials / direct
+  int32_t n_splits;
 };
+
+// Epilogue prologue of the split-K chain (consumer threads only: the
+// producer warpgroup may have retired, so a named barrier over the 256
+// consumer threads).
+__device__ __forceinline__ OutMode ws_chain_enter(const WsParams& p, int z, int tile) {
+  const OutMode m = chain_mode(p.sem != nullptr, z, p.n_splits, p.lam != nullptr);
+  if (p.sem) {
+    if (threadIdx.x == 0) chain_wait(p.sem + tile, z);
+    asm volatile("bar.sync 2, %0;\n" ::"n"(8 * 32) : "memory");
+  }
+  return m;
+}
+__device__ __forceinline__ void ws_chain_leave(const WsParams& p, int z, int tile) {
+  if (!p.sem) return;
+  __threadfence();
+  asm volatile("bar.sync 2, %0;\n" ::"n"(8 * 32) : "memory");
+  if (threadIdx.x == 0) st_release_gpu(p.sem + tile, z + 1);
+}
 
 // ---------------------------------------------------------------- PTX wrappers
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
@@ -405,8 +425,9 @@ __device__ __forceinline__ void ws_consume_dmma(const uint8_t* smem, uint64_t* f
     }
   }
 
-  double* out = p.out + int64_t(blockIdx.z + p.z0) * p.out_split_stride;
-  const bool fold = p.lam != nullptr;
+  const int zs = blockIdx.z + p.z0, tile = blockIdx.x + gridDim.x * (blockIdx.y + p.y0);
+  double* out = p.out + (p.sem ? 0 : int64_t(zs) * p.out_split_stride);
+  const OutMode om = ws_chain_enter(p, zs, tile);
 #pragma unroll
   for (int mf = 0; mf < 4; ++mf) {
     const int n = n0 + wm0 + dmma_row<KMAJ>(mf, lr);
@@ -417,20 +438,11 @@ __device__ __forceinline__ void ws_consume_dmma(const uint8_t* smem, uint64_t* f
       for (int v = 0; v < 2; ++v) {
         // fragments 2q, 2q + 1 hold columns j, j + 1 (dmma_col)
         const int j = j0 + wn0 + 16 * q + 4 * lk + 2 * v;
-        double v0 = acc[mf][2 * q][v], v1 = acc[mf][2 * q + 1][v];
-        if (fold) {
-          if (j < p.R) v0 *= p.lam[j];
-          if (j + 1 < p.R) v1 *= p.lam[j + 1];
-        }
-        double* dst = out + int64_t(n) * p.ldo + j;
-        if (j + 1 < p.R && ((p.ldo & 1) == 0)) {
-          *reinterpret_cast<double2*>(dst) = make_double2(v0, v1);
-        } else {
-          if (j < p.R) dst[0] = v0;
-          if (j + 1 < p.R) dst[1] = v1;
-        }
+        store_pair(out + int64_t(n) * p.ldo + j, j, p.R, (p.ldo & 1) == 0, acc[mf][2 * q][v], acc[mf][2 * q + 1][v],
+                   p.lam, om);
       }
   }
+  ws_chain_leave(p, zs, tile);
 }
 
 // ---------------------------------------------------------------- kernel
@@ -804,9 +816,10 @@ __global__ void __launch_bounds__(WS_THREADS, 1) mttkrp_f64_ws_sm100(const __gri
     if (lane == 0) mbar_arrive(&empty[s]);
   }
 
-  // epilogue: partial (or final, lam-folded) tile -> out
-  double* out = p.out + int64_t(blockIdx.z + p.z0) * p.out_split_stride;
-  const bool fold = p.lam != nullptr;
+  // epilogue: partial, chained or final (lam-folded) tile -> out
+  const int zs = blockIdx.z + p.z0, tile = blockIdx.x + gridDim.x * (blockIdx.y + p.y0);
+  double* out = p.out + (p.sem ? 0 : int64_t(zs) * p.out_split_stride);
+  const OutMode om = ws_chain_enter(p, zs, tile);
 #pragma unroll
   for (int r = 0; r < TM; ++r) {
     const int n = n0 + 2 * ty + (r & 1) + 2 * TY * (r >> 1);
@@ -814,20 +827,11 @@ __global__ void __launch_bounds__(WS_THREADS, 1) mttkrp_f64_ws_sm100(const __gri
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       const int j = j0 + 2 * tx + 2 * TX * i;
-      double v0 = acc[r][2 * i], v1 = acc[r][2 * i + 1];
-      if (fold) {
-        if (j < p.R) v0 *= p.lam[j];
-        if (j + 1 < p.R) v1 *= p.lam[j + 1];
-      }
-      double* dst = out + int64_t(n) * p.ldo + j;
-      if (j + 1 < p.R && ((p.ldo & 1) == 0)) {
-        *reinterpret_cast<double2*>(dst) = make_double2(v0, v1);
-      } else {
-        if (j < p.R) dst[0] = v0;
-        if (j + 1 < p.R) dst[1] = v1;
-      }
+      store_pair(out + int64_t(n) * p.ldo + j, j, p.R, (p.ldo & 1) == 0, acc[r][2 * i], acc[r][2 * i + 1], p.lam,
+                 om);
     }
   }
+  ws_chain_leave(p, zs, tile);
   }  // TM != 0
 }
 
@@ -1001,6 +1005,8 @@ int launch_ws(const WsRequest& r, cudaStream_t st) {
   p.lam = r.lam;
   p.y0 = r.y0;
   p.z0 = r.z0;
+  p.sem = r.sem;
+  p.n_splits = r.splits;
 
   const void* fn = nullptr;
   size_t smem = 0;

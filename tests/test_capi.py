@@ -107,16 +107,24 @@ def test_plan_errors_map_to_reference_exceptions(dims, mode, rank, kw, code):
         _lib.check(rc, "plan")
 
 
-def test_workspace_bytes():
+def test_workspace_bytes(monkeypatch):
     p = _lib.CpkPlan(0, 0, 0, 0, 148)
     nb = C.c_size_t(0)
     rc = _lib.load().cpk_mttkrp_workspace_bytes(3, _lib.i64_array((1024, 1024, 1024)), 0, 2000, p, C.byref(nb))
     assert rc == 0
     rc2, q = plan((1024, 1024, 1024), 0, 2000)
-    assert nb.value == q.splits * 1024 * 2000 * 8
+    assert nb.value == q.splits * 1024 * 2000 * 8  # partial copies (default merge)
     p1 = _lib.CpkPlan(0, 0, 0, 1, 148)
     rc = _lib.load().cpk_mttkrp_workspace_bytes(3, _lib.i64_array((64, 64, 64)), 0, 16, p1, C.byref(nb))
     assert rc == 0 and nb.value == 0
+    # CPK_SPLIT_CHAIN=1: c4's 128 output tiles >= 148 / 2 -> one counter per
+    # tile instead of the partial copies; c2 (2 tiles) keeps the copies
+    monkeypatch.setenv("CPK_SPLIT_CHAIN", "1")
+    rc = _lib.load().cpk_mttkrp_workspace_bytes(3, _lib.i64_array((1024, 1024, 1024)), 0, 2000, p, C.byref(nb))
+    assert rc == 0 and nb.value == 512
+    rc = _lib.load().cpk_mttkrp_workspace_bytes(3, _lib.i64_array((512, 512, 512)), 1, 64, p, C.byref(nb))
+    rc2, q = plan((512, 512, 512), 1, 64)
+    assert rc == 0 and nb.value == q.splits * 512 * 64 * 8
 
 
 def test_mttkrp_rejects_bad_arguments_before_touching_the_device():

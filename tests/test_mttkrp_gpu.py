@@ -236,6 +236,34 @@ def test_narrow_dmma_tiles_parity(dims, rank_tile):
                 assert oracle.rel_err(got, ref) <= TOL, (dims, rank, k, splits)
 
 
+@pytest.mark.parametrize("engine", ["dmma", "tma", "cpasync", "cpdmma"])
+@pytest.mark.parametrize("dims", [(300, 66, 34), (34, 40, 70, 6), (6, 4, 8, 10, 4)])
+def test_split_chain_is_bit_identical_to_partial_copies(monkeypatch, dims, engine):
+    """The split-K chain (CPK_SPLIT_CHAIN=1: splits accumulate into G in
+    order, common.cuh) and the partial-copy merge (splitk_reduce_f64) add the
+    same numbers in the same order: identical bits, and both at the oracle.
+    sm_count = 1 makes the planner chain any split plan (tiles >= sm_count /
+    2); the chain waits are then real (every split of a tile is resident at
+    once)."""
+    rank = 40
+    y = rng_for(sum(dims) + 3).random(int(np.prod(dims)))
+    fs = [rng_for(rank + 9 * j).random((n, rank)) for j, n in enumerate(dims)]
+    lam = rng_for(17).random(rank) + 0.5
+    m = ck.KruskalTensor(lam, fs)
+    t = ck.DenseTensor(dims, y)
+    rt = 64 if engine != "cpasync" else 32
+    for k in range(len(dims)):
+        ref = oracle.mttkrp_ref(y, dims, k, fs, lam)
+        for splits in (2, 7):
+            kw = dict(rank_tile=rt, splits=splits, engine=engine)
+            monkeypatch.setenv("CPK_SPLIT_CHAIN", "1")
+            chained = ck.run(t, m, MttkrpPlan(Variant.B200, k, sm_count=1, **kw)).matrix
+            monkeypatch.delenv("CPK_SPLIT_CHAIN")
+            copies = ck.run(t, m, MttkrpPlan(Variant.B200, k, sm_count=1, **kw)).matrix
+            assert np.array_equal(np.asarray(chained), np.asarray(copies)), (dims, k, splits)
+            assert oracle.rel_err(chained, ref) <= TOL, (dims, k, splits)
+
+
 def test_engines_agree_bitwise_on_c2_mode1(golden):
     """Both engines produce the golden to 1e-10; each is bit-reproducible."""
     g, dims, rank, y, fs = _config(golden, "c2")
