@@ -94,6 +94,7 @@ __device__ __forceinline__ void st_l2_hint(double* a, double x, uint64_t pol) {
 // G as the split chain's running sum (L2 hints; add = z > 0).
 struct OutMode {
   bool chain, add, fold;
+  bool hint;  // use the L2 policy `pol` on every access
   uint64_t pol;
 };
 
@@ -103,7 +104,16 @@ struct OutMode {
 __device__ __forceinline__ void store_pair(double* dst, int64_t j, int64_t R, bool vec, double v0, double v1,
                                            const double* lam, const OutMode& m) {
   const bool both = j + 1 < R && vec;
-  if (m.add) {
+  if (m.add && !m.hint) {
+    if (both) {
+      const double2 o = __ldcg(reinterpret_cast<const double2*>(dst));
+      v0 = o.x + v0;
+      v1 = o.y + v1;
+    } else {
+      if (j < R) v0 = __ldcg(dst) + v0;
+      if (j + 1 < R) v1 = __ldcg(dst + 1) + v1;
+    }
+  } else if (m.add) {
     if (both) {
       const double2 o = ld_l2_hint2(dst, m.pol);
       v0 = o.x + v0;
@@ -117,7 +127,7 @@ __device__ __forceinline__ void store_pair(double* dst, int64_t j, int64_t R, bo
     if (j < R) v0 *= lam[j];
     if (j + 1 < R) v1 *= lam[j + 1];
   }
-  if (m.chain) {
+  if (m.hint) {
     if (both) {
       st_l2_hint2(dst, v0, v1, m.pol);
     } else {
@@ -133,11 +143,15 @@ __device__ __forceinline__ void store_pair(double* dst, int64_t j, int64_t R, bo
 }
 
 // Chain state of split z: add for z > 0, lam on the last split, the L2 policy.
+// Without the hints the running sum went to DRAM between splits (c4: 2.05
+// GB written, +0.6 GB read per launch); evict_first on the partial copies
+// changed nothing (profiles/r02_chain_exp2.log).
 __device__ __forceinline__ OutMode chain_mode(bool chain, int z, int n_splits, bool have_lam) {
   OutMode m;
   m.chain = chain;
   m.add = chain && z > 0;
   m.fold = have_lam && (!chain || z == n_splits - 1);
+  m.hint = chain;
   m.pol = chain ? (z == n_splits - 1 ? l2_policy_release() : l2_policy_keep()) : 0;
   return m;
 }

@@ -351,9 +351,11 @@ __global__ void __launch_bounds__((BM / 8) * (BN / 8), 1)
   }
   }  // DFMA epilogue
   if (p.sem) {
-    __threadfence();
     __syncthreads();
-    if (threadIdx.x == 0) st_release_gpu(p.sem + tile, zs + 1);
+    if (threadIdx.x == 0) {
+      __threadfence();  // cumulative: the barrier ordered the CTA's stores before it
+      st_release_gpu(p.sem + tile, zs + 1);
+    }
   }
 }
 

@@ -78,9 +78,11 @@ __device__ __forceinline__ OutMode ws_chain_enter(const WsParams& p, int z, int 
 }
 __device__ __forceinline__ void ws_chain_leave(const WsParams& p, int z, int tile) {
   if (!p.sem) return;
-  __threadfence();
   asm volatile("bar.sync 2, %0;\n" ::"n"(8 * 32) : "memory");
-  if (threadIdx.x == 0) st_release_gpu(p.sem + tile, z + 1);
+  if (threadIdx.x == 0) {
+    __threadfence();  // cumulative: the barrier ordered the consumers' stores before it
+    st_release_gpu(p.sem + tile, z + 1);
+  }
 }
 
 // ---------------------------------------------------------------- PTX wrappers

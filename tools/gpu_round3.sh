@@ -14,7 +14,7 @@ for m in 0 1; do
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:mttkrp_f64 -s 1 -c 1 \
     -o /tmp/prof_c4_mode${m}_$TAG -f python tools/profile_one.py --mode $m --reps 2 > $O/ncu_full_mode${m}_$TAG.log 2>&1
   python tools/ncu_summary.py /tmp/prof_c4_mode${m}_$TAG.ncu-rep --tag $TAG --out $O >> $O/ncu_full_mode${m}_$TAG.log 2>&1
-  cp /tmp/prof_c4_mode${m}_$TAG.ncu-rep $O/ 2>/dev/null
+  python tools/ncu_lds.py /tmp/prof_c4_mode${m}_$TAG.ncu-rep regex:mttkrp 8 > $O/lds_c4_mode${m}_$TAG.txt 2>&1
 done
 du -sh $O
 echo done
