@@ -185,7 +185,8 @@ def test_c4_row_sampled_parity():
     for k in range(3):
         got = ck.run(t, m, MttkrpPlan(Variant.B200, k)).matrix.cpu().numpy()
         inner.append((got * fs[k]).sum(axis=0))  # the same vector for every mode
-        for n in (0, 517, 1023):
+        # first/last rows, both sides of the 256-row tile boundaries, one inside
+        for n in (0, 255, 256, 517, 767, 768, 1023):
             ys = gen.splitmix_slice(dims, k, n, seed)
             sub_dims = tuple(1 if j == k else e for j, e in enumerate(dims))
             sub_f = [a[n:n + 1] if j == k else a for j, a in enumerate(fs)]
@@ -509,7 +510,7 @@ def test_c5_full_size_row_sampled_parity():
             # size-independent identity: sum_n G_k[n, :] * A_k[n, :] = <Y, a_0j o a_1j o a_2j>
             # is the same vector for every mode k
             inner.append((got * fs[k]).sum(axis=0))
-            for n in (0, dims[k] - 1):
+            for n in (0, 255, 256, dims[k] - 1):
                 ys = gen.splitmix_slice(dims, k, n, seed)
                 sub_dims = tuple(1 if j == k else e for j, e in enumerate(dims))
                 sub_f = [a[n:n + 1] if j == k else a for j, a in enumerate(fs)]
