@@ -218,3 +218,27 @@ def test_single_mode_update_matches_reference(golden, monkeypatch, name, solve):
             err_a = oracle.rel_err(fs[k].cpu().numpy(), st[f"{name}/A{k}"])
             err_l = oracle.rel_err(lam.cpu().numpy(), st[f"{name}/lam{k}"])
             assert err_a <= tol and err_l <= tol, (k, path, err_a, err_l, tol)
+
+
+def test_random_shapes_cp_als_fuzz():
+    """Seeded fuzz of the whole sweep against the oracle's cp_als restatement
+    (cpals.py:92-171): orders 3-5, odd and even extents, ranks across every
+    rank tile (16 / 32 / 64 / 128 columns, rank tails) and both solve paths
+    (R > 256 takes the multi-CTA sweep), 3 sweeps each; fits <= 1e-8 and the
+    weights at the oracle's."""
+    rng = np.random.Generator(np.random.Philox(2024))
+    cases = []
+    for _ in range(10):
+        d = int(rng.integers(3, 6))
+        dims = tuple(int(x) for x in rng.integers(3, 26 if d > 3 else 60, size=d))
+        rank = int(rng.choice([1, 5, 16, 17, 33, 64, 70, 130]))
+        cases.append((dims, rank))
+    cases.append(((40, 36, 34), 300))  # the R > 256 solve
+    for dims, rank in cases:
+        y = rng.random(int(np.prod(dims)))
+        model, tr = ck.cp_als(ck.DenseTensor(dims, y), ck.AlsConfig(rank=rank, tol=0.0, max_iters=3, seed=3))
+        ref_lam, _, ref_fits = oracle.cp_als(y, dims, rank, max_iters=3, tol=0.0, seed=3)
+        dev = float(np.max(np.abs(np.asarray(tr.fits) - np.asarray(ref_fits))))
+        assert dev <= 1e-8, (dims, rank, dev)
+        w = model.weights.cpu().numpy() if hasattr(model.weights, "cpu") else np.asarray(model.weights)
+        assert oracle.rel_err(w, ref_lam) <= 1e-6, (dims, rank)
