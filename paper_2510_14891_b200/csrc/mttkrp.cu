@@ -838,11 +838,13 @@ static int mttkrp_impl(const double* y, int d, const int64_t* dims, int mode, co
         z1 = ld_.splits_ready(pr, plan.splits, landed_hi);
       }
     }
-    p.y0 = int32_t(y0);
     p.z0 = int32_t(z0);
-    dim3 grid(unsigned(ceil_div(rank, plan.rank_tile)), unsigned(y1 - y0), unsigned(z1 - z0));
-    if (grid.y > 65535u || grid.z > 65535u) return fail(CPK_ERR_PARAM, "grid too large (I_k or splits)");
-    if (grid.y > 0 && grid.z > 0) {
+    if (z1 - z0 > 65535) return fail(CPK_ERR_PARAM, "grid too large (splits)");
+    // row blocks beyond the 65535 grid-y limit go in several launches
+    for (int64_t yb = y0; yb < y1 && z1 > z0; yb += 65535) {
+      p.y0 = int32_t(yb);
+      dim3 grid(unsigned(ceil_div(rank, plan.rank_tile)), unsigned(std::min<int64_t>(y1 - yb, 65535)),
+                unsigned(z1 - z0));
       void* args[] = {&p};
       cudaError_t e = cudaLaunchKernel(ki.fn, grid, dim3(ki.threads), args, ki.smem, st);
       if (e != cudaSuccess) return fail(CPK_ERR_CUDA, "mttkrp launch: %s", cudaGetErrorString(e));

@@ -31,6 +31,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <cstdlib>
 #include <mutex>
 
@@ -1026,10 +1027,16 @@ int launch_ws(const WsRequest& r, cudaStream_t st) {
   if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) != cudaSuccess)
     return check_launch("ws set smem");
   const int64_t gx = (r.rank + BN - 1) / BN;
-  dim3 grid(unsigned(gx), unsigned(r.y1 - r.y0), unsigned(r.z1 - r.z0));
-  void* args[] = {&p};
-  cudaError_t e = cudaLaunchKernel(fn, grid, dim3(WS_THREADS), args, smem, st);
-  if (e != cudaSuccess) return fail(CPK_ERR_CUDA, "ws launch: %s", cudaGetErrorString(e));
+  if (r.z1 - r.z0 > 65535) return fail(CPK_ERR_PARAM, "too many splits for one launch");
+  // row blocks beyond the 65535 grid-y limit (I_k > 16.7 M rows at 256-row
+  // tiles) go in several launches; p.y0 keeps the global row block
+  for (int32_t y = r.y0; y < r.y1; y += 65535) {
+    p.y0 = y;
+    dim3 grid(unsigned(gx), unsigned(std::min(r.y1 - y, 65535)), unsigned(r.z1 - r.z0));
+    void* args[] = {&p};
+    cudaError_t e = cudaLaunchKernel(fn, grid, dim3(WS_THREADS), args, smem, st);
+    if (e != cudaSuccess) return fail(CPK_ERR_CUDA, "ws launch: %s", cudaGetErrorString(e));
+  }
   return CPK_OK;
 }
 

@@ -650,3 +650,17 @@ def test_gemm_and_full_krp_names_keep_reference_budgets():
         ck.mttkrp_gemm(t, m, 1, scratch_cap_bytes=10)
     with pytest.raises(ck.ParameterError):
         ck.mttkrp_gemm(ck.DenseTensor((5,), np.ones(5)), ck.KruskalTensor(np.ones(2), [np.ones((5, 2))]), 0)
+
+
+def test_tall_mode_beyond_the_grid_y_limit():
+    """A mode with more row blocks than gridDim.y allows (65535 x 256 rows):
+    the launch is cut into several along the rows (both kernel families)."""
+    dims, rank = (16_800_002, 2), 4
+    y = rng_for(77).random(int(np.prod(dims)))
+    fs = [rng_for(78 + j).random((n, rank)) for j, n in enumerate(dims)]
+    m = ck.KruskalTensor(np.ones(rank), fs, validate=False)
+    t = ck.DenseTensor(dims, y)
+    ref = oracle.mttkrp_ref(y, dims, 0, fs, None)
+    for engine in ("auto", "cpasync"):
+        got = ck.run(t, m, MttkrpPlan(Variant.B200, 0, engine=engine, rank_tile=0 if engine == "auto" else 32)).matrix
+        assert oracle.rel_err(got, ref) <= TOL, engine
