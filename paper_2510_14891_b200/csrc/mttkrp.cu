@@ -513,6 +513,52 @@ static KrMerge choose_kr_merge(const Problem& pr, const cpk_plan* plan_in) {
   return m;
 }
 
+// Orders beyond the kernels' three o-modes (d >= 6, or d >= 7 after the
+// Khatri-Rao merge of f): merge the fastest adjacent pair of o-modes
+// (neither k nor f, not the slowest mode, so the streamed/landed contract
+// holds) into one virtual o-mode with a materialized Khatri-Rao factor
+// W[i_a + I_a i_b] = A_a[i_a] o A_b[i_b]; each level of mttkrp_impl removes
+// one mode until three o-modes remain.  Any plan (a necessity, not a tuning
+// choice); the plan is unchanged by it (I_k, R, f and the chunk count are).
+static KrMerge choose_order_merge(const Problem& pr) {
+  KrMerge m;
+  if (pr.n_o <= 3) return m;
+  for (int a = 0; a + 1 < pr.d - 1; ++a) {
+    const int b = a + 1;
+    if (a == pr.k || b == pr.k || a == pr.f || b == pr.f) continue;
+    m.ldw = (pr.R + 1) & ~int64_t(1);
+    m.w_bytes = size_t(pr.dims[a]) * size_t(pr.dims[b]) * size_t(m.ldw) * sizeof(double);
+    m.on = true;
+    m.f = a;
+    m.d2 = pr.d - 1;
+    for (int i = 0, j = 0; i < pr.d; ++i) {
+      if (i == b) continue;
+      m.dims2[j++] = i == a ? pr.dims[a] * pr.dims[b] : pr.dims[i];
+    }
+    m.mode2 = pr.k < a ? pr.k : pr.k - 1;
+    return m;
+  }
+  return m;
+}
+
+// Workspace of a problem including any order merges: [inner][W] per level.
+static int order_ws(const Problem& pr, const cpk_plan& q, size_t* bytes) {
+  if (pr.n_o <= 3) {
+    *bytes = ws_bytes_for(pr, q);
+    return CPK_OK;
+  }
+  const KrMerge km = choose_order_merge(pr);
+  if (!km.on) return fail(CPK_ERR_PARAM, "order d=%d: no pair of o-modes to merge", pr.d);
+  Problem p2;
+  int rc = make_problem(km.d2, km.dims2, km.mode2, pr.R, &p2);
+  if (rc) return rc;
+  size_t inner = 0;
+  rc = order_ws(p2, q, &inner);
+  if (rc) return rc;
+  *bytes = align256(inner) + km.w_bytes;
+  return CPK_OK;
+}
+
 __global__ static void kr_pair_f64(const double* __restrict__ Af, int64_t ldf, const double* __restrict__ Ag,
                                    int64_t ldg, int64_t If, int64_t rows, int64_t R, double* __restrict__ W,
                                    int64_t ldw) {
@@ -569,7 +615,10 @@ extern "C" int cpk_mttkrp_workspace_bytes(int d, const int64_t* dims, int mode, 
     cpk_plan q = *plan;
     rc = resolve(p2, &q);
     if (rc) return rc;
-    *bytes = align256(ws_bytes_for(p2, q)) + merged_out_bytes(pr, mg);
+    size_t inner = 0;
+    rc = order_ws(p2, q, &inner);
+    if (rc) return rc;
+    *bytes = align256(inner) + merged_out_bytes(pr, mg);
     return CPK_OK;
   }
   const KrMerge km = choose_kr_merge(pr, plan);
@@ -580,14 +629,16 @@ extern "C" int cpk_mttkrp_workspace_bytes(int d, const int64_t* dims, int mode, 
     cpk_plan q = *plan;
     rc = resolve(p2, &q);
     if (rc) return rc;
-    *bytes = align256(ws_bytes_for(p2, q)) + km.w_bytes;
+    size_t inner = 0;
+    rc = order_ws(p2, q, &inner);
+    if (rc) return rc;
+    *bytes = align256(inner) + km.w_bytes;
     return CPK_OK;
   }
   cpk_plan p = *plan;
   rc = resolve(pr, &p);
   if (rc) return rc;
-  *bytes = ws_bytes_for(pr, p);
-  return CPK_OK;
+  return order_ws(pr, p, bytes);
 }
 
 // d == 1: G[n, j] = lam[j] * y[n] (ref_kernel with no factor products).
@@ -657,7 +708,10 @@ static int mttkrp_impl(const double* y, int d, const int64_t* dims, int mode, co
     cpk_plan q = plan_in ? *plan_in : cpk_plan{0, 0, 0, 0, 0, 0, 0, 0};
     rc = resolve(p2, &q);
     if (rc) return rc;
-    const size_t inner = align256(ws_bytes_for(p2, q));
+    size_t inner_raw = 0;
+    rc = order_ws(p2, q, &inner_raw);
+    if (rc) return rc;
+    const size_t inner = align256(inner_raw);
     if (!workspace || ws_bytes < inner + merged_out_bytes(pr, mg))
       return fail(CPK_ERR_RESOURCE, "merged-mode workspace needs %zu bytes, got %zu", inner + merged_out_bytes(pr, mg),
                   ws_bytes);
@@ -693,7 +747,10 @@ static int mttkrp_impl(const double* y, int d, const int64_t* dims, int mode, co
       cpk_plan q = plan_in ? *plan_in : cpk_plan{0, 0, 0, 0, 0, 0, 0, 0};
       rc = resolve(p2, &q);
       if (rc) return rc;
-      const size_t inner = align256(ws_bytes_for(p2, q));
+      size_t inner_raw = 0;
+      rc = order_ws(p2, q, &inner_raw);
+      if (rc) return rc;
+      const size_t inner = align256(inner_raw);
       if (!workspace || ws_bytes < inner + km.w_bytes)
         return fail(CPK_ERR_RESOURCE, "Khatri-Rao merge workspace needs %zu bytes, got %zu", inner + km.w_bytes,
                     ws_bytes);
@@ -717,8 +774,41 @@ static int mttkrp_impl(const double* y, int d, const int64_t* dims, int mode, co
                          landed_lo, landed_hi, false);
     }
   }
-  if (pr.n_o > 3)
-    return fail(CPK_ERR_PARAM, "order d=%d > 5 is not supported by the sm_100a kernel", d);
+  if (pr.n_o > 3) {  // more o-modes than the kernels take: merge a pair of them (choose_order_merge)
+    const KrMerge km = choose_order_merge(pr);
+    if (!km.on) return fail(CPK_ERR_PARAM, "order d=%d: no pair of o-modes to merge", d);
+    Problem p2;
+    rc = make_problem(km.d2, km.dims2, km.mode2, rank, &p2);
+    if (rc) return rc;
+    cpk_plan q = plan_in ? *plan_in : cpk_plan{0, 0, 0, 0, 0, 0, 0, 0};
+    q.merge = CPK_MERGE_NONE;
+    rc = resolve(p2, &q);
+    if (rc) return rc;
+    size_t inner_raw = 0;
+    rc = order_ws(p2, q, &inner_raw);
+    if (rc) return rc;
+    const size_t inner = align256(inner_raw);
+    if (!workspace || ws_bytes < inner + km.w_bytes)
+      return fail(CPK_ERR_RESOURCE, "order-merge workspace needs %zu bytes, got %zu", inner + km.w_bytes, ws_bytes);
+    double* W = reinterpret_cast<double*>(static_cast<char*>(workspace) + inner);
+    const int a = km.f, b = a + 1;
+    const int64_t wrows = dims[a] * dims[b];
+    const unsigned blocks = unsigned(std::max<int64_t>(1, std::min<int64_t>(ceil_div(wrows * rank, 256), 148 * 8)));
+    kr_pair_f64<<<blocks, 256, 0, st>>>(factors[a], ld ? ld[a] : rank, factors[b], ld ? ld[b] : rank, dims[a], wrows,
+                                        rank, W, km.ldw);
+    rc = check_launch("kr_pair (order merge)");
+    if (rc) return rc;
+    const double* f2[CPK_MAX_MODES];
+    int64_t ld2[CPK_MAX_MODES];
+    for (int i = 0, j = 0; i < d; ++i) {
+      if (i == b) continue;
+      f2[j] = i == a ? W : factors[i];
+      ld2[j] = i == a ? km.ldw : (ld ? ld[i] : rank);
+      ++j;
+    }
+    return mttkrp_impl(y, km.d2, km.dims2, km.mode2, f2, ld2, lam, rank, G, ldg, &q, workspace, inner, stream,
+                       landed_lo, landed_hi, false);
+  }
 
   cpk_plan plan = plan_in ? *plan_in : cpk_plan{0, 0, 0, 0, 0, 0, 0, 0};
   rc = resolve(pr, &plan);

@@ -242,3 +242,13 @@ def test_random_shapes_cp_als_fuzz():
         assert dev <= 1e-8, (dims, rank, dev)
         w = model.weights.cpu().numpy() if hasattr(model.weights, "cpu") else np.asarray(model.weights)
         assert oracle.rel_err(w, ref_lam) <= 1e-6, (dims, rank)
+
+
+@pytest.mark.parametrize("dims,rank", [((5, 4, 3, 6, 2, 3), 4), ((3, 4, 2, 3, 2, 3, 2), 6)])
+def test_cp_als_beyond_five_modes(dims, rank):
+    """CP-ALS on 6- and 7-way tensors: every mode's MTTKRP runs through the
+    o-mode merges (choose_order_merge); fits at the oracle's."""
+    y = rng_for(sum(dims)).random(int(np.prod(dims)))
+    _, tr = ck.cp_als(ck.DenseTensor(dims, y), ck.AlsConfig(rank=rank, tol=0.0, max_iters=3, seed=1))
+    _, _, ref = oracle.cp_als(y, dims, rank, max_iters=3, tol=0.0, seed=1)
+    assert np.max(np.abs(np.asarray(tr.fits) - np.asarray(ref))) <= 1e-8

@@ -664,3 +664,23 @@ def test_tall_mode_beyond_the_grid_y_limit():
     for engine in ("auto", "cpasync"):
         got = ck.run(t, m, MttkrpPlan(Variant.B200, 0, engine=engine, rank_tile=0 if engine == "auto" else 32)).matrix
         assert oracle.rel_err(got, ref) <= TOL, engine
+
+
+@pytest.mark.parametrize("dims", [(4, 3, 5, 2, 3, 4), (6, 2, 4, 2, 3, 2, 3), (2, 3, 2, 2, 3, 2, 2, 3),
+                                  (5, 4, 3, 6, 2, 3)])
+def test_orders_six_to_eight_merge_o_modes(dims):
+    """Orders the kernels cannot take directly (more than three o-modes):
+    pairs of adjacent o-modes are merged into materialized Khatri-Rao
+    factors until three remain (choose_order_merge), for every mode, with
+    explicit reference-style plans too."""
+    for rank in (5, 33):
+        y = rng_for(sum(dims) + rank).random(int(np.prod(dims)))
+        fs = [rng_for(rank + 3 * j).random((n, rank)) for j, n in enumerate(dims)]
+        lam = rng_for(19).random(rank) + 0.5
+        m = ck.KruskalTensor(lam, fs)
+        t = ck.DenseTensor(dims, y)
+        for k in range(len(dims)):
+            ref = oracle.mttkrp_ref(y, dims, k, fs, lam)
+            for plan in (MttkrpPlan(Variant.B200, k), MttkrpPlan(Variant.TILE, k, tile_volume=64)):
+                got = ck.run(t, m, plan).matrix
+                assert oracle.rel_err(got, ref) <= TOL, (dims, rank, k, plan.variant)
