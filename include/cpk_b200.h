@@ -48,7 +48,7 @@ enum {
   CPK_ERR_FORMAT = 8     /* FormatError     (dtensor.py:359-382)         */
 };
 
-#define CPK_MAX_MODES 8
+#define CPK_MAX_MODES 16
 
 /* Kernel knobs.  Mirrors MttkrpPlan (mttkrp.py:53-89): `unroll` (F) and
  * `tile_volume` (N_T) keep their meaning; `rank_tile` is the GPU rank tile

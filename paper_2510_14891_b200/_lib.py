@@ -36,7 +36,7 @@ _CODE_TO_EXC = {
     8: FormatError,
 }
 CPK_ERR_NOT_PD = 6
-CPK_MAX_MODES = 8
+CPK_MAX_MODES = 16
 CPK_DTEN_MAX_MODES = 64
 CPK_SUMSQ_PARTIALS = 1024
 

@@ -667,8 +667,8 @@ def test_tall_mode_beyond_the_grid_y_limit():
 
 
 @pytest.mark.parametrize("dims", [(4, 3, 5, 2, 3, 4), (6, 2, 4, 2, 3, 2, 3), (2, 3, 2, 2, 3, 2, 2, 3),
-                                  (5, 4, 3, 6, 2, 3)])
-def test_orders_six_to_eight_merge_o_modes(dims):
+                                  (5, 4, 3, 6, 2, 3), (2, 2, 3, 2, 2, 2, 3, 2, 2, 2, 2, 2)])
+def test_orders_six_to_twelve_merge_o_modes(dims):
     """Orders the kernels cannot take directly (more than three o-modes):
     pairs of adjacent o-modes are merged into materialized Khatri-Rao
     factors until three remain (choose_order_merge), for every mode, with
