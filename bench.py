@@ -37,6 +37,7 @@ sys.path.insert(0, str(ROOT))
 METRIC = "dense MTTKRP GFLOP/s & roofline fraction vs rank R; CP-ALS sec/iter at 1/2/4/8 GPU"
 DIMS = (1024, 1024, 1024)
 RANK = 2000
+SM = 2  # shard mode of the c4 leg at N > 1 (see run_b200)
 SEED = 0
 PEAKS_FILE = ROOT / "MEASURED_PEAKS.json"
 NCU_SUMMARY = ROOT / "profiles" / "ncu_summary.json"
@@ -322,9 +323,12 @@ def run_b200(args):
     from paper_2510_14891_b200 import harness
     from paper_2510_14891_b200.mttkrp import MttkrpPlan, Variant, mttkrp_device, resolve_plan
 
-    # ---- inputs resident in HBM: this rank's mode-0 slab of config 4
-    lo, hi = shard_rows(DIMS[0], world, rank)
-    local_dims = (hi - lo, DIMS[1], DIMS[2])
+    # ---- inputs resident in HBM: this rank's slab of config 4 along SM
+    # (every mode of the cube is "the longest"; the slowest one gives
+    # contiguous slabs and keeps the other modes' o-groups long: a mode-0
+    # slab of 128 rows at 8 GPUs would flush modes 1 and 2 every 8 chunks)
+    lo, hi = shard_rows(DIMS[SM], world, rank)
+    local_dims = tuple(hi - lo if m == SM else e for m, e in enumerate(DIMS))
     n_local = int(np.prod(local_dims))
     lib = _lib.load()
     # element (i0, i1, i2) of the global tensor is splitmix(i0 + 1024 i1 + 1024^2 i2)
@@ -333,12 +337,13 @@ def run_b200(args):
                                         torch.cuda.current_stream().cuda_stream), "fill")
     if world == 1:
         y = full
-    else:
-        y = full.view(DIMS[2] * DIMS[1], DIMS[0])[:, lo:hi].contiguous().view(-1)
+    else:  # the slowest mode's slab is one contiguous range
+        plane = DIMS[0] * DIMS[1]
+        y = full[lo * plane:hi * plane].clone()
         del full
     # the reference CLI's factor recipe (cli.py:137-141): Philox(seed + 1)
     fs_host = [np.asarray(a) for a in harness.bench_factors(DIMS, RANK, SEED).factors]
-    fs_host[0] = np.ascontiguousarray(fs_host[0][lo:hi])
+    fs_host[SM] = np.ascontiguousarray(fs_host[SM][lo:hi])
     fs = [torch.from_numpy(a).to(dev) for a in fs_host]
     torch.cuda.synchronize()
 
@@ -350,7 +355,7 @@ def run_b200(args):
             g, _, _ = mttkrp_device(y, local_dims, fs, k, None, MttkrpPlan(Variant.B200, k))
             if events is not None:
                 events[k][1].record()
-            if world > 1 and k != 0:
+            if world > 1 and k != SM:
                 dist.all_reduce(g)
             outs.append(g)
         return outs
@@ -512,9 +517,9 @@ def run_b200(args):
         y_host.copy_(y)
         fs_pinned = [torch.from_numpy(a).pin_memory() for a in fs_host]
         h2d = 8 * n_local + sum(8 * a.size for a in fs_host)
-        d2h = 8 * RANK * sum(local_dims) if world == 1 else 8 * RANK * (local_dims[0] + DIMS[1] + DIMS[2])
+        d2h = 8 * RANK * sum(local_dims)
 
-        g_pinned = [torch.empty((DIMS[k] if k else local_dims[0], RANK), dtype=torch.float64, pin_memory=True)
+        g_pinned = [torch.empty((local_dims[k], RANK), dtype=torch.float64, pin_memory=True)
                     for k in range(3)]
 
         def e2e_step():
@@ -525,7 +530,7 @@ def run_b200(args):
             yt = ck.DenseTensor(local_dims, y_host)
             fd = [a.to(dev, non_blocking=True) for a in fs_pinned]
             for k, g in enumerate(ck.mttkrp_modes(yt, fd, (0, 1, 2))):
-                if world > 1 and k != 0:
+                if world > 1 and k != SM:
                     dist.all_reduce(g)
                 g_pinned[k].copy_(g, non_blocking=True)
             torch.cuda.synchronize()
@@ -622,7 +627,7 @@ def run_b200(args):
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (splitmix64 counter-based U[0,1) tensor generated on device, Philox(1) factors)",
             "config": {"workload": "c4: 3-way 1024x1024x1024 f64 tensor, rank 2000, MTTKRP of all 3 modes per step",
-                       "dims": list(DIMS), "rank": RANK, "parallelism": f"mode-0 block partition x{world}",
+                       "dims": list(DIMS), "rank": RANK, "parallelism": f"mode-{SM} block partition x{world}",
                        "l2": "inputs 8 GiB >> 126 MB L2; no flush needed"},
             "per_mode_ms": per_mode,
             "paper_gflops": int(np.prod(DIMS)) * RANK * 3 * 3 * args.steps / elapsed / 1024 ** 3,

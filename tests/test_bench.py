@@ -53,7 +53,7 @@ def test_b200_arm_line():
 
 @pytest.mark.gpu
 def test_b200_arm_multi_rank_path():
-    """The N > 1 path of bench.py (torchrun, mode-0 slabs, allreduce of the
+    """The N > 1 path of bench.py (torchrun, mode-2 slabs, allreduce of the
     other modes, max-over-ranks timing, e2e per rank) with 2 ranks on the one
     GPU over gloo: one JSON line from rank 0, n_gpus = 2, the global
     workload's flops."""
@@ -70,7 +70,7 @@ def test_b200_arm_multi_rank_path():
     assert len(lines) == 1, out.stdout[-2000:]
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["value"] > 0 and d["e2e"]["value"] > 0
-    assert d["config"]["parallelism"] == "mode-0 block partition x2"
+    assert d["config"]["parallelism"] == "mode-2 block partition x2"
     # the sharded CP-ALS leg ran through the strict (device-only) communicator
     c5 = d["cp_als_c5"]
     assert "error" not in c5, c5
