@@ -82,6 +82,13 @@ typedef struct cpk_plan {
  * plans when those modes are short and the factor small; resolve reports
  * KR, and passing it back runs the same merged problem. */
 #define CPK_MERGE_KR 3
+/* KR_FOLD: for d >= 4 when k sits between the fastest non-k mode f and the
+ * first other mode o0 (so KR cannot reshape them), the DMMA kernel reads
+ * W = KR(A_f, A_o0) (rows i_f + I_f i_o0, materialized in the workspace) as
+ * its factor rows and an all-ones factor for o0: o-groups run I_o0 times
+ * longer.  AUTO picks it for automatic plans under the same conditions as
+ * KR; resolve reports it and passing it back runs the same thing. */
+#define CPK_MERGE_KR_FOLD 4
 
 /* engine: AUTO picks the warp-specialized TMA kernel with DMMA consumers
  * when the problem is aligned (even I_0 and leading dimensions, 16-byte

@@ -559,6 +559,46 @@ static int order_ws(const Problem& pr, const cpk_plan& q, size_t* bytes) {
   return CPK_OK;
 }
 
+// Khatri-Rao fold (CPK_MERGE_KR_FOLD): when the fastest non-k mode f is
+// short and k sits between it and the first o-mode o0 (c3's mode 1), the
+// reshape of choose_kr_merge is impossible, but the DMMA kernel can read
+// W = KR(A_f, A_o0) (rows i_f + I_f i_o0) as its factor rows and an all-ones
+// factor for o0: the chunk walk and the tensor tiles are unchanged, P_o no
+// longer changes with i_o0, so an o-group is I_o0 times longer
+// (WsParams::fold).  Needs the resolved plan: DMMA engine, I_f a multiple of
+// the chunk depth.  W is a two-mode partial Khatri-Rao product (d >= 4: the
+// other o-modes stay on the fly), capped like the KR merge.
+struct KrFold {
+  bool on = false;
+  int o0 = -1;
+  int64_t ldw = 0;
+  size_t w_bytes = 0, ones_bytes = 0;
+};
+
+static KrFold choose_kr_fold(const Problem& pr, const cpk_plan& resolved, const cpk_plan* plan_in) {
+  KrFold m;
+  const bool forced = plan_in && plan_in->merge == CPK_MERGE_KR_FOLD;
+  if (!forced && (!plan_is_auto(plan_in) || (plan_in && plan_in->merge != CPK_MERGE_AUTO))) return m;
+  if (pr.d < 4 || pr.f < 0 || pr.n_o < 2 || pr.n_o > 3 || resolved.engine != CPK_ENGINE_DMMA) return m;
+  if (resolved.block_k <= 0 || pr.dims[pr.f] % resolved.block_k != 0) return m;
+  if (!forced && pr.dims[pr.f] / resolved.block_k >= kKrMergeMinGroup) return m;  // o-groups already long
+  const int o0 = pr.o_modes[0];
+  m.ldw = (pr.R + 1) & ~int64_t(1);
+  m.w_bytes = size_t(pr.dims[pr.f]) * size_t(pr.dims[o0]) * size_t(m.ldw) * sizeof(double);
+  m.ones_bytes = size_t(pr.dims[o0]) * size_t(m.ldw) * sizeof(double);
+  if (!forced && m.w_bytes > kKrMergeBytes) return m;
+  m.on = true;
+  m.o0 = o0;
+  return m;
+}
+
+static size_t fold_bytes(const KrFold& kf) { return kf.on ? align256(kf.w_bytes) + align256(kf.ones_bytes) : 0; }
+
+__global__ static void fill_f64(double* x, int64_t n, double v) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+    x[i] = v;
+}
+
 __global__ static void kr_pair_f64(const double* __restrict__ Af, int64_t ldf, const double* __restrict__ Ag,
                                    int64_t ldg, int64_t If, int64_t rows, int64_t R, double* __restrict__ W,
                                    int64_t ldw) {
@@ -583,11 +623,13 @@ extern "C" int cpk_plan_resolve(int d, const int64_t* dims, int mode, int64_t ra
     plan->merge = mg.a < mode ? CPK_MERGE_PREV : CPK_MERGE_NEXT;
     return resolve(p2, plan);
   }
-  if (plan->merge != CPK_MERGE_AUTO && plan->merge != CPK_MERGE_NONE && plan->merge != CPK_MERGE_KR)
+  if (plan->merge != CPK_MERGE_AUTO && plan->merge != CPK_MERGE_NONE && plan->merge != CPK_MERGE_KR &&
+      plan->merge != CPK_MERGE_KR_FOLD)
     return fail(CPK_ERR_PARAM, "merge %d impossible for mode %d of a %d-way tensor", plan->merge, mode, d);
   const KrMerge km = choose_kr_merge(pr, plan);
   if (plan->merge == CPK_MERGE_KR && !km.on)
     return fail(CPK_ERR_PARAM, "Khatri-Rao merge impossible for mode %d of a %d-way tensor", mode, d);
+  const cpk_plan request = *plan;
   plan->merge = km.on ? CPK_MERGE_KR : CPK_MERGE_NONE;
   if (km.on) {  // the plan of the (d-1)-way problem with f and f + 1 merged
     Problem p2;
@@ -595,7 +637,13 @@ extern "C" int cpk_plan_resolve(int d, const int64_t* dims, int mode, int64_t ra
     if (rc) return rc;
     return resolve(p2, plan);
   }
-  return resolve(pr, plan);
+  rc = resolve(pr, plan);
+  if (rc) return rc;
+  const KrFold kf = choose_kr_fold(pr, *plan, &request);
+  if (request.merge == CPK_MERGE_KR_FOLD && !kf.on)
+    return fail(CPK_ERR_PARAM, "Khatri-Rao fold impossible for mode %d of a %d-way tensor", mode, d);
+  if (kf.on) plan->merge = CPK_MERGE_KR_FOLD;
+  return CPK_OK;
 }
 
 extern "C" int cpk_mttkrp_workspace_bytes(int d, const int64_t* dims, int mode, int64_t rank,
@@ -638,7 +686,11 @@ extern "C" int cpk_mttkrp_workspace_bytes(int d, const int64_t* dims, int mode, 
   cpk_plan p = *plan;
   rc = resolve(pr, &p);
   if (rc) return rc;
-  return order_ws(pr, p, bytes);
+  rc = order_ws(pr, p, bytes);
+  if (rc) return rc;
+  const KrFold kf = choose_kr_fold(pr, p, plan);
+  if (kf.on) *bytes = align256(*bytes) + fold_bytes(kf);
+  return CPK_OK;
 }
 
 // d == 1: G[n, j] = lam[j] * y[n] (ref_kernel with no factor products).
@@ -813,7 +865,11 @@ static int mttkrp_impl(const double* y, int d, const int64_t* dims, int mode, co
   cpk_plan plan = plan_in ? *plan_in : cpk_plan{0, 0, 0, 0, 0, 0, 0, 0};
   rc = resolve(pr, &plan);
   if (rc) return rc;
-  const size_t need = ws_bytes_for(pr, plan);
+  const KrFold kf = choose_kr_fold(pr, plan, plan_in);
+  if (plan_in && plan_in->merge == CPK_MERGE_KR_FOLD && !kf.on)
+    return fail(CPK_ERR_PARAM, "Khatri-Rao fold impossible for mode %d of a %d-way tensor", mode, d);
+  const size_t split_need = ws_bytes_for(pr, plan);
+  const size_t need = kf.on ? align256(split_need) + fold_bytes(kf) : split_need;
   if (need > 0 && (!workspace || ws_bytes < need))
     return fail(CPK_ERR_RESOURCE, "split-K workspace needs %zu bytes, got %zu", need, ws_bytes);
 
@@ -866,6 +922,30 @@ static int mttkrp_impl(const double* y, int d, const int64_t* dims, int mode, co
     wr.out_split_stride = out_split_stride;
     wr.lam = lam_fold;
     wr.sem = sem;
+    if (ws_eligible(wr) && kf.on) {
+      // the fold's factors: W = KR(A_f, A_o0) and all-ones rows for o0, once
+      // per MTTKRP (the first landed piece) in the workspace after the split state
+      char* base = static_cast<char*>(workspace) + align256(split_need);
+      double* W = reinterpret_cast<double*>(base);
+      double* ones = reinterpret_cast<double*>(base + align256(kf.w_bytes));
+      const int f = pr.f, o0 = kf.o0;
+      if (!ranged || landed_lo == 0) {
+        const int64_t wrows = pr.dims[f] * pr.dims[o0];
+        const unsigned blocks =
+            unsigned(std::max<int64_t>(1, std::min<int64_t>(ceil_div(wrows * rank, 256), 148 * 8)));
+        kr_pair_f64<<<blocks, 256, 0, st>>>(factors[f], ldof(f), factors[o0], ldof(o0), pr.dims[f], wrows, rank, W,
+                                            kf.ldw);
+        fill_f64<<<unsigned(std::max<int64_t>(1, std::min<int64_t>(ceil_div(pr.dims[o0] * kf.ldw, 256), 1024))),
+                   256, 0, st>>>(ones, pr.dims[o0] * kf.ldw, 1.0);
+        rc = check_launch("kr fold factors");
+        if (rc) return rc;
+      }
+      wr.factors[f] = W;
+      wr.ld[f] = kf.ldw;
+      wr.factors[o0] = ones;
+      wr.ld[o0] = kf.ldw;
+      wr.fold = 1;
+    }
     if (ws_eligible(wr)) {
       Landed ld_{plan.block_rows, plan.block_k, 0, 0};
       ld_.n_chunks = n_chunks_of(pr, plan.block_k);

@@ -26,6 +26,7 @@ struct WsRequest {
   int64_t ldo, out_split_stride;
   const double* lam;
   int* sem;  // split-K chain counters (common.cuh), or nullptr
+  int fold;  // Khatri-Rao fold: factors[f] is W = KR(A_f, A_o0), rows i_f + I_f i_o0 (WsParams::fold)
 };
 
 // TMA tile for a rank tile (DMMA 16 | 32 | 64 | 128 | 256, DFMA 64 | 128 | 256) and math: rows per CTA and chunk depth.

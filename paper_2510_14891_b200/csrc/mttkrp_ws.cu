@@ -62,8 +62,15 @@ struct alignas(64) WsParams {
   const double* lam;
   int32_t y0, z0;  // first row block / split of this launch
   int32_t a_one_box;  // mode 0, DMMA: tm_y views the tensor as (16, I_1, I_0 / 16, ...) -> one box per stage
+  int32_t b_one_box;  // DMMA, R % 16 == 0: tm_f views the factor as (16, rows, R / 16) -> one box per stage
   int* sem;           // split-K chain counters (one per output tile), or nullptr: partials / direct
   int32_t n_splits;
+  // Khatri-Rao fold (DMMA only): the factor map holds W = KR(A_f, A_o0)
+  // (rows i_f + I_f i_o0) and the first o-mode's factor is all ones, so
+  // P_o stops changing with i_o0: an o-group runs og_len = chunks_per_f x
+  // dim_o[0] chunks instead of chunks_per_f
+  int32_t fold;
+  int64_t og_len;  // chunks per o-group (the consumers' flush period)
 };
 
 // Epilogue prologue of the split-K chain (consumer threads only: the
@@ -294,10 +301,10 @@ __device__ __forceinline__ int dmma_kchunk(int lk, int s) { return 2 * lk + ((lk
 template <bool KMAJ, int NA, bool OG, int NO, int BM, int BN, int NF, int BK, int STAGE_BYTES, int A_BYTES>
 __device__ __forceinline__ void ws_dmma_loop(double (&acc)[4][NF][2], const uint8_t* smem, uint64_t* full,
                                              uint64_t* empty, int nst, int stages, int wm0, int wn0, int lane,
-                                             uint32_t tbase, int64_t q0, int64_t chunks_per_f) {
+                                             uint32_t tbase, int64_t q0, int64_t og_len) {
   const int lr = lane >> 2, lk = lane & 3;
   bool first = true;
-  int64_t qf = OG ? q0 % chunks_per_f : 0;  // position inside the o-group
+  int64_t qf = OG ? q0 % og_len : 0;  // position inside the o-group (og_len chunks long)
   for (int it = 0; it < nst; ++it) {
     const int s = it % stages;
     mbar_wait(&full[s], (it / stages) & 1);
@@ -350,7 +357,7 @@ __device__ __forceinline__ void ws_dmma_loop(double (&acc)[4][NF][2], const uint
           for (int nf = 0; nf < NA; ++nf) dmma_8x8x4(acc[mf][nf], a[mf][ph], b[nf][ph]);
     }
     if constexpr (OG && NA > 0) {
-      if (++qf == chunks_per_f || it == nst - 1) {  // o-group ends: fold it into the total
+      if (++qf == og_len || it == nst - 1) {  // o-group ends: fold it into the total
         og_flush<NO, BN, NF>(acc, tbase, reinterpret_cast<const double*>(st + A_BYTES + BK * BN * 8), wn0, lk,
                              first);
         first = false;
@@ -389,9 +396,10 @@ __device__ __forceinline__ void ws_consume_dmma(const uint8_t* smem, uint64_t* f
   const int live = p.R - j0 - wn0;
   // this warp's TMEM window: lanes 32 (warp % 4).., columns 128 (warp / 4)..
   const uint32_t tbase = tmem + (uint32_t((warp & 3) * 32) << 16) + uint32_t((warp >> 2) * 128);
+  const int64_t og_len = p.og_len;
 #define CPK_DMMA_LOOP(NA_)                                                                                     \
   ws_dmma_loop<KMAJ, NA_, OG, NO, BM, BN, NF, BK, STAGE_BYTES, A_BYTES>(acc, smem, full, empty, nst, stages, wm0, \
-                                                                        wn0, lane, tbase, q0, p.chunks_per_f)
+                                                                        wn0, lane, tbase, q0, og_len)
   // every branch runs exactly one loop (a warp that skipped it would never
   // release its stages); plain compares, the last case catches the rest
   if (live <= 0) {
@@ -611,10 +619,15 @@ __global__ void __launch_bounds__(WS_THREADS, 1) mttkrp_f64_ws_sm100(const __gri
         } else {
           tma_load<C::D>(a_s, &p.tm_y, &full_tma[s], c);
         }
-        if (TM == 0) {
+        // factor rows of the chunk: A_f rows, or (fold) W rows i_f + I_f i_o0
+        const int ifb = p.fold ? (qf + int(p.chunks_per_f) * od[0]) * BK : if0;
+        if (TM == 0 && p.b_one_box) {  // all BN / 16 column panels as one box {16, BK, BN / 16}
+          const int cf[3] = {0, ifb, j0 >> 4};
+          tma_load<3>(b_s, &p.tm_f, &full_tma[s], cf);
+        } else if (TM == 0) {
 #pragma unroll
           for (int pc = 0; pc < BN / 16; ++pc) {  // 16-column swizzled panels [k][16]
-            const int cf[2] = {j0 + 16 * pc, if0};
+            const int cf[2] = {j0 + 16 * pc, ifb};
             tma_load<2>(b_s + pc * (16 * BK), &p.tm_f, &full_tma[s], cf);
           }
         } else {
@@ -976,11 +989,34 @@ int launch_ws(const WsRequest& r, cudaStream_t st) {
     rc = encode(&p.tm_y, r.y, d, gdim, gstr, box, CU_TENSOR_MAP_SWIZZLE_128B);
   }
   if (rc) return rc;
+  int o0 = -1;  // the first o-mode (the fold's second KR factor)
+  for (int m = 0; m < d; ++m)
+    if (m != k && m != f) {
+      o0 = m;
+      break;
+    }
+  if (r.fold && (r.math != WS_MATH_DMMA || o0 < 0 || r.dims[f] % BK != 0))
+    return fail(CPK_ERR_PARAM, "Khatri-Rao fold needs the DMMA engine, an o-mode and I_f %% %d == 0", BK);
+  p.fold = r.fold ? 1 : 0;
+  p.og_len = 0;  // set below from chunks_per_f
   {
-    const cuuint64_t fd[2] = {cuuint64_t(r.rank), cuuint64_t(r.dims[f])};
-    const cuuint64_t fs[1] = {cuuint64_t(r.ld[f] * 8)};
-    const cuuint32_t fb[2] = {cuuint32_t(dmma ? 16 : BN), cuuint32_t(BK)};
-    rc = encode(&p.tm_f, r.factors[f], 2, fd, fs, fb, dmma ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE);
+    // fold: factors[f] is W (I_f I_o0 rows) -- see WsParams::fold
+    const cuuint64_t frows = cuuint64_t(r.fold ? r.dims[f] * r.dims[o0] : r.dims[f]);
+    static const bool b_boxes_off = getenv("CPK_WS_PANEL_BOXES") != nullptr;  // A/B: per-panel boxes
+    if (dmma && r.rank % 16 == 0 && !b_boxes_off) {
+      // (column mod 16, row, column / 16): every panel column < R, so the
+      // view never reads past a row; panels past R zero-fill
+      const cuuint64_t fd[3] = {16, frows, cuuint64_t(r.rank / 16)};
+      const cuuint64_t fs[2] = {cuuint64_t(r.ld[f] * 8), 16 * 8};
+      const cuuint32_t fb[3] = {16, cuuint32_t(BK), cuuint32_t(BN / 16)};
+      rc = encode(&p.tm_f, r.factors[f], 3, fd, fs, fb, CU_TENSOR_MAP_SWIZZLE_128B);
+      p.b_one_box = 1;
+    } else {
+      const cuuint64_t fd[2] = {cuuint64_t(r.rank), frows};
+      const cuuint64_t fs[1] = {cuuint64_t(r.ld[f] * 8)};
+      const cuuint32_t fb[2] = {cuuint32_t(dmma ? 16 : BN), cuuint32_t(BK)};
+      rc = encode(&p.tm_f, r.factors[f], 2, fd, fs, fb, dmma ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE);
+    }
     if (rc) return rc;
   }
   int oi = 0;
@@ -998,6 +1034,7 @@ int launch_ws(const WsRequest& r, cudaStream_t st) {
   p.n_chunks = p.chunks_per_f;
   for (int i = 0; i < oi; ++i) p.n_chunks *= p.dim_o[i];
   p.chunks_per_split = (p.n_chunks + r.splits - 1) / r.splits;
+  p.og_len = p.fold ? p.chunks_per_f * p.dim_o[0] : p.chunks_per_f;
   p.Ik = int(r.dims[k]);
   p.If = int(r.dims[f]);
   p.R = int(r.rank);

@@ -156,10 +156,11 @@ def test_small_mode_merge_is_reported_and_round_trips():
 def test_khatri_rao_merge_is_reported_sized_and_round_trips():
     # config 3 (128^4, R = 256): modes 0, 2, 3 merge their two fastest non-k
     # modes into one Khatri-Rao mode (CPK_MERGE_KR = 3); mode 1 cannot (k sits
-    # between them); the workspace includes the 128 * 128 x 256 factor; the
-    # resolved plan is a fixed point; 3-way problems never merge this way
+    # between them) and folds KR(A_0, A_2) into its factor rows instead
+    # (CPK_MERGE_KR_FOLD = 4); the workspace includes the 128 * 128 x 256
+    # factor; the resolved plan is a fixed point; 3-way problems never merge
     dims = (128, 128, 128, 128)
-    for k, want in ((0, 3), (1, -1), (2, 3), (3, 3)):
+    for k, want in ((0, 3), (1, 4), (2, 3), (3, 3)):
         rc, p = plan(dims, k, 256)
         assert rc == 0 and p.merge == want, (k, p.merge)
     rc, p = plan(dims, 0, 256)
@@ -174,3 +175,12 @@ def test_khatri_rao_merge_is_reported_sized_and_round_trips():
     assert rc == 0 and p.merge == -1
     forced = _lib.CpkPlan(0, 0, 0, 0, 148, 0, 0, 3)  # KR for mode 1: impossible
     assert _lib.load().cpk_plan_resolve(4, _lib.i64_array(dims), 1, 256, forced) == 3
+    # the fold round-trips and sizes W (128 * 128 x 256) plus the ones rows
+    rc, p = plan(dims, 1, 256)
+    q = _lib.CpkPlan(p.rank_tile, p.block_rows, p.tile_volume, p.splits, p.sm_count, p.block_k, p.engine, p.merge)
+    assert _lib.load().cpk_plan_resolve(4, _lib.i64_array(dims), 1, 256, q) == 0 and q.merge == 4
+    assert _lib.load().cpk_mttkrp_workspace_bytes(4, _lib.i64_array(dims), 1, 256, req, _lib.C.byref(nbytes)) == 0
+    assert nbytes.value >= 128 * 128 * 256 * 8 + 128 * 256 * 8
+    # 3-way problems never fold (the fold would be the whole Khatri-Rao matrix)
+    rc, p = plan((64, 64, 64), 1, 64)
+    assert rc == 0 and p.merge != 4

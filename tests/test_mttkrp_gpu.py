@@ -684,3 +684,22 @@ def test_orders_six_to_twelve_merge_o_modes(dims):
             for plan in (MttkrpPlan(Variant.B200, k), MttkrpPlan(Variant.TILE, k, tile_volume=64)):
                 got = ck.run(t, m, plan).matrix
                 assert oracle.rel_err(got, ref) <= TOL, (dims, rank, k, plan.variant)
+
+
+@pytest.mark.parametrize("dims", [(32, 20, 24, 6), (16, 40, 12, 10, 4), (48, 30, 20, 8)])
+def test_khatri_rao_fold_for_a_middle_mode(dims):
+    """Mode 1 of a d >= 4 tensor (k between the fastest non-k mode and the
+    first o-mode): the automatic plan folds KR(A_0, A_2) into the factor
+    rows (CPK_MERGE_KR_FOLD) -- against the oracle, against the unfolded
+    plan, with weights, and round-tripped through the resolved plan."""
+    for rank in (6, 40, 130):
+        y = rng_for(sum(dims) * rank).random(int(np.prod(dims)))
+        fs = [rng_for(rank + 11 * j).random((n, rank)) for j, n in enumerate(dims)]
+        lam = rng_for(23).random(rank) + 0.5
+        m = ck.KruskalTensor(lam, fs)
+        t = ck.DenseTensor(dims, y)
+        ref = oracle.mttkrp_ref(y, dims, 1, fs, lam)
+        folded = ck.run(t, m, MttkrpPlan(Variant.B200, 1)).matrix
+        plain = ck.run(t, m, MttkrpPlan(Variant.B200, 1, engine="dmma", rank_tile=64)).matrix
+        assert oracle.rel_err(folded, ref) <= TOL, (dims, rank)
+        assert oracle.rel_err(plain, ref) <= TOL, (dims, rank)
