@@ -932,7 +932,16 @@ extern "C" int cpk_solve_factor_spec_f64(const double* gamma, int64_t rank, void
   double* L = reinterpret_cast<double*>(base);
   double* w = reinterpret_cast<double*>(base + off_w);
   if (use_small_chol(rank)) return chol_small(gamma, rank, 0.0, L, info_out, st);
-  if (solve_path(rank) == SolvePath::Sweep) return sweep_inverse(gamma, rank, 0.0, work, work_bytes, info_out, 0, st);
+  if (solve_path(rank) == SolvePath::Sweep) {
+    // On the side stream the sweep runs beside the mode's MTTKRP: a
+    // full-machine cooperative grid fights it for SMs, 16 CTAs stay hidden
+    // behind it (128^4, R = 300: 21.2 ms per sweep either way; small-tensor
+    // R = 512 runs 4.7 -> 4.4 ms; c5 hides either; profiles/r02_sweep_ctas*.log).
+    // CPK_SWEEP_CTAS overrides (0 = full machine).
+    const char* c = getenv("CPK_SWEEP_CTAS");
+    const int ctas = c ? atoi(c) : std::min(16, sweep_default_ctas(rank));
+    return sweep_inverse(gamma, rank, 0.0, work, work_bytes, info_out, ctas, st);
+  }
   const unsigned cblocks = unsigned(std::min<int64_t>((rank * rank + 255) / 256, 148 * 4));
   copy_regularize_kernel<<<std::max(cblocks, 1u), 256, 0, st>>>(gamma, rank, 0.0, L);
   rc = check_launch("copy_regularize");
