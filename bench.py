@@ -27,6 +27,7 @@ import subprocess
 import sys
 import threading
 import time
+from dataclasses import replace
 from pathlib import Path
 
 import numpy as np
@@ -596,6 +597,8 @@ def run_b200(args):
                 proj = bench_c5_projection(dev, args.c5_iters, c5_dims, args.c5_rank)
                 for pt in proj["points"]:
                     pt["projected_speedup"] = c5["sec_per_iter"] / pt["rank0_sec_per_iter"]
+                    pt["per_mode_projected_speedup"] = (c5["per_mode"]["sec_per_iter"]
+                                                        / pt["per_mode_rank0_sec_per_iter"])
                 c5["projection"] = proj
             except Exception as exc:  # noqa: BLE001
                 c5["projection"] = {"error": f"{type(exc).__name__}: {exc}"[:300]}
@@ -667,29 +670,33 @@ def run_b200(args):
 
 
 def bench_cpals(ck, dev, iters):
-    """CP-ALS seconds per sweep at config 3 (128^4, R=256)."""
+    """CP-ALS seconds per sweep at config 3 (128^4, R=256): the API default
+    (dimension tree, split 2: two tensor passes per sweep), its graph
+    replay, and the per-mode sweep (four passes, the reference's structure)."""
     import torch
+
+    from paper_2510_14891_b200.perfmodel import roofline_seconds
 
     dims = (128, 128, 128, 128)
     t = ck.DenseTensor.uniform(dims, seed=SEED, device=dev)
-    res = {"config": "c3: 4-way 128^4 f64, rank 256", "iters": iters}
-    for graph in (None, True):
-        ck.cp_als(t, ck.AlsConfig(rank=256, tol=0.0, max_iters=2, seed=0), graph=graph)  # warm-up
+    roof = 4 * roofline_seconds(dims, 256)  # the sweep's 4 MTTKRPs at the north-star roofline
+    res = {"config": "c3: 4-way 128^4 f64, rank 256", "iters": iters, "roofline_sec_per_iter": roof}
+    for tree, graph in ((None, None), (None, True), (False, None), (False, True)):
+        cfg = ck.AlsConfig(rank=256, tol=0.0, max_iters=iters, seed=0, dimtree=tree)
+        ck.cp_als(t, replace(cfg, max_iters=2), graph=graph)  # warm-up
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        _, tr = ck.cp_als(t, ck.AlsConfig(rank=256, tol=0.0, max_iters=iters, seed=0), graph=graph)
+        _, tr = ck.cp_als(t, cfg, graph=graph)
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
-        if graph is None:  # the API default (eager below GRAPH_MIN_ITERS sweeps)
-            from paper_2510_14891_b200.perfmodel import roofline_seconds
-
-            roof = 4 * roofline_seconds(dims, 256)  # the sweep's 4 MTTKRPs at the north-star roofline
-            res.update({"sec_per_iter": dt / iters, "roofline_sec_per_iter": roof,
-                        "roofline_frac": roof / (dt / iters),
+        dst = res if tree is None else res.setdefault("per_mode", {"what": "dimtree=False: 4 MTTKRPs per sweep"})
+        if graph is None:  # eager below GRAPH_MIN_ITERS sweeps
+            dst.update({"sec_per_iter": dt / iters, "roofline_frac": roof / (dt / iters),
                         "mttkrp_sec_per_iter": statistics.median(sum(s) for s in tr.mttkrp_seconds),
-                        "other_sec_per_iter": statistics.median(tr.other_seconds), "fit_last": tr.fits[-1]})
+                        "other_sec_per_iter": statistics.median(tr.other_seconds), "fit_last": tr.fits[-1],
+                        "tree_split": tr.tree_split})
         else:  # forced capture: sweeps 2.. are one CUDA-graph replay each
-            res.update({"graph_sec_per_iter": dt / iters,
+            dst.update({"graph_sec_per_iter": dt / iters,
                         "graph_sec_per_replayed_sweep": statistics.median(
                             sum(m) + o for m, o in zip(tr.mttkrp_seconds[1:], tr.other_seconds[1:]))})
     return res
@@ -709,16 +716,22 @@ def bench_c5(dev, iters, dims=(4096, 2048, 2048), r=512):
     part = sharded.partition_for(dims, comm.world)
     y = sharded.uniform_slab(part, comm.rank, seed=SEED, device=dev)
     sharded.cp_als_sharded(y, part, AlsConfig(rank=r, tol=0.0, max_iters=1, seed=0), comm, gather=False)  # warm-up
+    torch.cuda.empty_cache()
     comm.reset()
     _, tr = sharded.cp_als_sharded(y, part, AlsConfig(rank=r, tol=0.0, max_iters=iters, seed=0), comm,
                                    gather=False)
     sec = statistics.median(tr.sweep_seconds)
     mt = statistics.median(sum(s) for s in tr.mttkrp_seconds)
     comm_s = tr.comm_seconds / max(1, len(tr.fits))
+    # the per-mode sweep (dimtree=False: 3 tensor passes, the reference's structure)
+    torch.cuda.empty_cache()
+    _, tr_pm = sharded.cp_als_sharded(y, part, AlsConfig(rank=r, tol=0.0, max_iters=iters, seed=0, dimtree=False),
+                                      comm, gather=False)
+    sec_pm = statistics.median(tr_pm.sweep_seconds)
     if comm.world > 1:
-        t = torch.tensor([sec, mt, comm_s], dtype=torch.float64, device=dev)
+        t = torch.tensor([sec, mt, comm_s, sec_pm], dtype=torch.float64, device=dev)
         comm.dist.all_reduce(t, op=comm.dist.ReduceOp.MAX)
-        sec, mt, comm_s = (float(v) for v in t.tolist())
+        sec, mt, comm_s, sec_pm = (float(v) for v in t.tolist())
     del y
     flops = 3 * algo_flops(dims, r)
     from paper_2510_14891_b200.perfmodel import roofline_seconds
@@ -731,7 +744,11 @@ def bench_c5(dev, iters, dims=(4096, 2048, 2048), r=512):
             "mttkrp_gflops": flops / mt / 1e9, "mttkrp_gflops_per_gpu": flops / mt / 1e9 / comm.world,
             "comm_sec_per_iter": comm_s, "comm_bytes_per_iter": tr.comm_bytes // max(1, len(tr.fits)),
             "comm_calls_per_iter": tr.comm_calls / max(1, len(tr.fits)), "rollbacks": tr.rollbacks,
-            "timing": "CUDA events per sweep (sweep start -> stats readback), max over ranks", "fits": tr.fits}
+            "tree_split": tr.tree_split,
+            "timing": "CUDA events per sweep (sweep start -> stats readback), max over ranks", "fits": tr.fits,
+            "per_mode": {"what": "dimtree=False: 3 MTTKRPs per sweep", "sec_per_iter": sec_pm,
+                         "mttkrp_gflops": flops / statistics.median(sum(s) for s in tr_pm.mttkrp_seconds) / 1e9,
+                         "fits": tr_pm.fits}}
 
 
 def bench_c5_projection(dev, iters, dims=(4096, 2048, 2048), r=512, worlds=(2, 4, 8)):
@@ -764,11 +781,18 @@ def bench_c5_projection(dev, iters, dims=(4096, 2048, 2048), r=512, worlds=(2, 4
         part = sharded.partition_for(dims, world)
         y = sharded.uniform_slab(part, 0, seed=SEED, device=dev)
         sharded.cp_als_sharded(y, part, AlsConfig(rank=r, tol=0.0, max_iters=1, seed=0), comm, gather=False)
+        comm.bytes = 0
         _, tr = sharded.cp_als_sharded(y, part, AlsConfig(rank=r, tol=0.0, max_iters=iters, seed=0), comm,
                                        gather=False)
+        elided = comm.bytes // max(1, len(tr.fits))
+        torch.cuda.empty_cache()
+        _, tr_pm = sharded.cp_als_sharded(y, part, AlsConfig(rank=r, tol=0.0, max_iters=iters, seed=0,
+                                                             dimtree=False), comm, gather=False)
         out.append({"gpus": world, "rank0_sec_per_iter": statistics.median(tr.sweep_seconds),
                     "rank0_mttkrp_sec_per_iter": statistics.median(sum(m) for m in tr.mttkrp_seconds),
-                    "elided_bytes_per_iter": comm.bytes // max(1, len(tr.fits)), "rollbacks": tr.rollbacks})
+                    "elided_bytes_per_iter": elided, "rollbacks": tr.rollbacks,
+                    "tree_split": tr.tree_split,
+                    "per_mode_rank0_sec_per_iter": statistics.median(tr_pm.sweep_seconds)})
         del y
         torch.cuda.empty_cache()
     return {"what": "rank 0's sweep at P ranks on this one GPU, collectives elided (loopback)",

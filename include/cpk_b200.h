@@ -215,6 +215,21 @@ int cpk_solve_normal_spec_f64(const double* gamma, double* G, int64_t rows,
                               int64_t rank, void* work, size_t work_bytes,
                               int* info_out, void* stream);
 
+/* Dimension-tree CP-ALS, in-group step (no reference counterpart as one
+ * call: it is the second half of the reference sweep's mode-k MTTKRP,
+ * cpals.py:121-124, when the sweep splits the modes into two groups).
+ * W (prod(ext) x rank, row stride ldw, group multi-index first-mode-fastest)
+ * is the MTTKRP of the tensor over the modes OUTSIDE a group of g modes with
+ * extents ext[0..g-1]; out (ext[j] x rank, row stride ldo) =
+ *   sum over i_l, l != j, of W[i, r] * prod_{l != j} factors[l][i_l, r],
+ * i.e. group mode j's MTTKRP.  factors[j] is not read (may be NULL);
+ * factors[l] has row stride lda[l].  Deterministic (fixed summation order). */
+int cpk_dimtree_contract_f64(const double* W, int64_t ldw, int g,
+                             const int64_t* ext, int j,
+                             const double* const* factors, const int64_t* lda,
+                             int64_t rank, double* out, int64_t ldo,
+                             void* stream);
+
 /* The same speculative solve in its two halves, so the factorization (which
  * needs only Gamma) can run on a side stream while the mode's MTTKRP
  * produces G: _factor writes the Cholesky factor into `work` and the flag

@@ -93,6 +93,8 @@ _PROTOS = {
     "cpk_solve_normal_spec_f64": (C.c_int, [_P, _P, _I64, _I64, _P, C.c_size_t, _P, _P]),
     "cpk_solve_factor_spec_f64": (C.c_int, [_P, _I64, _P, C.c_size_t, _P, _P]),
     "cpk_solve_apply_spec_f64": (C.c_int, [_P, _I64, _I64, _P, C.c_size_t, _P, _P]),
+    "cpk_dimtree_contract_f64": (C.c_int, [_P, _I64, C.c_int, C.POINTER(_I64), C.c_int, C.POINTER(_P),
+                                           C.POINTER(_I64), _I64, _P, _I64, _P]),
     "cpk_colnorms_sq_f64": (C.c_int, [_P, _I64, _I64, _I64, _P, _P]),
     "cpk_scale_columns_f64": (C.c_int, [_P, _I64, _I64, _I64, _P, _P, _P]),
     "cpk_normalize_columns_f64": (C.c_int, [_P, _I64, _I64, _I64, _P, _P, _P]),

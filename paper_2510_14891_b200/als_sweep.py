@@ -12,7 +12,15 @@ world size, so the sharded driver runs exactly the single-GPU machinery:
   is one (2 + d)-scalar readback (fit terms + flags) for the stopping rule
   (cpals.py:157).  A flag restores the sweep's snapshot and reruns it through
   the full eps ladder (cpals.py:78-89), so the trajectory is the ladder's;
-* optional CUDA-graph replay of sweeps 2.. (world 1).
+* optional CUDA-graph replay of sweeps 2.. (world 1);
+* dimension tree (`tree_split`): the modes split into a left group
+  {0..p-1} and a right group {p..d-1}; one MTTKRP over a view of the tensor
+  with the group merged into one mode gives W_G (I_G x R, the contraction
+  with every factor outside the group), and each mode of the group reads its
+  MTTKRP out of W_G (cpk_dimtree_contract_f64).  A sweep then runs 2 tensor
+  passes instead of d; the factors each mode sees are the reference's
+  (cpals.py:118-135: a group's outside factors are unchanged until the group
+  is done), so only the summation order differs.
 
 Sharding (world > 1, `Shard`): the tensor is a block of rows [lo, hi) of
 mode s, and A_s holds only those rows.  The exchange steps are the ones the
@@ -61,6 +69,52 @@ def init_factors(dims, rank: int, seed: int) -> list:
     """Philox(seed) uniform [0,1) factors in mode order (cpals.py:108-109)."""
     rng = np.random.Generator(np.random.Philox(seed))
     return [rng.random((i_k, rank)) for i_k in dims]
+
+
+# FP64 issue rate and HBM bandwidth of a B200 (MEASURED_PEAKS.json /
+# cpk_fp64_peak_probe), only their ratio matters for the tree decision
+_TREE_FLOPS = 37.1e12
+_TREE_BW = 6.5e12
+
+
+def tree_split(dims, rank: int, shard_mode: int = -1, budget_bytes: int | None = None, force: bool = False):
+    """Dimension-tree split point p (left group {0..p-1}, right {p..d-1}) for a
+    CP-ALS sweep over `dims` at `rank`, or None when no split pays.
+
+    A group of one mode is its plain MTTKRP; a group G of two or more keeps
+    W_G (prod I_G x R doubles), written once and read once per mode of G.
+    Sharded (`shard_mode` >= 0): every multi-mode group must hold the shard
+    mode, so W_G is rank-local (a group without it would need W_G summed
+    over ranks).  Among the splits whose largest W_G fits `budget_bytes`,
+    the one with the least W_G traffic; it is used when that traffic costs
+    less than half of the (d - 2) tensor passes the tree saves (`force`:
+    whenever one fits).
+    """
+    d = len(dims)
+    if d < 3:
+        return None
+    n = math.prod(dims)
+    best = None
+    for p in range(1, d):
+        big = [g for g in (range(p), range(p, d)) if len(g) >= 2]
+        if shard_mode >= 0 and any(shard_mode not in g for g in big):
+            continue
+        wbytes = [math.prod(dims[m] for m in g) * rank * 8 for g in big]
+        if budget_bytes is not None and max(wbytes) > budget_bytes:
+            continue
+        traffic = sum((1 + len(g)) * b for g, b in zip(big, wbytes))
+        if best is None or traffic < best[0]:
+            best = (traffic, p)
+    if best is None:
+        return None
+    pass_s = max(8.0 * n / _TREE_BW, 2.0 * n * rank / _TREE_FLOPS)
+    if not force and best[0] / _TREE_BW >= 0.5 * (d - 2) * pass_s:
+        return None
+    return best[1]
+
+
+def tree_groups(d: int, p: int):
+    return (tuple(range(p)), tuple(range(p, d)))
 
 
 # -------------------------------------------------------------------- comm
@@ -187,6 +241,7 @@ class DeviceBackend:
         if base.splits == 0 and base.sm_count == 0 and base.tile_volume is None:
             base = replace(base, sm_count=max(1, torch.cuda.get_device_properties(self.dev).multi_processor_count - 1))
         d = len(self.dims)
+        self._base = base
         self.plans = [mt.plan_for_mode(base, self.dims, k) for k in range(d)]
         nb = 0
         for k in range(d):
@@ -236,6 +291,58 @@ class DeviceBackend:
 
     def mttkrp(self, factors, k, out):
         mt.mttkrp_device(self.y, self.dims, factors, k, None, self.plans[k], out=out, workspace_buf=self.mt_ws)
+
+    # dimension tree ----------------------------------------------------------
+    def tree_budget(self) -> int:
+        """Bytes the tree's W_G may take: the free device memory less a margin."""
+        free = torch.cuda.mem_get_info(self.dev)[0]
+        return max(0, free - max(2 << 30, free // 4))
+
+    def setup_tree(self, p: int) -> None:
+        """Views, plans and W_G buffers for split p (als_sweep.tree_split)."""
+        d = len(self.dims)
+        self.tree_p = p
+        self.tree_groups = tree_groups(d, p)
+        self.tree_views, self.tree_w = [], []
+        nb = self.mt_ws.numel() * 8
+        for gi, grp in enumerate(self.tree_groups):
+            if len(grp) < 2:
+                self.tree_views.append(None)
+                self.tree_w.append(None)
+                continue
+            ig = math.prod(self.dims[m] for m in grp)
+            vdims, vmode = ((ig,) + self.dims[p:], 0) if gi == 0 else (self.dims[:p] + (ig,), p)
+            plan = mt.plan_for_mode(self._base, vdims, vmode)
+            n = _lib.C.c_size_t(0)
+            _lib.check(self.lib.cpk_mttkrp_workspace_bytes(len(vdims), _lib.i64_array(vdims), vmode, self.rank,
+                                                            mt._plan_request(plan), _lib.C.byref(n)),
+                       "workspace (tree view)")
+            nb = max(nb, n.value)
+            self.tree_views.append((vdims, vmode, plan))
+            self.tree_w.append(torch.empty((ig, self.rank), dtype=torch.float64, device=self.dev))
+        if nb > self.mt_ws.numel() * 8:
+            self.mt_ws = torch.empty((nb + 7) // 8, dtype=torch.float64, device=self.dev)
+
+    def tree_mttkrp(self, gi: int, factors) -> None:
+        """W_G: the MTTKRP of the view with group gi merged into one mode."""
+        vdims, vmode, plan = self.tree_views[gi]
+        p = self.tree_p
+        vf = [None] + list(factors[p:]) if gi == 0 else list(factors[:p]) + [None]
+        mt.mttkrp_device(self.y, vdims, vf, vmode, None, plan, out=self.tree_w[gi], workspace_buf=self.mt_ws)
+
+    def tree_contract(self, gi: int, factors, j: int, out) -> None:
+        """Mode j of group gi: its MTTKRP out of W_G (cpk_dimtree_contract_f64)."""
+        grp = self.tree_groups[gi]
+        w = self.tree_w[gi]
+        ptrs = _lib.ptr_array([factors[m].data_ptr() if l != j else 0 for l, m in enumerate(grp)])
+        lds = _lib.i64_array([factors[m].stride(0) for m in grp])
+        _lib.check(self.lib.cpk_dimtree_contract_f64(w.data_ptr(), w.stride(0), len(grp),
+                                                     _lib.i64_array([self.dims[m] for m in grp]), j, ptrs, lds,
+                                                     self.rank, out.data_ptr(), out.stride(0), self.sp()),
+                   "dimtree contract")
+
+    def tree_keep(self) -> list:
+        return [w for w in getattr(self, "tree_w", []) if w is not None]
 
     def factor_spec(self, gamma, info_k):
         """Cholesky of Gamma (rung 0) on the side stream, after the main
@@ -312,6 +419,7 @@ class SweepResult:
     sweep_seconds: list
     converged: bool
     rollbacks: int
+    tree_split: int | None = None
 
 
 # Capturing a sweep costs ~6 ms once and saves ~0.5 ms of host gaps per
@@ -322,13 +430,16 @@ GRAPH_MIN_ITERS = 12
 
 
 def run_sweeps(be, dims, rank: int, seed: int, max_iters: int, tol: float, norm_src, comm: Comm | None = None,
-               shard: Shard | None = None, graph: bool | None = None, pad_first: bool = False) -> SweepResult:
+               shard: Shard | None = None, graph: bool | None = None, pad_first: bool = False,
+               tree: bool | None = None) -> SweepResult:
     """CP-ALS sweeps (cpals.py:92-171) over backend `be`.
 
     `dims` are the global extents; `be.dims` the extents the kernels run on
     (this rank's block of the shard mode, and I_0 + 1 when `pad_first`: the
     extra A_0 row stays exactly zero).  `norm_src` is the unpadded local
-    tensor ||Y||^2 is summed over.
+    tensor ||Y||^2 is summed over.  `tree`: None runs the dimension tree when
+    `tree_split` finds a split that pays and fits, True whenever a split fits,
+    False never (d tensor passes per sweep, the reference's structure).
     """
     world = comm.world if comm is not None else 1
     sharded = world > 1
@@ -353,6 +464,18 @@ def run_sweeps(be, dims, rank: int, seed: int, max_iters: int, tol: float, norm_
         raise ParameterError("tensor has non-finite entries")
     if norm_y == 0.0:
         raise ParameterError("cannot fit an all-zero tensor (fit is undefined)")
+
+    tree_p = None
+    if tree is not False and hasattr(be, "setup_tree"):
+        budget = be.tree_budget()
+        tree_p = tree_split(run_dims, r, s, budget)
+        if tree and tree_p is None:
+            tree_p = tree_split(run_dims, r, s, budget, force=True)
+        if tree_p is not None:
+            be.setup_tree(tree_p)
+    elif tree:
+        raise ParameterError("this backend has no dimension-tree sweep")
+    groups = tree_groups(d, tree_p) if tree_p is not None else None
 
     init = init_factors(dims, r, seed)  # replicated Philox stream (cpals.py:108-109)
     if sharded:
@@ -393,7 +516,14 @@ def run_sweeps(be, dims, rank: int, seed: int, max_iters: int, tol: float, norm_
             if spec:
                 be.factor_spec(gamma, info[k:k + 1])
             st_mt[k][0].record()
-            be.mttkrp(factors, k, factors[k])
+            grp = None if groups is None else groups[0 if k < tree_p else 1]
+            if grp is None or len(grp) == 1:
+                be.mttkrp(factors, k, factors[k])
+            else:
+                gi = 0 if k < tree_p else 1
+                if k == grp[0]:  # W_G, from the factors outside the group
+                    be.tree_mttkrp(gi, factors)
+                be.tree_contract(gi, factors, k - grp[0], factors[k])
             st_mt[k][1].record()
             if sharded and k != s:
                 comm.allreduce_(factors[k])  # partial G_k -> G_k on every rank
@@ -442,7 +572,7 @@ def run_sweeps(be, dims, rank: int, seed: int, max_iters: int, tol: float, norm_
             spec_sweep()  # eager: one host sync per sweep
         else:
             if captured is None:
-                captured = be.capture(spec_sweep, keep=[be.mt_ws, be.solve_ws, be.sumsq_ws])
+                captured = be.capture(spec_sweep, keep=[be.mt_ws, be.solve_ws, be.sumsq_ws] + be.tree_keep())
             captured.replay()
         st_sweep[1].synchronize()
         if bool((stats_host[2:] != 0).any()):
@@ -467,4 +597,4 @@ def run_sweeps(be, dims, rank: int, seed: int, max_iters: int, tol: float, norm_
     be.synchronize()
     return SweepResult(lam=lam, factors=factors, fits=fits, mttkrp_seconds=mttkrp_seconds,
                        other_seconds=other_seconds, sweep_seconds=sweep_seconds, converged=converged,
-                       rollbacks=rollbacks)
+                       rollbacks=rollbacks, tree_split=tree_p)

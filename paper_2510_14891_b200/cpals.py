@@ -54,6 +54,10 @@ class AlsConfig:
     seed: int = 0
     plan: mt.MttkrpPlan = field(default=mt.MttkrpPlan(variant=mt.Variant.B200, mode=0))
     init: str = "random-uniform"
+    # B200 extension: dimension-tree sweep (als_sweep.tree_split) -- None:
+    # when it pays and its W_G fits; True: whenever it fits; False: d
+    # tensor passes per sweep like the reference
+    dimtree: bool | None = None
 
     def validate(self) -> None:
         if self.rank < 1:
@@ -64,6 +68,8 @@ class AlsConfig:
             raise ParameterError(f"tol must be >= 0, got {self.tol}")
         if self.init not in _INITS:
             raise ParameterError(f"unknown init {self.init!r}; choose from {_INITS}")
+        if self.dimtree not in (None, True, False):
+            raise ParameterError(f"dimtree must be None, True or False, got {self.dimtree!r}")
 
 
 @dataclass
@@ -76,6 +82,7 @@ class AlsTrace:
     total_seconds: float
     iterations: int
     converged: bool
+    tree_split: int | None = None  # B200: the dimension-tree split point, None = per-mode sweep
 
 
 class _Solver:
@@ -154,7 +161,8 @@ def cp_als(y: DenseTensor, config: AlsConfig, graph: bool | None = None) -> tupl
     y_src = y.device_data(dev)
     y_dev = y.even_device_data(dev) if pad else y_src
     be = DeviceBackend(y_dev, run_dims, r, config.plan, dev)
-    res = run_sweeps(be, dims, r, config.seed, config.max_iters, config.tol, y_src, graph=graph, pad_first=pad)
+    res = run_sweeps(be, dims, r, config.seed, config.max_iters, config.tol, y_src, graph=graph, pad_first=pad,
+                     tree=config.dimtree)
     torch.cuda.synchronize(dev)
     total = time.perf_counter() - t_start
     factors = res.factors
@@ -168,5 +176,6 @@ def cp_als(y: DenseTensor, config: AlsConfig, graph: bool | None = None) -> tupl
         total_seconds=total,
         iterations=len(res.fits),
         converged=res.converged,
+        tree_split=res.tree_split,
     )
     return model, trace

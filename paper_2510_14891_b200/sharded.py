@@ -177,7 +177,7 @@ def cp_als_sharded(y_local, part: Partition, config: AlsConfig, comm: Comm | Non
         y_src = backend.y
     shard = Shard(s, lo, hi) if comm.world > 1 else None
     res = run_sweeps(backend, dims, r, config.seed, config.max_iters, config.tol, y_src, comm=comm, shard=shard,
-                     graph=graph, pad_first=pad)
+                     graph=graph, pad_first=pad, tree=config.dimtree)
     total = time.perf_counter() - t_start
     factors = res.factors
     if pad:
@@ -188,5 +188,6 @@ def cp_als_sharded(y_local, part: Partition, config: AlsConfig, comm: Comm | Non
     trace = ShardedTrace(fits=res.fits, mttkrp_seconds=res.mttkrp_seconds, other_seconds=res.other_seconds,
                          total_seconds=total, iterations=len(res.fits), converged=res.converged,
                          sweep_seconds=res.sweep_seconds, comm_seconds=comm.seconds, comm_bytes=comm.bytes,
-                         comm_calls=comm.calls, world=comm.world, shard_mode=s, rollbacks=res.rollbacks)
+                         comm_calls=comm.calls, world=comm.world, shard_mode=s, rollbacks=res.rollbacks,
+                         tree_split=res.tree_split)
     return model, trace

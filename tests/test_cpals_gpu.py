@@ -99,7 +99,9 @@ def test_c3_ten_sweeps_match_reference(golden):
     als = golden("als")
     dims = (128, 128, 128, 128)
     y = ck.DenseTensor(dims, gen.philox_tensor(dims, 0))
-    model, tr = ck.cp_als(y, ck.AlsConfig(rank=256, tol=0.0, max_iters=10, seed=0))
+    # per-mode sweeps (four tensor passes, the reference's structure); the
+    # automatic dimension tree is pinned in test_dimtree_gpu.py
+    model, tr = ck.cp_als(y, ck.AlsConfig(rank=256, tol=0.0, max_iters=10, seed=0, dimtree=False))
     ref = als["c3/fits"]
     assert np.max(np.abs(np.asarray(tr.fits) - ref)) <= 1e-12
     # observed: max |dfit| 1e-15, lam 7.9e-12 (tools/c3_lam_drift.py); the

@@ -1,0 +1,117 @@
+"""Dimension-tree CP-ALS on the device (als_sweep.tree_split,
+cpk_dimtree_contract_f64): the in-group contraction against numpy, whole
+sweeps against the oracle's per-mode cp_als (cpals.py:92-171) and against
+the device's per-mode sweep."""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2510_14891_b200 as ck
+from conftest import rng_for
+from oracle import gen, oracle
+from paper_2510_14891_b200 import _lib
+
+pytestmark = pytest.mark.gpu
+
+
+def _contract_np(w, ext, j, fs):
+    g, r = len(ext), w.shape[1]
+    t = w.reshape(tuple(reversed(ext)) + (r,))
+    for l in range(g):
+        if l != j:
+            shape = [1] * g + [r]
+            shape[g - 1 - l] = ext[l]
+            t = t * fs[l].reshape(shape)
+    return t.sum(axis=tuple(g - 1 - l for l in range(g) if l != j))
+
+
+@pytest.mark.parametrize("ext,rank", [((7, 9), 5), ((40, 3), 33), ((3, 50), 70), ((5, 4, 6), 17),
+                                      ((3, 2, 4, 5), 64), ((128, 128), 256)])
+def test_contract_matches_numpy(ext, rank):
+    """Every group mode j, ragged rank chunks, padded leading dimensions."""
+    rng = rng_for(sum(ext) + rank)
+    lib = _lib.load()
+    rows = int(np.prod(ext))
+    ldw, lda, ldo = rank + 3, rank + 1, rank + 5
+    w = torch.from_numpy(rng.random((rows, ldw))).cuda()
+    fs = [torch.from_numpy(rng.random((n, lda))).cuda() for n in ext]
+    for j in range(len(ext)):
+        out = torch.full((ext[j], ldo), -7.0, dtype=torch.float64, device="cuda")
+        ptrs = _lib.ptr_array([f.data_ptr() if l != j else 0 for l, f in enumerate(fs)])
+        rc = lib.cpk_dimtree_contract_f64(w.data_ptr(), ldw, len(ext), _lib.i64_array(ext), j, ptrs,
+                                          _lib.i64_array([lda] * len(ext)), rank, out.data_ptr(), ldo, None)
+        assert rc == 0, _lib.load().cpk_last_error()
+        torch.cuda.synchronize()
+        got = out.cpu().numpy()
+        ref = _contract_np(w.cpu().numpy()[:, :rank], ext, j, [f.cpu().numpy()[:, :rank] for f in fs])
+        assert oracle.rel_err(got[:, :rank], ref) <= 1e-13, j
+        assert np.all(got[:, rank:] == -7.0)  # padding columns untouched
+
+
+def test_contract_rejects_bad_arguments():
+    # 3 = CPK_ERR_PARAM, 1 = CPK_ERR_SHAPE (include/cpk_b200.h)
+    lib = _lib.load()
+    ext = _lib.i64_array([4, 4])
+    ptrs = _lib.ptr_array([0, 0])
+    lds = _lib.i64_array([4, 4])
+    buf = torch.zeros(64, dtype=torch.float64, device="cuda")
+    p = buf.data_ptr()
+    assert lib.cpk_dimtree_contract_f64(p, 4, 1, ext, 0, ptrs, lds, 4, p, 4, None) == 3
+    assert lib.cpk_dimtree_contract_f64(p, 4, 2, ext, 2, ptrs, lds, 4, p, 4, None) == 3
+    assert lib.cpk_dimtree_contract_f64(p, 4, 2, ext, 0, ptrs, lds, 4, p, 4, None) == 3  # NULL A_1
+    assert lib.cpk_dimtree_contract_f64(p, 3, 2, ext, 0, _lib.ptr_array([0, p]), lds, 4, p, 4, None) \
+        == 1
+    assert lib.cpk_dimtree_contract_f64(None, 4, 2, ext, 0, ptrs, lds, 4, p, 4, None) == 3
+
+
+@pytest.mark.parametrize("dims,rank", [((40, 36, 34), 24), ((41, 30, 28), 17), ((20, 12, 16, 10), 33),
+                                       ((9, 8, 7), 4), ((12, 6, 8, 5, 6), 16), ((5, 4, 3, 6, 2, 3), 4),
+                                       ((64, 48, 40), 130)])
+def test_tree_sweeps_follow_the_oracle(dims, rank):
+    """Forced tree (3- to 6-way, odd I_0 on the padded copy, rank tails):
+    fits and weights at the oracle's per-mode trajectory."""
+    y = rng_for(sum(dims) + rank).random(int(np.prod(dims)))
+    model, tr = ck.cp_als(ck.DenseTensor(dims, y), ck.AlsConfig(rank=rank, tol=0.0, max_iters=4, seed=2,
+                                                                dimtree=True))
+    assert tr.tree_split is not None
+    ref_lam, ref_f, ref_fits = oracle.cp_als(y, dims, rank, max_iters=4, tol=0.0, seed=2)
+    assert np.max(np.abs(np.asarray(tr.fits) - np.asarray(ref_fits))) <= 1e-8
+    assert oracle.rel_err(model.weights.cpu().numpy(), ref_lam) <= 1e-6
+    assert [tuple(a.shape) for a in model.factors] == [(n, rank) for n in dims]
+
+
+def test_tree_and_per_mode_sweeps_agree():
+    """Same run with and without the tree: the sums differ in order only."""
+    dims, rank = (48, 40, 36, 20), 24
+    y = ck.DenseTensor(dims, rng_for(7).random(int(np.prod(dims))))
+    m_t, t_t = ck.cp_als(y, ck.AlsConfig(rank=rank, tol=0.0, max_iters=6, seed=1, dimtree=True))
+    m_p, t_p = ck.cp_als(y, ck.AlsConfig(rank=rank, tol=0.0, max_iters=6, seed=1, dimtree=False))
+    assert t_t.tree_split == 2 and t_p.tree_split is None
+    assert np.max(np.abs(np.asarray(t_t.fits) - np.asarray(t_p.fits))) <= 1e-12
+    for a, b in zip(m_t.factors, m_p.factors):
+        assert oracle.rel_err(a.cpu().numpy(), b.cpu().numpy()) <= 1e-10
+
+
+def test_tree_graph_replay_matches_eager_bitwise():
+    dims, rank = (30, 20, 24, 10), 12
+    y = ck.DenseTensor(dims, rng_for(3).random(int(np.prod(dims))))
+    cfg = ck.AlsConfig(rank=rank, tol=0.0, max_iters=6, seed=3, dimtree=True)
+    m_g, t_g = ck.cp_als(y, cfg, graph=True)
+    m_e, t_e = ck.cp_als(y, cfg, graph=False)
+    assert t_g.fits == t_e.fits
+    for a, b in zip(m_g.factors, m_e.factors):
+        assert np.array_equal(a.cpu().numpy(), b.cpu().numpy())
+
+
+def test_c3_tree_sweeps_match_reference(golden):
+    """BASELINE config 3 (128^4, R = 256, 10 sweeps): the automatic plan runs
+    the tree (split 2: two tensor passes per sweep instead of four) and stays
+    on the reference's trajectory."""
+    als = golden("als")
+    dims = (128, 128, 128, 128)
+    y = ck.DenseTensor(dims, gen.philox_tensor(dims, 0))
+    model, tr = ck.cp_als(y, ck.AlsConfig(rank=256, tol=0.0, max_iters=10, seed=0))
+    assert tr.tree_split == 2
+    assert np.max(np.abs(np.asarray(tr.fits) - als["c3/fits"])) <= 1e-12
+    assert oracle.rel_err(model.weights.cpu().numpy(), als["c3/lam"]) <= 1e-10

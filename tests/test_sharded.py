@@ -16,7 +16,7 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 from oracle import oracle
-from paper_2510_14891_b200 import sharded
+from paper_2510_14891_b200 import als_sweep, sharded
 from paper_2510_14891_b200.cpals import AlsConfig
 from paper_2510_14891_b200.dtensor import DenseTensor
 
@@ -109,6 +109,39 @@ class CpuOracleBackend:
         out[0] = float(lv @ h.numpy() @ lv)
         out[1] = float(np.sum((g.numpy() * lv) * a.numpy()))
 
+    # dimension tree (als_sweep.tree_split): W_G from the oracle's MTTKRP of
+    # the merged view, the in-group contraction in numpy
+    def tree_budget(self):
+        return 1 << 40
+
+    def setup_tree(self, p):
+        self.tree_p = p
+        self.tree_groups = als_sweep.tree_groups(len(self.dims), p)
+        self.tree_w = [None, None]
+
+    def tree_mttkrp(self, gi, factors):
+        p, grp = self.tree_p, self.tree_groups[gi]
+        ig = int(np.prod([self.dims[m] for m in grp]))
+        r = factors[0].shape[1]
+        fs = [f.numpy() for f in factors]
+        if gi == 0:
+            vdims, vf, k = (ig,) + self.dims[p:], [np.zeros((ig, r))] + fs[p:], 0
+        else:
+            vdims, vf, k = self.dims[:p] + (ig,), fs[:p] + [np.zeros((ig, r))], p
+        self.tree_w[gi] = oracle.mttkrp_ref(self.y.numpy(), vdims, k, vf)
+
+    def tree_contract(self, gi, factors, j, out):
+        grp = self.tree_groups[gi]
+        g, ext = len(grp), [self.dims[m] for m in grp]
+        r = out.shape[1]
+        t = self.tree_w[gi].reshape(tuple(reversed(ext)) + (r,))  # first-mode-fastest rows
+        for l, m in enumerate(grp):
+            if l != j:
+                shape = [1] * g + [r]
+                shape[g - 1 - l] = ext[l]
+                t = t * factors[m].numpy().reshape(shape)
+        out.copy_(torch.from_numpy(np.ascontiguousarray(t.sum(axis=tuple(g - 1 - l for l in range(g) if l != j)))))
+
     def readback(self, src, dst):
         dst.copy_(src)
 
@@ -122,7 +155,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, dims, rank_r, mode, iters, out_q):
+def _worker(rank, world, port, dims, rank_r, mode, iters, out_q, tree=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
@@ -131,19 +164,20 @@ def _worker(rank, world, port, dims, rank_r, mode, iters, out_q):
         part = sharded.partition_for(dims, world, mode)
         y_local = sharded.local_slab(DenseTensor(dims, data), part, rank)
         be = CpuOracleBackend(y_local, part.local_dims(rank))
-        model, tr = sharded.cp_als_sharded(y_local, part, AlsConfig(rank=rank_r, tol=0.0, max_iters=iters, seed=3),
-                                           sharded.Comm(), backend=be)
+        cfg = AlsConfig(rank=rank_r, tol=0.0, max_iters=iters, seed=3, dimtree=tree)
+        model, tr = sharded.cp_als_sharded(y_local, part, cfg, sharded.Comm(), backend=be)
         out_q.put((rank, tr.fits, [np.asarray(a) for a in model.factors], np.asarray(model.weights), tr.comm_bytes,
-                   tr.comm_calls))
+                   tr.comm_calls, tr.tree_split))
     finally:
         dist.destroy_process_group()
 
 
-def _run(world, dims, rank_r, mode, iters):
+def _run(world, dims, rank_r, mode, iters, tree=False):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, dims, rank_r, mode, iters, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, dims, rank_r, mode, iters, q, tree))
+             for r in range(world)]
     for p in procs:
         p.start()
     res = [q.get(timeout=240) for _ in procs]
@@ -164,7 +198,7 @@ def test_sharded_protocol_matches_single_process(world, dims, mode):
     lam_ref, f_ref, fits_ref = oracle.cp_als(data, dims, rank_r, max_iters=iters, tol=0.0, seed=3, mttkrp="ref")
     res = _run(world, dims, rank_r, mode, iters)
     d = len(dims)
-    for rank, fits, factors, lam, nbytes, calls in res:
+    for rank, fits, factors, lam, nbytes, calls, _ in res:
         assert np.max(np.abs(np.asarray(fits) - np.asarray(fits_ref))) <= 1e-10, rank
         assert oracle.rel_err(lam, lam_ref) <= 1e-9
         for a, b in zip(factors, f_ref):
@@ -252,3 +286,61 @@ def test_graph_replay_is_single_rank_only():
     for p in procs:
         p.join(timeout=60)
     assert res == [(0, "ParameterError"), (1, "ParameterError")]
+
+
+def test_tree_split_choices():
+    """als_sweep.tree_split: the split with the least W_G traffic that fits,
+    multi-mode groups holding the shard mode, off when it does not pay."""
+    ts = als_sweep.tree_split
+    assert ts((4096, 2048, 2048), 512) == 1  # W = I_1 I_2 x R (17 GB), not I_0 I_1 x R
+    assert ts((4096, 2048, 2048), 512, shard_mode=0) == 2  # the left group holds mode 0
+    assert ts((4096, 2048, 2048), 512, shard_mode=2) == 1
+    assert ts((128,) * 4, 256) == 2
+    assert ts((1024,) * 3, 2000) == 1
+    assert ts((4096, 2048, 2048), 512, budget_bytes=1 << 30) is None
+    assert ts((8, 9), 4) is None and ts((8, 9), 4, force=True) is None  # two modes: nothing to share
+    # R far above the other group's extents: W_G outweighs the saved pass
+    assert ts((36, 20, 28), 70) is None and ts((36, 20, 28), 70, force=True) == 1
+    for d in range(3, 8):
+        dims = (5,) * d
+        for s in range(d):
+            p = ts(dims, 3, shard_mode=s, force=True)
+            assert p is not None
+            assert all(s in g for g in als_sweep.tree_groups(d, p) if len(g) > 1)
+
+
+@pytest.mark.parametrize("dims,rank", [((9, 6, 5), 3), ((6, 5, 4, 3), 4), ((4, 3, 5, 2, 3), 2),
+                                        ((3, 4, 2, 3, 2, 3), 3)])
+def test_tree_sweep_matches_oracle(dims, rank):
+    """The dimension-tree sweep (W_G + in-group contraction) on the oracle
+    backend follows the oracle's per-mode cp_als trajectory."""
+    rng = np.random.Generator(np.random.Philox(9))
+    data = rng.random(int(np.prod(dims)))
+    be = CpuOracleBackend(data, dims)
+    res = als_sweep.run_sweeps(be, dims, rank, 3, 5, 0.0, be.y, tree=True)
+    assert res.tree_split is not None
+    lam_ref, f_ref, fits_ref = oracle.cp_als(data, dims, rank, max_iters=5, tol=0.0, seed=3, mttkrp="ref")
+    assert np.max(np.abs(np.asarray(res.fits) - np.asarray(fits_ref))) <= 1e-10
+    assert oracle.rel_err(res.lam.numpy(), lam_ref) <= 1e-9
+    for a, b in zip(res.factors, f_ref):
+        assert oracle.rel_err(a.numpy(), b) <= 1e-9
+
+
+@pytest.mark.parametrize("world,dims,mode", [(2, (9, 6, 5), 0), (3, (7, 8, 5), 2), (2, (6, 5, 4, 3), 1)])
+def test_sharded_tree_protocol_matches_single_process(world, dims, mode):
+    """Sharded dimension tree: the split keeps every W_G rank-local, the
+    collectives are the per-mode sweep's, every rank ends on the oracle
+    trajectory."""
+    rank_r, iters = 3, 5
+    data = np.random.Generator(np.random.Philox(42)).random(int(np.prod(dims)))
+    lam_ref, f_ref, fits_ref = oracle.cp_als(data, dims, rank_r, max_iters=iters, tol=0.0, seed=3, mttkrp="ref")
+    res = _run(world, dims, rank_r, mode, iters, tree=True)
+    d = len(dims)
+    for rank, fits, factors, lam, nbytes, calls, split in res:
+        assert split is not None
+        assert all(mode in g for g in als_sweep.tree_groups(d, split) if len(g) > 1)
+        assert np.max(np.abs(np.asarray(fits) - np.asarray(fits_ref))) <= 1e-10, rank
+        assert oracle.rel_err(lam, lam_ref) <= 1e-9
+        for a, b in zip(factors, f_ref):
+            assert oracle.rel_err(a, b) <= 1e-9
+        assert calls == 2 + iters * (d + 2), calls
