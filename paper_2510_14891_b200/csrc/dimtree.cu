@@ -20,6 +20,8 @@
 // 32 rank columns), 8 warps splitting the summed rows, lanes on consecutive
 // columns (256-byte coalesced rows of W_G), a fixed-order shared-memory
 // reduction (deterministic, run-to-run reproducible).
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace cpk {
@@ -31,45 +33,80 @@ struct GroupFactors {
 };
 
 constexpr int DT_WARPS = 8;
-constexpr int DT_UNROLL = 4;
+constexpr int DT_UNROLL = 8;
 
 // Two-mode group (every group of a 3- or 4-way tensor): one of J_lo / J_hi is
 // 1, so a summed row is s * stride_s + i_j * stride_j and its Khatri-Rao
-// weight is the other mode's factor row s -- no index arithmetic.
+// weight is the other mode's factor row s -- no index arithmetic.  V columns
+// per lane (V = 2: 16-byte loads, 512-byte warp rows when every row start is
+// 16-byte aligned), DT_UNROLL rows in flight per warp.
+template <int V>
 __global__ void __launch_bounds__(DT_WARPS * 32)
 dimtree_contract2_kernel(const double* __restrict__ W, int64_t ldw, const double* __restrict__ B, int64_t ldb,
                          int64_t S, int64_t stride_s, int64_t stride_j, int64_t rows_out, int64_t rank,
                          double* __restrict__ out, int64_t ldo) {
-  __shared__ double red[DT_WARPS][32];
+  using vec = typename std::conditional<V == 2, double2, double>::type;
+  __shared__ vec red[DT_WARPS][32];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int64_t chunks = (rank + 31) / 32;
+  const int64_t chunks = (rank + 32 * V - 1) / (32 * V);
   for (int64_t b = blockIdx.x; b < rows_out * chunks; b += gridDim.x) {
     const int64_t ij = b / chunks;
-    const int64_t c = (b - ij * chunks) * 32 + lane;
-    const int64_t cc = c < rank ? c : rank - 1;  // dead lanes read a live column, never write
+    const int64_t c = (b - ij * chunks) * (32 * V) + V * lane;
+    const int64_t cc = c < rank ? c : rank - V;  // dead lanes read a live column, never write
     const double* wp = W + ij * stride_j * ldw + cc;
     const double* bp = B + cc;
-    double acc = 0.0;
+    const int64_t ws = stride_s * ldw;
+    vec acc = vec{};
     int64_t s = w;
     for (; s + (DT_UNROLL - 1) * DT_WARPS < S; s += DT_UNROLL * DT_WARPS) {
-      double wv[DT_UNROLL], bv[DT_UNROLL];
+      vec wv[DT_UNROLL], bv[DT_UNROLL];
 #pragma unroll
       for (int u = 0; u < DT_UNROLL; ++u) {
         const int64_t su = s + u * DT_WARPS;
-        wv[u] = __ldg(wp + su * stride_s * ldw);
-        bv[u] = __ldg(bp + su * ldb);
+        wv[u] = __ldg(reinterpret_cast<const vec*>(wp + su * ws));
+        bv[u] = __ldg(reinterpret_cast<const vec*>(bp + su * ldb));
       }
 #pragma unroll
-      for (int u = 0; u < DT_UNROLL; ++u) acc = fma(wv[u], bv[u], acc);
+      for (int u = 0; u < DT_UNROLL; ++u) {
+        if constexpr (V == 2) {
+          acc.x = fma(wv[u].x, bv[u].x, acc.x);
+          acc.y = fma(wv[u].y, bv[u].y, acc.y);
+        } else {
+          acc = fma(wv[u], bv[u], acc);
+        }
+      }
     }
-    for (; s < S; s += DT_WARPS) acc = fma(__ldg(wp + s * stride_s * ldw), __ldg(bp + s * ldb), acc);
+    for (; s < S; s += DT_WARPS) {
+      const vec wv = __ldg(reinterpret_cast<const vec*>(wp + s * ws));
+      const vec bv = __ldg(reinterpret_cast<const vec*>(bp + s * ldb));
+      if constexpr (V == 2) {
+        acc.x = fma(wv.x, bv.x, acc.x);
+        acc.y = fma(wv.y, bv.y, acc.y);
+      } else {
+        acc = fma(wv, bv, acc);
+      }
+    }
     red[w][lane] = acc;
     __syncthreads();
     if (w == 0) {
-      double t = red[0][lane];
+      vec t = red[0][lane];
 #pragma unroll
-      for (int q = 1; q < DT_WARPS; ++q) t += red[q][lane];
-      if (c < rank) out[ij * ldo + c] = t;
+      for (int q = 1; q < DT_WARPS; ++q) {
+        if constexpr (V == 2) {
+          t.x += red[q][lane].x;
+          t.y += red[q][lane].y;
+        } else {
+          t += red[q][lane];
+        }
+      }
+      if (c < rank) {
+        if constexpr (V == 2) {
+          out[ij * ldo + c] = t.x;
+          out[ij * ldo + c + 1] = t.y;
+        } else {
+          out[ij * ldo + c] = t;
+        }
+      }
     }
     __syncthreads();
   }
@@ -148,8 +185,16 @@ extern "C" int cpk_dimtree_contract_f64(const double* W, int64_t ldw, int g, con
   if (g == 2) {
     const int o = 1 - j;  // the other mode of the pair
     const int64_t stride_s = (j == 0) ? ext[0] : 1, stride_j = (j == 0) ? 1 : ext[0];
-    dimtree_contract2_kernel<<<grid, DT_WARPS * 32, 0, st>>>(W, ldw, factors[o], lda[o], S, stride_s, stride_j,
-                                                             rows_out, rank, out, ldo);
+    const bool v2 = rank % 2 == 0 && ldw % 2 == 0 && lda[o] % 2 == 0 && (reinterpret_cast<uintptr_t>(W) & 15) == 0 &&
+                    (reinterpret_cast<uintptr_t>(factors[o]) & 15) == 0;
+    if (v2) {
+      const int64_t blocks2 = rows_out * ((rank + 63) / 64);
+      dimtree_contract2_kernel<2><<<unsigned(blocks2 < 148 * 64 ? blocks2 : 148 * 64), DT_WARPS * 32, 0, st>>>(
+          W, ldw, factors[o], lda[o], S, stride_s, stride_j, rows_out, rank, out, ldo);
+    } else {
+      dimtree_contract2_kernel<1><<<grid, DT_WARPS * 32, 0, st>>>(W, ldw, factors[o], lda[o], S, stride_s,
+                                                                  stride_j, rows_out, rank, out, ldo);
+    }
   } else {
     dimtree_contract_kernel<<<grid, DT_WARPS * 32, 0, st>>>(W, ldw, gf, g, j, j_lo, S, rows_out, rank, out, ldo);
   }

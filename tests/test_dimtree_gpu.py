@@ -27,13 +27,18 @@ def _contract_np(w, ext, j, fs):
 
 
 @pytest.mark.parametrize("ext,rank", [((7, 9), 5), ((40, 3), 33), ((3, 50), 70), ((5, 4, 6), 17),
-                                      ((3, 2, 4, 5), 64), ((128, 128), 256)])
+                                      ((3, 2, 4, 5), 64), ((128, 128), 256), ((300, 70), 96), ((2, 500), 2)])
 def test_contract_matches_numpy(ext, rank):
     """Every group mode j, ragged rank chunks, padded leading dimensions."""
     rng = rng_for(sum(ext) + rank)
     lib = _lib.load()
     rows = int(np.prod(ext))
-    ldw, lda, ldo = rank + 3, rank + 1, rank + 5
+    # odd leading dimensions (scalar lanes), and even ones (two columns per lane)
+    for ldw, lda, ldo in ((rank + 3, rank + 1, rank + 5), (rank, rank, rank), (rank + 2, rank + 4, rank + 1)):
+        _check_contract(lib, rng, ext, rank, rows, ldw, lda, ldo)
+
+
+def _check_contract(lib, rng, ext, rank, rows, ldw, lda, ldo):
     w = torch.from_numpy(rng.random((rows, ldw))).cuda()
     fs = [torch.from_numpy(rng.random((n, lda))).cuda() for n in ext]
     for j in range(len(ext)):
