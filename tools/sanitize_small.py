@@ -2,7 +2,8 @@
 racecheck / synccheck): 4-way MTTKRP (Khatri-Rao merge + o-group TMEM
 accumulation), 3-way with rank tails, the narrow 16/32-column DMMA tiles and
 the swizzled mode-0 panels, the split chain (CPK_SPLIT_CHAIN=1), the solve
-kernels (one-CTA Cholesky and the multi-CTA sweep), CP-ALS."""
+kernels (one-CTA Cholesky and the multi-CTA sweep), CP-ALS (per-mode and
+dimension-tree sweeps)."""
 import os
 import sys
 from pathlib import Path
@@ -35,6 +36,11 @@ for k in range(3):
 del os.environ["CPK_SPLIT_CHAIN"]
 y = ck.DenseTensor((20, 18, 16, 6), rng.random(20 * 18 * 16 * 6))
 ck.cp_als(y, ck.AlsConfig(rank=40, max_iters=3, tol=0.0), graph=False)
+# dimension tree: W_G views and the contraction (two-mode groups, both lane
+# widths: R even / odd; a three-mode group of a 5-way tensor)
+for dims, r in (((20, 18, 16, 6), 40), ((21, 10, 12), 33), ((6, 5, 4, 7, 3), 9)):
+    ck.cp_als(ck.DenseTensor(dims, rng.random(int(np.prod(dims)))),
+              ck.AlsConfig(rank=r, max_iters=2, tol=0.0, dimtree=True), graph=False)
 ck.cp_als(ck.DenseTensor((24, 20, 18), rng.random(24 * 20 * 18)), ck.AlsConfig(rank=300, max_iters=2, tol=0.0),
           graph=False)  # R > 256: the multi-CTA sweep solve
 os.environ["CPK_SOLVE"] = "kernel"
