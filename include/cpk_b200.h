@@ -76,11 +76,12 @@ typedef struct cpk_plan {
 #define CPK_MERGE_NONE (-1)
 #define CPK_MERGE_PREV 1
 #define CPK_MERGE_NEXT 2
-/* KR: for d >= 4, the two fastest non-k modes run as one virtual mode whose
- * factor is their Khatri-Rao product, materialized in the workspace (longer
- * o-groups for the kernel's per-group scaling).  AUTO picks it for automatic
- * plans when those modes are short and the factor small; resolve reports
- * KR, and passing it back runs the same merged problem. */
+/* KR: the two fastest non-k modes run as one virtual mode whose factor is
+ * their Khatri-Rao product, materialized in the workspace (longer o-groups
+ * for the kernel's per-group scaling).  AUTO picks it for automatic plans
+ * when those modes are short and the factor small (d >= 4: o-groups under
+ * 64 chunks; d = 3, where it is the whole product: under 16 chunks);
+ * resolve reports KR, and passing it back runs the same merged problem. */
 #define CPK_MERGE_KR 3
 /* KR_FOLD: for d >= 4 when k sits between the fastest non-k mode f and the
  * first other mode o0 (so KR cannot reshape them), the DMMA kernel reads

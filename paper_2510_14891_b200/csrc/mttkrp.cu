@@ -478,11 +478,14 @@ __global__ static void merged_contract_f64(const double* __restrict__ gp, int64_
 // are merged into one virtual mode whose factor W[i_f + I_f i_g, :] =
 // A_f[i_f, :] o A_g[i_g, :] is materialized in the workspace (c3: 128 x 128
 // rows x R = 32 MB); the (d-1)-way problem then has I_f I_g / BK chunks per
-// o-group.  The slowest mode is untouched, so streamed (landed) calls keep
-// their slab contract.  Automatic plans only; off when a small-mode merge
+// o-group.  For d = 3 the pair is both non-k modes (W is the full
+// Khatri-Rao product) and only very short o-groups merge; when g is the
+// slowest mode, streamed (landed) slabs [lo, hi) of g map to the merged
+// range [lo I_f, hi I_f).  Automatic plans only; off when a small-mode merge
 // applies or W would exceed kKrMergeBytes.
 constexpr size_t kKrMergeBytes = size_t(256) << 20;
 constexpr int64_t kKrMergeMinGroup = 64;  // merge while an o-group is shorter than this many chunks
+constexpr int64_t kKrMergeMinGroup3 = 16;  // the same for the full-product merge of a 3-way tensor
 
 struct KrMerge {
   bool on = false;
@@ -497,7 +500,22 @@ static KrMerge choose_kr_merge(const Problem& pr, const cpk_plan* plan_in) {
   const bool forced = plan_in && plan_in->merge == CPK_MERGE_KR;
   if (!forced && (!plan_is_auto(plan_in) || (plan_in && plan_in->merge != CPK_MERGE_AUTO))) return m;
   const int f = pr.f, g = f + 1;
-  if (pr.d < 4 || f < 0 || g == pr.k || g >= pr.d - 1) return m;
+  if (pr.d < 3 || f < 0 || g == pr.k || g >= pr.d) return m;
+  // g the slowest mode (every 3-way case): the merged mode becomes the
+  // slowest one, and a streamed (landed) slab [lo, hi) of g is the merged
+  // range [lo I_f, hi I_f); CPK_KR_MERGE_LAST=0 restricts merges to d >= 4
+  // with g below the slowest mode (the round-2 rule)
+  if (g == pr.d - 1 || pr.d < 4) {
+    static const bool last_ok = [] {
+      const char* e = getenv("CPK_KR_MERGE_LAST");
+      return !(e && e[0] == '0');
+    }();
+    if (!last_ok && !forced) return m;
+    // a 3-way merge is the whole Khatri-Rao product: only for very short
+    // o-groups (the dimension tree's c3 views, I_f = 128: +5 %); at I_f = 512
+    // (c2) W's extra pass loses 11-14 % (profiles/r02_kr_merge_last_ab.md)
+    if (!forced && pr.dims[f] / 16 >= kKrMergeMinGroup3) return m;
+  }
   if (!forced && pr.dims[f] / 16 >= kKrMergeMinGroup) return m;  // o-groups already long (BK >= 16)
   m.ldw = (pr.R + 1) & ~int64_t(1);
   m.w_bytes = size_t(pr.dims[f]) * size_t(pr.dims[g]) * size_t(m.ldw) * sizeof(double);
@@ -822,8 +840,9 @@ static int mttkrp_impl(const double* y, int d, const int64_t* dims, int mode, co
         ld2[j] = i == f ? km.ldw : (ld ? ld[i] : rank);
         ++j;
       }
+      const int64_t sc = (g == d - 1) ? dims[f] : 1;  // merged slowest mode: i_f + I_f i_g
       return mttkrp_impl(y, km.d2, km.dims2, km.mode2, f2, ld2, lam, rank, G, ldg, &q, workspace, inner, stream,
-                         landed_lo, landed_hi, false);
+                         ranged ? landed_lo * sc : landed_lo, ranged ? landed_hi * sc : landed_hi, false);
     }
   }
   if (pr.n_o > 3) {  // more o-modes than the kernels take: merge a pair of them (choose_order_merge)
