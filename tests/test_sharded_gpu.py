@@ -10,16 +10,17 @@ import torch
 
 import paper_2510_14891_b200 as ck
 from oracle import gen, oracle
-from paper_2510_14891_b200 import sharded
+from paper_2510_14891_b200 import als_sweep, sharded
 
 pytestmark = pytest.mark.gpu
 
 
+@pytest.mark.parametrize("tree", [None, True])
 @pytest.mark.parametrize("dims", [(40, 36, 34), (41, 10, 6, 12)])
-def test_world1_sharded_is_cp_als_bitwise(dims):
+def test_world1_sharded_is_cp_als_bitwise(dims, tree):
     rng = np.random.Generator(np.random.Philox(4))
     y = ck.DenseTensor(dims, rng.random(int(np.prod(dims))))
-    cfg = ck.AlsConfig(rank=12, tol=0.0, max_iters=5, seed=1)
+    cfg = ck.AlsConfig(rank=12, tol=0.0, max_iters=5, seed=1, dimtree=tree)
     ref, tr_ref = ck.cp_als(y, cfg, graph=False)
     part = sharded.partition_for(dims, 1)
     model, tr = sharded.cp_als_sharded(y, part, cfg)
@@ -45,7 +46,7 @@ def test_uniform_slab_matches_cpu_twin():
     assert np.array_equal(t.data.cpu().numpy(), full.ravel(order="F"))
 
 
-def _gpu_worker(rank, world, port, dims, rank_r, iters, dten, out_q):
+def _gpu_worker(rank, world, port, dims, rank_r, iters, dten, out_q, tree=None):
     import os
 
     import torch.distributed as dist
@@ -63,16 +64,17 @@ def _gpu_worker(rank, world, port, dims, rank_r, iters, dten, out_q):
             y_local = sharded.uniform_slab(part, rank, seed=7)
         comm = sharded.Comm(device=torch.device("cuda", 0))  # strict: CUDA tensors only
         model, tr = sharded.cp_als_sharded(y_local, part, ck.AlsConfig(rank=rank_r, tol=0.0, max_iters=iters,
-                                                                       seed=3), comm)
+                                                                       seed=3, dimtree=tree), comm)
         out_q.put((rank, tr.fits, [a.cpu().numpy() for a in model.factors], model.weights.cpu().numpy(),
-                   tr.comm_calls))
+                   tr.comm_calls, tr.tree_split))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,dims,dten", [(2, (40, 36, 34), False), (3, (30, 20, 8, 6), False),
-                                             (2, (33, 24, 18), True)])
-def test_multi_process_device_path_matches_single_process(tmp_path, world, dims, dten):
+@pytest.mark.parametrize("world,dims,dten,tree", [(2, (40, 36, 34), False, None), (3, (30, 20, 8, 6), False, None),
+                                                  (2, (33, 24, 18), True, None), (2, (40, 36, 34), False, True),
+                                                  (3, (30, 20, 8, 6), False, True)])
+def test_multi_process_device_path_matches_single_process(tmp_path, world, dims, dten, tree):
     """world 2-3 processes, each running the sm_100a kernels on its slab
     (generated on device, or read from a DTEN file), gloo collectives:
     every rank ends with the single-process trajectory and model."""
@@ -90,7 +92,7 @@ def test_multi_process_device_path_matches_single_process(tmp_path, world, dims,
         port = s.getsockname()[1]
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_gpu_worker, args=(r, world, port, dims, 6, 4, path, q)) for r in range(world)]
+    procs = [ctx.Process(target=_gpu_worker, args=(r, world, port, dims, 6, 4, path, q, tree)) for r in range(world)]
     for p in procs:
         p.start()
     res = sorted([q.get(timeout=300) for _ in procs], key=lambda x: x[0])
@@ -98,7 +100,11 @@ def test_multi_process_device_path_matches_single_process(tmp_path, world, dims,
         p.join(timeout=60)
         assert p.exitcode == 0
     _, tr_ref = ck.cp_als(ck.DenseTensor(dims, full), ck.AlsConfig(rank=6, tol=0.0, max_iters=4, seed=3))
-    for rank, fits, factors, lam, calls in res:
+    part = sharded.partition_for(dims, world)
+    for rank, fits, factors, lam, calls, split in res:
+        if tree:  # the dimension tree on the slabs: every multi-mode group holds the shard mode
+            assert split is not None
+            assert all(part.mode in g for g in als_sweep.tree_groups(len(dims), split) if len(g) > 1)
         assert np.max(np.abs(np.asarray(fits) - np.asarray(tr_ref.fits))) <= 1e-10, rank
         assert calls == 2 + 4 * (len(dims) + 2)
         assert [a.shape for a in factors] == [(n, 6) for n in dims]
