@@ -37,14 +37,28 @@ for p in d["rank_sweep"]["points"]:
 cp, c5 = d["cp_als"], d["cp_als_c5"]
 print("\n| CP-ALS | sec / sweep | roofline sweep | roofline / measured |")
 print("|---|---|---|---|")
-print(f"| {cp['config']} ({cp['iters']} sweeps) | {cp['sec_per_iter']:.4f} (graph replay {cp['graph_sec_per_replayed_sweep']:.4f}) | "
-      f"{cp['roofline_sec_per_iter']:.4f} | {cp['roofline_frac']:.2f} |")
+tree = " [dimension tree, split {}]".format(cp["tree_split"]) if cp.get("tree_split") else ""
+print(f"| {cp['config']} ({cp['iters']} sweeps){tree} | {cp['sec_per_iter']:.4f} (graph replay "
+      f"{cp['graph_sec_per_replayed_sweep']:.4f}) | {cp['roofline_sec_per_iter']:.4f} | {cp['roofline_frac']:.2f} |")
+if cp.get("per_mode"):
+    pm = cp["per_mode"]
+    print(f"| same, per-mode sweep (4 MTTKRPs, the reference's structure) | {pm['sec_per_iter']:.4f} (graph replay "
+          f"{pm['graph_sec_per_replayed_sweep']:.4f}) | {cp['roofline_sec_per_iter']:.4f} | "
+          f"{cp['roofline_sec_per_iter'] / pm['sec_per_iter']:.2f} |")
 if "sec_per_iter" in c5 and c5.get("sec_per_iter"):
-    print(f"| {c5['config']} ({c5['gpus']} GPU) | {c5['sec_per_iter']:.4f} | {c5['roofline_sec_per_iter']:.4f} | "
+    tree = " [dimension tree, split {}]".format(c5["tree_split"]) if c5.get("tree_split") else ""
+    print(f"| {c5['config']} ({c5['gpus']} GPU){tree} | {c5['sec_per_iter']:.4f} | {c5['roofline_sec_per_iter']:.4f} | "
           f"{c5['roofline_frac']:.2f} |")
+    if c5.get("per_mode"):
+        pm = c5["per_mode"]
+        print(f"| same, per-mode sweep (3 MTTKRPs) | {pm['sec_per_iter']:.4f} | {c5['roofline_sec_per_iter']:.4f} | "
+              f"{c5['roofline_sec_per_iter'] / pm['sec_per_iter']:.2f} |")
     for p in c5.get("projection", {}).get("points", []):
-        print(f"| c5 rank-0 sweep at P = {p['gpus']} (projection, collectives elided) | {p['rank0_sec_per_iter']:.4f} | "
-              f"{c5['roofline_sec_per_iter'] / p['gpus']:.4f} | {c5['roofline_sec_per_iter'] / p['gpus'] / p['rank0_sec_per_iter']:.2f} |")
+        roof = c5["roofline_sec_per_iter"] / p["gpus"]
+        extra = (f"; per-mode {p['per_mode_rank0_sec_per_iter']:.4f}"
+                 if p.get("per_mode_rank0_sec_per_iter") else "")
+        print(f"| c5 rank-0 sweep at P = {p['gpus']} (projection, collectives elided) | {p['rank0_sec_per_iter']:.4f}"
+              f"{extra} | {roof:.4f} | {roof / p['rank0_sec_per_iter']:.2f} |")
 print("\n| baseline | value |")
 print("|---|---|")
 print(f"| this repo, c4 device-resident | {d['value'] / 1e3:.2f} TFLOP/s |")
