@@ -322,7 +322,7 @@ def run_b200(args):
     import paper_2510_14891_b200 as ck
     from paper_2510_14891_b200 import _lib
     from paper_2510_14891_b200 import harness
-    from paper_2510_14891_b200.mttkrp import MttkrpPlan, Variant, mttkrp_device, resolve_plan
+    from paper_2510_14891_b200.mttkrp import MttkrpPlan, Variant, mttkrp_device, mttkrp_modes, resolve_plan
 
     # ---- inputs resident in HBM: this rank's slab of config 4 along SM
     # (every mode of the cube is "the longest"; the slowest one gives
@@ -410,6 +410,29 @@ def run_b200(args):
         dfma = {"engine": "tma (DFMA outer products, warp-specialized TMA)", "rank_tile": dplan["rank_tile"],
                 "per_mode_ms": dfma_mode,
                 "gflops": algo_flops(local_dims, RANK) * 3 / (sum(dfma_mode) * 1e-3) / 1e9}
+
+    # ---- the same three MTTKRPs through a dimension tree (mttkrp_modes
+    # tree=True: M_0, then W = Y x_0 A_0 (I_1 I_2 x R) once and M_1, M_2 read
+    # out of it): two tensor passes per step; not part of `value`
+    tree_leg = None
+    if args.tree_steps > 0 and world == 1:
+        ref_outs = step()
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.tree_steps + 1)]
+        outs = mttkrp_modes(y, fs, tree=True)  # warm-up
+        torch.cuda.synchronize()
+        evs[0].record()
+        for i in range(args.tree_steps):
+            outs = mttkrp_modes(y, fs, tree=True)
+            evs[i + 1].record()
+        evs[-1].synchronize()
+        t_ms = evs[0].elapsed_time(evs[-1]) / args.tree_steps
+        per_call = [evs[i].elapsed_time(evs[i + 1]) for i in range(args.tree_steps)]
+        dev_rel = max(float(torch.linalg.norm(a - b) / torch.linalg.norm(b)) for a, b in zip(outs, ref_outs))
+        tree_leg = {"what": "mttkrp_modes(tree=True): M_0 + one W_R = Y x_0 A_0 MTTKRP (16.8 GB) + 2 contractions",
+                    "ms_per_step": t_ms, "gflops": algo_flops(DIMS, RANK) * 3 / (t_ms * 1e-3) / 1e9,
+                    "max_rel_frobenius_vs_per_mode": dev_rel, "steps": args.tree_steps, "per_call_ms": per_call}
+        del outs, ref_outs
+        torch.cuda.empty_cache()
 
     total_flops = algo_flops(DIMS, RANK) * 3 * args.steps
     value = total_flops / elapsed / 1e9
@@ -652,6 +675,7 @@ def run_b200(args):
                          "north_star_roofline_ms_per_mode": roof_t * 1e3,
                          "north_star_frac": roof_t * 3 * args.steps / elapsed},
             "dfma_engine": dfma,
+            "all_modes_dimension_tree": tree_leg,
             "rank_sweep": rank_sweep,
             "gemm_baseline": gemm,
             "fp32_path": f32,
@@ -810,6 +834,7 @@ def main():
     ap.add_argument("--gemm-steps", type=int, default=2)
     ap.add_argument("--rank-sweep", type=int, default=1, help="1: add the GFLOP/s-vs-rank leg (c2 shape)")
     ap.add_argument("--f32-steps", type=int, default=2)
+    ap.add_argument("--tree-steps", type=int, default=3, help="c4 step through mttkrp_modes(tree=True)")
     ap.add_argument("--cpals-iters", type=int, default=10)
     ap.add_argument("--c5-iters", type=int, default=3)
     ap.add_argument("--c5-dims", default="4096,2048,2048", help="CP-ALS leg shape (tests shrink it)")

@@ -333,13 +333,8 @@ class DeviceBackend:
     def tree_contract(self, gi: int, factors, j: int, out) -> None:
         """Mode j of group gi: its MTTKRP out of W_G (cpk_dimtree_contract_f64)."""
         grp = self.tree_groups[gi]
-        w = self.tree_w[gi]
-        ptrs = _lib.ptr_array([factors[m].data_ptr() if l != j else 0 for l, m in enumerate(grp)])
-        lds = _lib.i64_array([factors[m].stride(0) for m in grp])
-        _lib.check(self.lib.cpk_dimtree_contract_f64(w.data_ptr(), w.stride(0), len(grp),
-                                                     _lib.i64_array([self.dims[m] for m in grp]), j, ptrs, lds,
-                                                     self.rank, out.data_ptr(), out.stride(0), self.sp()),
-                   "dimtree contract")
+        mt.dimtree_contract(self.tree_w[gi], [self.dims[m] for m in grp], j, [factors[m] for m in grp], out,
+                            self.rank)
 
     def tree_keep(self) -> list:
         return [w for w in getattr(self, "tree_w", []) if w is not None]

@@ -453,7 +453,8 @@ def _start_upload(y: DenseTensor, dev):
     return y_dev, bounds, landed
 
 
-def mttkrp_modes(tensor, factors, modes=None, weights=None, plan: MttkrpPlan | None = None) -> list:
+def mttkrp_modes(tensor, factors, modes=None, weights=None, plan: MttkrpPlan | None = None,
+                 tree: bool = False) -> list:
     """The MTTKRPs of several modes against the same factors (e.g. every mode
     of a step), returned as a list of (I_k, R) matrices of the input's kind.
 
@@ -466,6 +467,11 @@ def mttkrp_modes(tensor, factors, modes=None, weights=None, plan: MttkrpPlan | N
     launches, ~0.5 ms of tail each on one stream).  Each mode keeps its own
     plan, workspace and merge order: results are bit-identical to one
     resident call per mode.
+
+    ``tree=True`` computes the modes through a dimension tree instead
+    (_modes_tree): two tensor passes for all d modes, equal to the per-mode
+    results up to summation order (the tensor is uploaded whole first; no
+    streaming overlap).
     """
     if isinstance(factors, KruskalTensor):
         m = factors
@@ -479,6 +485,11 @@ def mttkrp_modes(tensor, factors, modes=None, weights=None, plan: MttkrpPlan | N
     for k in modes:
         _check_inputs(y, m, k)
     dev = require_cuda()
+    if tree and y.ndim >= 3 and len(set(modes)) > 2:
+        outs = _modes_tree(y.device_data(dev), y.dims, m.device_factors(dev),
+                           None if _unit_weights(m.weights) else m.device_weights(dev), modes, plan, dev)
+        host = not isinstance(y.data, torch.Tensor)
+        return [np.ascontiguousarray(g.cpu().numpy()) for g in outs] if host else outs
     stream_it = y.needs_upload(dev) and y.size * 8 >= STREAM_MIN_BYTES and y.ndim >= 2 and y.dims[-1] >= 2
     if not stream_it and y.landing is None:
         return [mttkrp(y, m, k, plan=plan) for k in modes]
@@ -515,6 +526,54 @@ def mttkrp_modes(tensor, factors, modes=None, weights=None, plan: MttkrpPlan | N
         out.record_stream(main)
     host = not isinstance(y.data, torch.Tensor)
     return [np.ascontiguousarray(g.cpu().numpy()) for g in outs] if host else outs
+
+
+def dimtree_contract(w: torch.Tensor, exts, j: int, group_factors, out: torch.Tensor, rank: int) -> None:
+    """out = mode j of a group's MTTKRP read out of W_G (cpk_dimtree_contract_f64):
+    W_G (prod(exts) x R rows, group multi-index first-mode-fastest) is the
+    MTTKRP over the modes outside the group; group_factors[l] (l != j) are
+    the group's factors (row-major, unit column stride)."""
+    ptrs = _lib.ptr_array([f.data_ptr() if l != j else 0 for l, f in enumerate(group_factors)])
+    lds = _lib.i64_array([f.stride(0) for f in group_factors])
+    _lib.check(_lib.load().cpk_dimtree_contract_f64(w.data_ptr(), w.stride(0), len(exts), _lib.i64_array(exts), j,
+                                                    ptrs, lds, rank, out.data_ptr(), out.stride(0),
+                                                    stream_ptr(out.device)), "dimtree contract")
+
+
+def _modes_tree(y_dev, dims, fac, lam, modes, plan, dev) -> list:
+    """Several modes' MTTKRPs by a dimension tree (als_sweep.tree_split): per
+    group of two or more modes one MTTKRP over the view with the group merged
+    (W_G, weights folded in), then each mode of the group out of W_G; a
+    one-mode group is its plain MTTKRP.  Two tensor passes for all modes."""
+    from .als_sweep import tree_groups, tree_split
+
+    d, rank = len(dims), int(fac[0].shape[1])
+    budget = max(0, torch.cuda.mem_get_info(dev)[0] - (2 << 30))
+    p = tree_split(dims, rank, budget_bytes=budget, force=True)
+    if p is None:
+        raise ResourceError("no dimension-tree split fits in device memory")
+    want = set(modes)
+    res = {}
+    for gi, grp in enumerate(tree_groups(d, p)):
+        ks = [k for k in grp if k in want]
+        if len(grp) == 1 or len(ks) == 1:  # a one-mode group (or one wanted mode): its plain MTTKRP
+            for k in ks:
+                pk = replace(plan, mode=k) if plan is not None else MttkrpPlan(Variant.B200, k)
+                res[k] = mttkrp_device(y_dev, dims, fac, k, lam, pk)[0]
+            continue
+        if not ks:
+            continue
+        ig = int(np.prod([dims[m] for m in grp]))
+        vdims, vmode = ((ig,) + tuple(dims[p:]), 0) if gi == 0 else (tuple(dims[:p]) + (ig,), p)
+        vf = [None] + list(fac[p:]) if gi == 0 else list(fac[:p]) + [None]
+        pv = replace(plan, mode=vmode) if plan is not None else MttkrpPlan(Variant.B200, vmode)
+        w = mttkrp_device(y_dev, vdims, vf, vmode, lam, pv)[0]
+        for k in ks:
+            out = torch.empty((dims[k], rank), dtype=torch.float64, device=dev)
+            dimtree_contract(w, [dims[m] for m in grp], k - grp[0], [fac[m] for m in grp], out, rank)
+            res[k] = out
+        del w
+    return [res[k] for k in modes]
 
 
 def _mttkrp_streamed(y: DenseTensor, fac, plan: MttkrpPlan, lam, dev):

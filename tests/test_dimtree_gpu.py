@@ -120,3 +120,26 @@ def test_c3_tree_sweeps_match_reference(golden):
     assert tr.tree_split == 2
     assert np.max(np.abs(np.asarray(tr.fits) - als["c3/fits"])) <= 1e-12
     assert oracle.rel_err(model.weights.cpu().numpy(), als["c3/lam"]) <= 1e-10
+
+
+@pytest.mark.parametrize("dims,rank,modes", [((40, 36, 34), 24, None), ((20, 12, 16, 10), 33, None),
+                                             ((12, 6, 8, 5, 6), 16, (4, 0, 2, 1)), ((41, 30, 28), 17, (2, 0, 1)),
+                                             ((20, 12, 16, 10), 8, (0, 1, 3))])
+def test_mttkrp_modes_tree_matches_per_mode(dims, rank, modes):
+    """mttkrp_modes(tree=True): every requested mode (any order, subsets,
+    weights, host or device input) at the per-mode result and the oracle."""
+    rng = rng_for(sum(dims) + rank)
+    y = rng.random(int(np.prod(dims)))
+    fs = [rng.random((n, rank)) for n in dims]
+    lam = rng.random(rank) + 0.5
+    ks = list(range(len(dims))) if modes is None else list(modes)
+    got = ck.mttkrp_modes(ck.DenseTensor(dims, y), ck.KruskalTensor(lam, fs), modes, tree=True)
+    assert all(isinstance(g, np.ndarray) for g in got)  # host in, host out
+    for k, g in zip(ks, got):
+        assert oracle.rel_err(g, oracle.mttkrp_ref(y, dims, k, fs, lam)) <= 1e-12, k
+    yd = torch.from_numpy(y).cuda()
+    fd = [torch.from_numpy(a).cuda() for a in fs]
+    got_d = ck.mttkrp_modes(yd, fd, modes, tree=True)
+    per = ck.mttkrp_modes(yd, fd, modes)
+    for a, b in zip(got_d, per):
+        assert a.is_cuda and oracle.rel_err(a.cpu().numpy(), b.cpu().numpy()) <= 1e-13

@@ -19,6 +19,7 @@ ap.add_argument("--dims", default="16384,16384")
 ap.add_argument("--mode", type=int, default=0)
 ap.add_argument("--rank", type=int, default=256)
 ap.add_argument("--reps", type=int, default=5)
+ap.add_argument("--max-ws-gb", type=float, default=8.0, help="skip plans whose split-K workspace is larger")
 a = ap.parse_args()
 dims = tuple(int(x) for x in a.dims.split(","))
 d, k, r = len(dims), a.mode, a.rank
@@ -38,6 +39,8 @@ flops = 2.0 * n * r
 def run(plan, reps):
     nb = _lib.C.c_size_t(0)
     if lib.cpk_mttkrp_workspace_bytes(d, dims_c, k, r, _lib.C.byref(plan), _lib.C.byref(nb)):
+        return None
+    if nb.value > a.max_ws_gb * 2 ** 30:
         return None
     ws = torch.empty(max(1, (nb.value + 7) // 8), dtype=torch.float64, device="cuda")
     res = _lib.CpkPlan()
