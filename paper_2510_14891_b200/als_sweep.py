@@ -117,6 +117,26 @@ def tree_groups(d: int, p: int):
     return (tuple(range(p)), tuple(range(p, d)))
 
 
+# W_G up to this size is taken without asking the driver for free memory
+# (cudaMemGetInfo costs milliseconds on a busy device)
+TREE_SMALL_BYTES = 1 << 30
+
+
+def tree_peak_bytes(dims, rank: int, p: int) -> int:
+    """The largest W_G of split p (bytes; 0 when both groups are single modes)."""
+    return max([math.prod(dims[m] for m in g) * rank * 8 for g in tree_groups(len(dims), p) if len(g) > 1] or [0])
+
+
+def choose_tree(dims, rank: int, shard_mode: int, want, budget_fn):
+    """Split point for `want` (None: when it pays, True: whenever it fits);
+    `budget_fn()` (free device bytes for W_G) is only called for large W_G."""
+    force = bool(want)
+    p = tree_split(dims, rank, shard_mode, None, force=force)
+    if p is None or tree_peak_bytes(dims, rank, p) <= TREE_SMALL_BYTES:
+        return p
+    return tree_split(dims, rank, shard_mode, budget_fn(), force=force)
+
+
 # -------------------------------------------------------------------- comm
 class Comm:
     """torch.distributed plumbing for the sharded sweep.
@@ -462,10 +482,7 @@ def run_sweeps(be, dims, rank: int, seed: int, max_iters: int, tol: float, norm_
 
     tree_p = None
     if tree is not False and hasattr(be, "setup_tree"):
-        budget = be.tree_budget()
-        tree_p = tree_split(run_dims, r, s, budget)
-        if tree and tree_p is None:
-            tree_p = tree_split(run_dims, r, s, budget, force=True)
+        tree_p = choose_tree(run_dims, r, s, tree, be.tree_budget)
         if tree_p is not None:
             be.setup_tree(tree_p)
     elif tree:

@@ -545,11 +545,10 @@ def _modes_tree(y_dev, dims, fac, lam, modes, plan, dev) -> list:
     group of two or more modes one MTTKRP over the view with the group merged
     (W_G, weights folded in), then each mode of the group out of W_G; a
     one-mode group is its plain MTTKRP.  Two tensor passes for all modes."""
-    from .als_sweep import tree_groups, tree_split
+    from .als_sweep import choose_tree, tree_groups
 
     d, rank = len(dims), int(fac[0].shape[1])
-    budget = max(0, torch.cuda.mem_get_info(dev)[0] - (2 << 30))
-    p = tree_split(dims, rank, budget_bytes=budget, force=True)
+    p = choose_tree(dims, rank, -1, True, lambda: max(0, torch.cuda.mem_get_info(dev)[0] - (2 << 30)))
     if p is None:
         raise ResourceError("no dimension-tree split fits in device memory")
     want = set(modes)
