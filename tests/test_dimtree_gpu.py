@@ -143,3 +143,26 @@ def test_mttkrp_modes_tree_matches_per_mode(dims, rank, modes):
     per = ck.mttkrp_modes(yd, fd, modes)
     for a, b in zip(got_d, per):
         assert a.is_cuda and oracle.rel_err(a.cpu().numpy(), b.cpu().numpy()) <= 1e-13
+
+
+def test_tree_rollback_on_singular_gamma_matches_per_mode():
+    """Rank above the extents (every Gamma_k of a 2x2x2 tensor at R = 5 has
+    rank <= 4): the speculative Cholesky fails inside tree sweeps (eager and
+    replayed), the sweep is rolled back and rerun through the ladder; the
+    trajectory follows the per-mode run's."""
+    from paper_2510_14891_b200 import als_sweep
+
+    dims, r = (2, 2, 2), 5
+    y = torch.from_numpy(rng_for(17).random(8)).cuda()
+    plan = ck.MttkrpPlan(ck.Variant.B200, 0)
+    ref = als_sweep.run_sweeps(als_sweep.DeviceBackend(y, dims, r, plan), dims, r, 1, 8, 0.0, y, graph=False,
+                               tree=False)
+    assert ref.rollbacks > 0
+    for graph in (False, True):
+        res = als_sweep.run_sweeps(als_sweep.DeviceBackend(y, dims, r, plan), dims, r, 1, 8, 0.0, y, graph=graph,
+                                   tree=True)
+        assert res.tree_split is not None and res.rollbacks > 0
+        assert np.all(np.isfinite(res.fits))
+        # an exact fit (residual ~0): fit = 1 - sqrt(resid)/||Y|| turns the
+        # 1e-16 summation-order difference into ~1e-8, hence 1e-6 here
+        assert np.max(np.abs(np.asarray(res.fits) - np.asarray(ref.fits))) <= 1e-6
