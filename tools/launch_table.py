@@ -1,28 +1,27 @@
-"""Per-launch table (time, DRAM bytes, GB/s) from an ncu --csv launch list
-with gpu__time_duration.sum / dram__bytes_read.sum / dram__bytes_write.sum:
-    python tools/launch_table.py gpurun_out/dt_launch_c5p_dt2.csv [--min-us 20]"""
+"""Aggregate an ncu --metrics gpu__time_duration.sum --csv launch list.
+
+    python tools/launch_table.py gpurun_out/launches.csv [--last N]
+"""
 import argparse
+import collections
 import csv
-import io
 
-SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1e-3, "us": 1, "usecond": 1, "ms": 1e3,
-         "msecond": 1e3, "nsecond": 1e-3, "s": 1e6, "second": 1e6}
-
+SCALE = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6, "ns": 1e-3, "us": 1.0, "ms": 1e3, "s": 1e6}
 ap = argparse.ArgumentParser()
 ap.add_argument("csv")
-ap.add_argument("--min-us", type=float, default=20.0)
+ap.add_argument("--last", type=int, default=0, help="only the last N launches")
 a = ap.parse_args()
-txt = open(a.csv).read()
-rows = list(csv.DictReader(io.StringIO(txt[txt.find('"ID"'):])))
-launches = {}
-for r in rows:
-    m = launches.setdefault(int(r["ID"]), {"name": r["Kernel Name"]})
-    m[r["Metric Name"]] = float(r["Metric Value"].replace(",", "")) * SCALE[r["Metric Unit"]]
-print(f"| id | kernel | us | DRAM read GB | DRAM write GB | GB/s |\n|---|---|---|---|---|---|")
-for i, m in sorted(launches.items()):
-    t = m["gpu__time_duration.sum"]
-    if t < a.min_us:
-        continue
-    rd, wr = m["dram__bytes_read.sum"] / 1e9, m["dram__bytes_write.sum"] / 1e9
-    name = m["name"].split("(")[0].replace("void ", "")
-    print(f"| {i} | `{name}` | {t:.1f} | {rd:.3f} | {wr:.3f} | {(rd + wr) * 1e9 / (t * 1e-6) / 1e9:.0f} |")
+rows = [r for r in csv.reader(open(a.csv)) if len(r) > 10]
+h = rows[0]
+ik, iv, iu = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
+ks = [(r[ik].split("(")[0][:80], float(r[iv].replace(",", "")) * SCALE[r[iu]]) for r in rows[1:]]
+if a.last:
+    ks = ks[-a.last:]
+agg = collections.defaultdict(lambda: [0, 0.0])
+for k, t in ks:
+    agg[k][0] += 1
+    agg[k][1] += t
+tot = sum(v[1] for v in agg.values())
+for k, v in sorted(agg.items(), key=lambda x: -x[1][1]):
+    print(f"{v[1]:12.1f} us {v[0]:5d} launches  {100 * v[1] / tot:5.1f}%  {k}")
+print(f"{tot:12.1f} us total, {len(ks)} launches")
