@@ -21,7 +21,12 @@ ap.add_argument("--ranks", type=int, nargs="+", default=[256, 384, 512, 1000, 20
 ap.add_argument("--paths", nargs="+", default=["kernel", "sweep", "cusolver"])
 ap.add_argument("--rows", type=int, nargs="+", default=[128, 1024, 4096])
 ap.add_argument("--reps", type=int, default=20)
+ap.add_argument("--lib", default=None, help="A/B: time this build of the library")
 a = ap.parse_args()
+if a.lib:
+    from paper_2510_14891_b200 import _lib  # noqa: E402
+
+    _lib.LIB_PATH = Path(a.lib).resolve()
 dev = torch.device("cuda", 0)
 for r in a.ranks:
     rng = np.random.Generator(np.random.Philox(r))
