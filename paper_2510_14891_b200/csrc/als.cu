@@ -247,7 +247,10 @@ __global__ void copy_regularize_kernel(const double* __restrict__ gamma, int64_t
 // factors the diagonal block in registers (lane = row, shuffles carry the
 // pivot column), the CTA solves the panel below it against that block (one
 // thread per row), and 64-thread groups apply the symmetric rank-32 update
-// to the trailing lower triangle in 32 x 32 tiles (4 x 4 per thread).  The
+// to the trailing lower triangle in 32 x 32 tiles (4 x 4 per thread), with a
+// look-ahead: the next block column's tiles first, then warp 0 factors the
+// next diagonal block while the other groups finish the trailing update (the
+// serial factorization was a third of the kernel, profiles/r02_chol_small.md).  The
 // matrix lives in the caller's workspace (L2-resident); the panel is staged
 // in shared memory for the update.  On exit the lower triangle holds L and
 // the upper triangle of each 32 x 32 diagonal block the transposed strictly
@@ -294,155 +297,199 @@ __global__ void __launch_bounds__(CHOL_THREADS, 1) chol_small_kernel(const doubl
   __syncthreads();
 
   const int nblk = (R + CB - 1) / CB;
-#pragma unroll 1
-  for (int j = 0; j < nblk; ++j) {
-    const int j0 = j * CB, bw = min(CB, R - j0);
-    const double* src = j == 0 ? gamma : L;
-    const double dshift = j == 0 ? shift : 0.0;
-    if (warp == 0) {
-      // unblocked Cholesky of the diagonal block in registers: lane = row,
-      // a[c] = A[lane][c]; every loop is unrolled, so a[] never leaves the
-      // register file, and shuffles carry the pivot column
-      double a[CB];
-      const bool in = lane < bw;
+  // unblocked Cholesky of diagonal block jb by warp 0 in registers: lane =
+  // row, a[c] = A[lane][c]; every loop is unrolled, so a[] never leaves the
+  // register file, and shuffles carry the pivot column.  Block 0 reads Gamma
+  // (+ shift), later blocks the trailing-updated L.
+  auto factor_diag = [&](int jb) {
+    const int j0 = jb * CB, bw = min(CB, R - j0);
+    const double* src = jb == 0 ? gamma : L;
+    const double dshift = jb == 0 ? shift : 0.0;
+    double a[CB];
+    const bool in = lane < bw;
+#pragma unroll
+    for (int c = 0; c < CB; ++c)
+      a[c] = (in && c <= lane) ? src[int64_t(j0 + lane) * R + j0 + c] + (c == lane ? dshift : 0.0) : 0.0;
+    int bad = 0;
+#pragma unroll
+    for (int k = 0; k < CB; ++k) {
+      if (k < bw && bad == 0) {  // warp-uniform
+        const double dkk = __shfl_sync(~0u, a[k], k);
+        if (!(dkk > 0.0)) {  // also catches NaN
+          bad = k + 1;
+        } else {
+          // potf2 scales the column by 1 / sqrt(pivot); rsqrt is one MUFU
+          // + Newton steps, shorter than sqrt then a reciprocal
+          const double rl = rsqrt(dkk);
+          a[k] = lane == k ? dkk * rl : (lane > k ? a[k] * rl : 0.0);
+          colk[lane] = a[k];  // column k, read back as broadcasts
+          __syncwarp();
+          // unpredicated: lanes < c only touch their (unused) upper entries
+#pragma unroll
+          for (int c = 1; c < CB; ++c) {  // constant trip count: unrolls fully
+            if (c <= k) continue;
+            a[c] = fma(-a[k], colk[c], a[c]);
+          }
+          __syncwarp();
+        }
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < CB; ++c) dg[lane * 33 + c] = a[c];
+    __syncwarp();
+    if (bad) {
+      if (lane == 0) fail = j0 + bad;
+    } else {
 #pragma unroll
       for (int c = 0; c < CB; ++c)
-        a[c] = (in && c <= lane) ? src[int64_t(j0 + lane) * R + j0 + c] + (c == lane ? dshift : 0.0) : 0.0;
-      int bad = 0;
-#pragma unroll
-      for (int k = 0; k < CB; ++k) {
-        if (k < bw && bad == 0) {  // warp-uniform
-          const double dkk = __shfl_sync(~0u, a[k], k);
-          if (!(dkk > 0.0)) {  // also catches NaN
-            bad = k + 1;
-          } else {
-            // potf2 scales the column by 1 / sqrt(pivot); rsqrt is one MUFU
-            // + Newton steps, shorter than sqrt then a reciprocal
-            const double rl = rsqrt(dkk);
-            a[k] = lane == k ? dkk * rl : (lane > k ? a[k] * rl : 0.0);
-            colk[lane] = a[k];  // column k, read back as broadcasts
-            __syncwarp();
-            // unpredicated: lanes < c only touch their (unused) upper entries
-#pragma unroll
-            for (int c = 1; c < CB; ++c) {  // constant trip count: unrolls fully
-              if (c <= k) continue;
-              a[c] = fma(-a[k], colk[c], a[c]);
-            }
-            __syncwarp();
-          }
-        }
-      }
-#pragma unroll
-      for (int c = 0; c < CB; ++c) dg[lane * 33 + c] = a[c];
-      __syncwarp();
-      if (bad) {
-        if (lane == 0) fail = j0 + bad;
-      } else {
-#pragma unroll
-        for (int c = 0; c < CB; ++c)
-          if (in && c <= lane) L[int64_t(j0 + lane) * R + j0 + c] = a[c];
-        rdg[lane] = lane < bw ? 1.0 / dg[lane * 33 + lane] : 0.0;
-      }
+        if (in && c <= lane) L[int64_t(j0 + lane) * R + j0 + c] = a[c];
+      rdg[lane] = lane < bw ? 1.0 / dg[lane * 33 + lane] : 0.0;
     }
-    __syncthreads();
-    if (fail) {
-      if (tid == 0) *info = fail;
-      return;
+  };
+  // the last warp inverts a factored diagonal block for the row solve: lane
+  // j = column j of L_bb^-1 (forward substitution on e_j); its strictly-lower
+  // part goes, transposed, into the unused upper triangle of the block:
+  // L[j0 + j][j0 + i] = (L_bb^-1)[i][j], i > j
+  auto invert_diag = [&](int j0, int bw) {
+    double x[CB];
+#pragma unroll
+    for (int i = 0; i < CB; ++i) {
+      double v = i == lane ? 1.0 : 0.0;
+#pragma unroll
+      for (int u = 0; u < i; ++u) v = fma(-dg[i * 33 + u], x[u], v);  // x[u] = 0 for u < lane
+      x[i] = i >= lane ? v * rdg[i] : 0.0;
     }
-    // panel rows p0..: X L_jj^T = A, solved in place in shared memory
-    const int p0 = j0 + CB, np = R - p0, npr = ((np + CB - 1) / CB) * CB;
-    for (int t0 = warp; t0 < npr; t0 += 8 * (CHOL_THREADS / 32)) {  // 8 rows in flight per warp
-      double v[8];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int t = t0 + u * (CHOL_THREADS / 32);
-        v[u] = t < np ? src[int64_t(p0 + t) * R + j0 + lane] : 0.0;
+    for (int i = 0; i < CB; ++i)
+      if (i > lane && i < bw) L[int64_t(j0 + lane) * R + j0 + i] = x[i];
+  };
+  // One copy of each unrolled helper in the code (instruction cache): the
+  // loop starts at j = -1, whose only work is factoring diagonal block 0.
+  const int grp = tid >> 6, gl = tid & 63, ty = gl >> 3, tx = gl & 7;
+  constexpr int NGRP = CHOL_THREADS / 64;
+  int p0 = 0, np = 0, nb2 = 0;
+  const double* src = gamma;
+  double dshift = 0.0;
+  // trailing lower triangle -= P P^T in 32 x 32 tiles (bi, bl), bl <= bi,
+  // one tile per 64-thread group (4 x 4 per thread)
+  auto update_tile = [&](int bi, int bl) {
+    const int r0 = bi * CB + ty * 4, c0 = bl * CB + tx * 4;
+    double acc[4][4];  // starts as the old values, loaded before the products
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int jj = 0; jj < 4; ++jj) {
+        const int rr = r0 + i, cc = c0 + jj;
+        acc[i][jj] = (rr < np && cc <= rr) ? src[int64_t(p0 + rr) * R + p0 + cc] + (rr == cc ? dshift : 0.0) : 0.0;
       }
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int t = t0 + u * (CHOL_THREADS / 32);
-        if (t < npr) pan[t * 33 + lane] = v[u];
-      }
-    }
-    __syncthreads();
-    static_assert(CHOL_KERNEL_CAP - CB <= CHOL_THREADS - 32, "one panel row per thread, last warp free");
-    if (warp == CHOL_THREADS / 32 - 1) {
-      // meanwhile the last warp inverts the diagonal block for the row
-      // solve: lane j = column j of L_bb^-1 (forward substitution on e_j);
-      // its strictly-lower part goes, transposed, into the unused upper
-      // triangle of the block: L[j0 + j][j0 + i] = (L_bb^-1)[i][j], i > j
-      double x[CB];
-#pragma unroll
-      for (int i = 0; i < CB; ++i) {
-        double v = i == lane ? 1.0 : 0.0;
-#pragma unroll
-        for (int u = 0; u < i; ++u) v = fma(-dg[i * 33 + u], x[u], v);  // x[u] = 0 for u < lane
-        x[i] = i >= lane ? v * rdg[i] : 0.0;
-      }
-#pragma unroll
-      for (int i = 0; i < CB; ++i)
-        if (i > lane && i < bw) L[int64_t(j0 + lane) * R + j0 + i] = x[i];
-    }
-    if (tid < np) {  // not a loop: the dg reads would be hoisted and spill
-      const int t = tid;
-      double x[CB];  // fully unrolled: stays in registers
-#pragma unroll
-      for (int c = 0; c < CB; ++c) x[c] = pan[t * 33 + c];
-#pragma unroll
-      for (int c = 0; c < CB; ++c) {
-        double v = x[c];
-#pragma unroll
-        for (int u = 0; u < c; ++u) v = fma(-x[u], dg[c * 33 + u], v);
-        x[c] = v * rdg[c];
-      }
-#pragma unroll
-      for (int c = 0; c < CB; ++c) pan[t * 33 + c] = x[c];
-    }
-    __syncthreads();
-    for (int idx = tid; idx < np * CB; idx += CHOL_THREADS) {
-      const int t = idx >> 5, c = idx & 31;
-      L[int64_t(p0 + t) * R + j0 + c] = pan[t * 33 + c];
-    }
-    // trailing lower triangle -= P P^T, 32 x 32 tiles
-    const int nb2 = npr / CB, ntiles = nb2 * (nb2 + 1) / 2;
-    const int grp = tid >> 6, gl = tid & 63, ty = gl >> 3, tx = gl & 7;
-    for (int tile = grp; tile < ntiles; tile += CHOL_THREADS / 64) {
-      int bi = 0, bl = tile;
-      while (bl > bi) {
-        bl -= bi + 1;
-        ++bi;
-      }
-      const int r0 = bi * CB + ty * 4, c0 = bl * CB + tx * 4;
-      double acc[4][4];  // starts as the old values, loaded before the products
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int jj = 0; jj < 4; ++jj) {
-          const int rr = r0 + i, cc = c0 + jj;
-          acc[i][jj] = (rr < np && cc <= rr) ? src[int64_t(p0 + rr) * R + p0 + cc] + (rr == cc ? dshift : 0.0) : 0.0;
-        }
 #pragma unroll 8
-      for (int u = 0; u < CB; ++u) {
-        double pr[4], pc[4];
+    for (int u = 0; u < CB; ++u) {
+      double pr[4], pc[4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          pr[i] = pan[(r0 + i) * 33 + u];
-          pc[i] = pan[(c0 + i) * 33 + u];
-        }
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-          for (int jj = 0; jj < 4; ++jj) acc[i][jj] = fma(-pr[i], pc[jj], acc[i][jj]);
+      for (int i = 0; i < 4; ++i) {
+        pr[i] = pan[(r0 + i) * 33 + u];
+        pc[i] = pan[(c0 + i) * 33 + u];
       }
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int jj = 0; jj < 4; ++jj) {
-          const int rr = r0 + i, cc = c0 + jj;
-          if (rr < np && cc <= rr) L[int64_t(p0 + rr) * R + p0 + cc] = acc[i][jj];
-        }
+        for (int jj = 0; jj < 4; ++jj) acc[i][jj] = fma(-pr[i], pc[jj], acc[i][jj]);
     }
-    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int jj = 0; jj < 4; ++jj) {
+        const int rr = r0 + i, cc = c0 + jj;
+        if (rr < np && cc <= rr) L[int64_t(p0 + rr) * R + p0 + cc] = acc[i][jj];
+      }
+  };
+  auto tri = [](int t, int& bi, int& bl) {  // t-th tile of a lower triangle, row-major
+    bi = 0;
+    bl = t;
+    while (bl > bi) {
+      bl -= bi + 1;
+      ++bi;
+    }
+  };
+#pragma unroll 1
+  for (int j = -1; j < nblk; ++j) {
+    // look-ahead when the trailing matrix has >= 4 block rows: the next block
+    // column's tiles first, then warp 0 factors the next diagonal block while
+    // groups 1.. update the rest (a shorter trailing matrix: all tiles, then
+    // the factorization; the extra barrier would cost more than it hides)
+    bool la = false;
+    if (j >= 0) {
+      const int j0 = j * CB;
+      src = j == 0 ? gamma : L;
+      dshift = j == 0 ? shift : 0.0;
+      // panel rows p0..: X L_jj^T = A, solved in place in shared memory (none
+      // for the last block: every loop below is empty)
+      p0 = j0 + CB;
+      np = max(0, R - p0);
+      const int npr = ((np + CB - 1) / CB) * CB;
+      for (int t0 = warp; t0 < npr; t0 += 8 * (CHOL_THREADS / 32)) {  // 8 rows in flight per warp
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int t = t0 + u * (CHOL_THREADS / 32);
+          v[u] = t < np ? src[int64_t(p0 + t) * R + j0 + lane] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int t = t0 + u * (CHOL_THREADS / 32);
+          if (t < npr) pan[t * 33 + lane] = v[u];
+        }
+      }
+      __syncthreads();
+      static_assert(CHOL_KERNEL_CAP - CB <= CHOL_THREADS - 32, "one panel row per thread, last warp free");
+      if (warp == CHOL_THREADS / 32 - 1) invert_diag(j0, min(CB, R - j0));  // meanwhile
+      if (tid < np) {  // not a loop: the dg reads would be hoisted and spill
+        const int t = tid;
+        double x[CB];  // fully unrolled: stays in registers
+#pragma unroll
+        for (int c = 0; c < CB; ++c) x[c] = pan[t * 33 + c];
+#pragma unroll
+        for (int c = 0; c < CB; ++c) {
+          double v = x[c];
+#pragma unroll
+          for (int u = 0; u < c; ++u) v = fma(-x[u], dg[c * 33 + u], v);
+          x[c] = v * rdg[c];
+        }
+#pragma unroll
+        for (int c = 0; c < CB; ++c) pan[t * 33 + c] = x[c];
+      }
+      __syncthreads();
+      for (int idx = tid; idx < np * CB; idx += CHOL_THREADS) {
+        const int t = idx >> 5, c = idx & 31;
+        L[int64_t(p0 + t) * R + j0 + c] = pan[t * 33 + c];
+      }
+      nb2 = npr / CB;
+      la = nb2 >= 4;
+      const int n1 = la ? nb2 : nb2 * (nb2 + 1) / 2;
+      for (int t = grp; t < n1; t += NGRP) {
+        int bi = t, bl = 0;
+        if (!la) tri(t, bi, bl);
+        update_tile(bi, bl);
+      }
+      __syncthreads();
+    }
+    if (j + 1 < nblk) {
+      if (warp == 0) {
+        factor_diag(j + 1);  // its block is trailing tile (0, 0), already updated
+      } else if (la && grp > 0) {
+        const int m = nb2 - 1, nt = m * (m + 1) / 2;  // tiles 1 <= bl <= bi
+        for (int t = grp - 1; t < nt; t += NGRP - 1) {
+          int bi, bl;
+          tri(t, bi, bl);
+          update_tile(bi + 1, bl + 1);
+        }
+      }
+      __syncthreads();
+      if (fail) {
+        if (tid == 0) *info = fail;
+        return;
+      }
+    }
   }
   if (tid == 0) *info = 0;
 }
