@@ -165,23 +165,33 @@ static int64_t n_chunks_of(const Problem& pr, int bk) {
 //    r01_exp_splits.log), so each CTA walks at most kChunksPerCta chunks.
 //  * the split-K workspace (splits x I_k x R doubles, read back once by the
 //    reduction) stays under kWorkspaceBudget.
-// Within those bounds, the first split count whose CTAs fill whole waves.
+// Within those bounds, the split count minimizing a time model in units of
+// one CTA's chunk: waves x (chunks per CTA + a fixed per-CTA cost) + the
+// merge's read of the partial copies.  Filling the last wave is not free
+// when it takes many short CTAs: the dimension tree's c3 view (16384 x 128 x
+// 128, R = 256; 256 tiles, 1024 chunks) ran 15 splits (99.8 % wave fill)
+// 3 % slower than 4 (98.8 %); the model ranks the measured plans in order
+// (profiles/r02_c3_view_plan_sweep.log).
 constexpr int64_t kChunksPerCta = 512;
 constexpr int64_t kMaxSplits = 4096;
 constexpr double kWorkspaceBudget = 2.0 * (1 << 30);
+constexpr double kCtaFixedSeconds = 5e-6;   // prologue (TMEM, barriers, pipeline fill) + epilogue store
+constexpr double kSmFp64Flops = 2.0 * 64 * 1.9e9;  // one SM's FP64 (DFMA = DMMA) rate
+constexpr double kHbmBytesPerSecond = 6.5e12;
 
-static int auto_splits(int64_t tiles, int64_t chunks, int slots, double bytes_per_split) {
+static int auto_splits(int64_t tiles, int64_t chunks, int slots, double bytes_per_split, double chunk_seconds) {
   const int64_t cap = std::max<int64_t>(1, int64_t(kWorkspaceBudget / std::max(bytes_per_split, 1.0)));
   const int64_t max_s = std::max<int64_t>(1, std::min<int64_t>({chunks / 4, kMaxSplits, cap}));
   const int64_t lo = std::min<int64_t>(max_s, std::max<int64_t>(1, ceil_div(chunks, kChunksPerCta)));
-  double best = -1.0;
+  const double fixed = kCtaFixedSeconds / chunk_seconds;
+  const double merge = 2.0 * bytes_per_split / kHbmBytesPerSecond / chunk_seconds;  // write + read back, per split
+  double best = 1e300;
   int64_t best_s = lo;
   for (int64_t s = lo; s <= max_s; ++s) {
-    const int64_t work = tiles * s;
-    const int64_t waves = ceil_div(work, slots);
-    const double eff = double(work) / double(waves * slots);
-    if (eff > best + 5e-3) {
-      best = eff;
+    const int64_t waves = ceil_div(tiles * s, slots);
+    const double cost = double(waves) * (double(ceil_div(chunks, s)) + fixed) + (s > 1 ? double(s) * merge : 0.0);
+    if (cost < best * (1 - 1e-9)) {
+      best = cost;
       best_s = s;
     }
   }
@@ -321,7 +331,15 @@ static int resolve(const Problem& pr, cpk_plan* plan) {
         per_sm = ki.fn ? ctas_per_sm(ki) : 1;
       }
       const double ldw = double((pr.R + 1) & ~int64_t(1));
-      plan->splits = auto_splits(tiles, chunks, plan->sm_count * per_sm, double(pr.Ik) * ldw * sizeof(double));
+      // one chunk of one CTA: its FP64 work at the SM's rate, or its share of
+      // the tensor tile's HBM bytes (the rank tiles split them) if larger;
+      // CTAs sharing an SM share its rate
+      const double n_rt = double(ceil_div(pr.R, plan->rank_tile));
+      const double t_flop = 2.0 * plan->block_k * bm * plan->rank_tile / kSmFp64Flops;
+      const double t_hbm = double(plan->block_k) * bm * sizeof(double) / n_rt / (kHbmBytesPerSecond / plan->sm_count);
+      const double chunk_s = std::max(t_flop, t_hbm) * per_sm;
+      plan->splits =
+          auto_splits(tiles, chunks, plan->sm_count * per_sm, double(pr.Ik) * ldw * sizeof(double), chunk_s);
     }
   }
   if (plan->splits > chunks) plan->splits = int(chunks);
