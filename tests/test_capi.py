@@ -184,3 +184,16 @@ def test_khatri_rao_merge_is_reported_sized_and_round_trips():
     # 3-way problems never fold (the fold would be the whole Khatri-Rao matrix)
     rc, p = plan((64, 64, 64), 1, 64)
     assert rc == 0 and p.merge != 4
+
+
+def test_split_count_time_model():
+    # the dimension tree's c3 view (16384 x 128 x 128, R = 256): 256 tiles of
+    # 1024 chunks; 4 splits (98.8 % wave fill) measured 3.3 % faster than the
+    # 15 (99.8 %) the first-wave-filling rule took (profiles/r02n_plan_ab.log)
+    for dims, mode in (((16384, 128, 128), 0), ((128, 128, 16384), 2)):
+        rc, p = plan(dims, mode, 256)
+        assert rc == 0 and p.rank_tile == 64 and p.block_rows == 256 and p.splits == 4, (dims, p.splits)
+    # c4 keeps its 128 splits (<= 512 chunks per CTA, 2 GiB workspace cap)
+    for mode in range(3):
+        rc, p = plan((1024, 1024, 1024), mode, 2000)
+        assert rc == 0 and p.splits == 128
