@@ -50,8 +50,8 @@ def plan(dims, mode, rank, **kw):
 
 def test_plan_resolution_fills_waves():
     # c4: 1024^3, R=2000: DMMA tile 256 x 64 -> 4 row tiles x 32 rank tiles =
-    # 128 tiles; the split count is the smallest one whose CTAs fill >= 99%
-    # of their waves
+    # 128 tiles; the split count the time model picks fills >= 99 % of its
+    # waves
     rc, p = plan((1024, 1024, 1024), 0, 2000)
     assert rc == 0
     assert p.rank_tile == 64 and p.block_rows == 256 and p.engine == 3
