@@ -138,6 +138,149 @@ static void run(const std::vector<int8_t>& A, const std::vector<int8_t>& B) {
   cudaFree(dD);
 }
 
+
+// Ozaki-shaped loop: NDIAG int32 accumulators of N columns in TMEM (one per
+// slice diagonal), PER_GROUP MMAs per o-group spread over them, then 8 drain
+// warps read every accumulator (tcgen05.ld), fold them into an FP64 running
+// sum (scale 2^-7d, times a per-column o-row product) while the MMA warp
+// waits -- no double buffering (7 x 64 columns leave no room).  The rate
+// counted is the int8 work of the MMAs; /28 it is the FP64-equivalent rate
+// of a 7-slice emulation.
+template <int N, int NDIAG, int PER_GROUP>
+__global__ void __launch_bounds__(320, 1) ozaki_sim(const int8_t* A, const int8_t* B, double* out, int groups) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  int8_t* As = reinterpret_cast<int8_t*>(smem);
+  int8_t* Bs = reinterpret_cast<int8_t*>(smem + 16384);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 16384 + N * 128);  // [0] acc full, [1] drained
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 2);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int i = tid; i < M * K; i += blockDim.x) As[swz_off(i / K, i % K)] = A[i];
+  for (int i = tid; i < N * K; i += blockDim.x) Bs[swz_off(i / K, i % K)] = B[i];
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(&bars[0])));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 8;\n" ::"r"(smem_u32(&bars[1])));
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tslot)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  const uint32_t tmem = *tslot;
+  constexpr uint32_t id = idesc_i8(M, N);
+  auto wait = [](uint64_t* b, unsigned ph) {
+    asm volatile(
+        "{\n\t.reg .pred P;\nW%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t@!P bra W%=;\n}\n" ::"r"(smem_u32(b)),
+        "r"(ph)
+        : "memory");
+  };
+  if (warp == 0) {
+    if (lane == 0) {
+      const uint64_t da0 = sdesc(As), db0 = sdesc(Bs);
+      for (int g = 0; g < groups; ++g) {
+        if (g > 0) wait(&bars[1], (g - 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+        for (int i = 0; i < PER_GROUP; ++i) {
+          const int dgl = i % NDIAG, k = (i / NDIAG) & 3;
+          const uint32_t acc = i >= NDIAG ? 1u : 0u;
+          asm volatile(
+              "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+              "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem + uint32_t(dgl * N)),
+              "l"(da0 + uint64_t(2 * k)), "l"(db0 + uint64_t(2 * k)), "r"(id), "r"(acc));
+        }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                         smem_u32(&bars[0]))
+                     : "memory");
+      }
+    }
+  } else if (warp >= 2) {
+    // 8 drain warps: lane quarter (warp & 3), column half ((warp - 2) >> 2)
+    constexpr int HALF = N / 2;
+    const int quarter = warp & 3, c_base = ((warp - 2) >> 2) * HALF;
+    const uint32_t lane_base = tmem + (uint32_t(quarter * 32) << 16);
+    double sum[HALF];
+#pragma unroll
+    for (int j = 0; j < HALF; ++j) sum[j] = 0.0;
+    for (int g = 0; g < groups; ++g) {
+      wait(&bars[0], g & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+      const double po = 1.0 + 1e-3 * g;  // stands in for the o-rows' product
+#pragma unroll
+      for (int c0 = 0; c0 < HALF; c0 += 16) {
+        double t[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) t[j] = 0.0;
+#pragma unroll
+        for (int dd = NDIAG - 1; dd >= 0; --dd) {  // smallest terms first
+          uint32_t v[16];
+          asm volatile(
+              "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+              : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+                "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+              : "r"(lane_base + uint32_t(dd * N + c_base + c0)));
+          asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+          const double sc = ldexp(1.0, -7 * dd);
+#pragma unroll
+          for (int j = 0; j < 16; ++j) t[j] = fma(double(int32_t(v[j])), sc, t[j]);
+        }
+#pragma unroll
+        for (int j = 0; j < 16; ++j) sum[c0 + j] = fma(po, t[j], sum[c0 + j]);
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+      __syncwarp();
+      if (lane == 0) asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(&bars[1]))
+                                  : "memory");
+    }
+    double acc = 0.0;
+#pragma unroll
+    for (int j = 0; j < HALF; ++j) acc += sum[j];
+    out[size_t(blockIdx.x) * 256 + (warp - 2) * 32 + lane] = acc;
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(512));
+  }
+}
+
+template <int N, int NDIAG, int PER_GROUP>
+static void run_ozaki(const std::vector<int8_t>& A, const std::vector<int8_t>& B) {
+  int8_t *dA, *dB;
+  double* dO;
+  const int blocks = 148, groups = 200;
+  cudaMalloc(&dA, A.size());
+  cudaMalloc(&dB, size_t(N) * K);
+  cudaMalloc(&dO, size_t(blocks) * 256 * 8);
+  cudaMemcpy(dA, A.data(), A.size(), cudaMemcpyHostToDevice);
+  cudaMemcpy(dB, B.data(), size_t(N) * K, cudaMemcpyHostToDevice);
+  const int smem = 16384 + N * 128 + 1024;
+  cudaFuncSetAttribute(ozaki_sim<N, NDIAG, PER_GROUP>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  ozaki_sim<N, NDIAG, PER_GROUP><<<blocks, 320, smem>>>(dA, dB, dO, 4);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0);
+  ozaki_sim<N, NDIAG, PER_GROUP><<<blocks, 320, smem>>>(dA, dB, dO, groups);
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  float ms = 0;
+  cudaEventElapsedTime(&ms, e0, e1);
+  const double ops = 2.0 * M * N * 32 * double(PER_GROUP) * groups * blocks;
+  printf("{\"ozaki_sim\": true, \"N\": %d, \"diagonals\": %d, \"mmas_per_group\": %d, \"launch\": \"%s\", "
+         "\"int8_tops\": %.1f, \"fp64_equiv_tflops_28_products\": %.1f, \"fp64_equiv_tflops_21_products\": %.1f}\n",
+         N, NDIAG, PER_GROUP, cudaGetErrorString(cudaGetLastError()), ops / (ms * 1e-3) / 1e12,
+         ops / (ms * 1e-3) / 1e12 / 28, ops / (ms * 1e-3) / 1e12 / 21);
+  cudaFree(dA);
+  cudaFree(dB);
+  cudaFree(dO);
+}
+
 int main() {
   std::vector<int8_t> A(size_t(M) * K), B(size_t(256) * K);
   srand(1);
@@ -147,5 +290,9 @@ int main() {
   run<64>(A, B);
   run<128>(A, B);
   run<256>(A, B);
+  // o-group of I_f = 1024: 28 slice products x 32 K-steps = 896 MMAs (7 slices), 21 x 32 = 672 (6 slices)
+  run_ozaki<64, 7, 896>(A, B);
+  run_ozaki<64, 6, 672>(A, B);
+  run_ozaki<64, 7, 1792>(A, B);  // I_f = 2048
   return 0;
 }
