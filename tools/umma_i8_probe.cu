@@ -185,13 +185,15 @@ __global__ void __launch_bounds__(320, 1) ozaki_sim(const int8_t* A, const int8_
       for (int g = 0; g < groups; ++g) {
         if (g > 0) wait(&bars[1], (g - 1) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-        for (int i = 0; i < PER_GROUP; ++i) {
-          const int dgl = i % NDIAG, k = (i / NDIAG) & 3;
-          const uint32_t acc = i >= NDIAG ? 1u : 0u;
-          asm volatile(
-              "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-              "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem + uint32_t(dgl * N)),
-              "l"(da0 + uint64_t(2 * k)), "l"(db0 + uint64_t(2 * k)), "r"(id), "r"(acc));
+        for (int it = 0; it < PER_GROUP / NDIAG; ++it) {  // no divisions in the issue loop
+          const int k = it & 3;
+          const uint32_t acc = it > 0 ? 1u : 0u;
+#pragma unroll
+          for (int dgl = 0; dgl < NDIAG; ++dgl)
+            asm volatile(
+                "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem + uint32_t(dgl * N)),
+                "l"(da0 + uint64_t(2 * k)), "l"(db0 + uint64_t(2 * k)), "r"(id), "r"(acc));
         }
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
                          smem_u32(&bars[0]))
@@ -294,5 +296,6 @@ int main() {
   run_ozaki<64, 7, 896>(A, B);
   run_ozaki<64, 6, 672>(A, B);
   run_ozaki<64, 7, 1792>(A, B);  // I_f = 2048
+  run_ozaki<64, 7, 3584>(A, B);  // I_f = 4096
   return 0;
 }
